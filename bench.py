@@ -1,0 +1,405 @@
+#!/usr/bin/env python
+"""bsort on B200 — benchmark (driver contract).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--quick]
+
+N=1 (default): one step = one full sort of BASELINE.json cfg3 (2^30 f32 keys, mixed
+distribution, ascending) already resident in HBM.  N>1 (torchrun, one rank per GPU, NCCL):
+one step = sort_dist of 2^30 cfg3-distributed f32 keys PER RANK (weak scaling): MSD
+histogram + all-reduce + partition + all-to-all + local sort.  Rank 0 prints ONE JSON line.
+
+Timing: CUDA events on the sorting stream around each step (device time); the input is
+restored by a device copy between steps, outside the events.  Inputs are 4 GiB per buffer,
+far larger than the 126 MB L2, so no flush is needed.  The per-kernel roofline comes from
+libbsort's own CUDA events recorded around every kernel during the same timed steps.
+--impl reference times the CPU oracle (the reference arm for this tier) on a bounded sample.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+REPO = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, REPO)
+
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+
+METRIC = "keys/sec sorted (i32/f32/u8/f64) at 1/2/4/8 B200; % of HBM/NVLink roofline"
+UNIT = "keys/s"
+N_CFG3 = 1 << 30
+
+
+def load_peaks():
+    p = os.path.join(REPO, "MEASURED_PEAKS.json")
+    try:
+        with open(p) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs, copy)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+def load_traffic(kernel: str):
+    p = os.path.join(REPO, "profiles", "traffic.json")
+    try:
+        with open(p) as f:
+            d = json.load(f)
+        return d.get(kernel)
+    except Exception:
+        return None
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                 "--format=csv,noheader,nounits", "-lms", "50"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+            time.sleep(0.3)
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *a):
+        if self.proc:
+            time.sleep(0.1)
+            self.proc.terminate()
+            try:
+                self.proc.wait(2)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            f = [x.strip() for x in ln.split(",")]
+            if len(f) < 9:
+                continue
+            try:
+                sm.append(float(f[1]))
+                mx = float(f[2])
+            except ValueError:
+                continue
+            for nm, v in zip(names, f[5:9]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": mx, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def cpu_cores_used():
+    return 1  # the oracle is single-threaded C
+
+
+def oracle_time(sample_np: np.ndarray, descending=False):
+    import oracle
+    t0 = time.perf_counter()
+    oracle.sort_native(sample_np, descending=descending)
+    return time.perf_counter() - t0
+
+
+# ------------------------------------------------------------------------------ workloads
+
+def cfg3_input(n, device, rank=0):
+    import workloads as W
+    if rank == 0:
+        return W.mixed_f32(n, W.SEEDS["cfg3"], device)
+    return W.mixed_f32(n, W.SEEDS["cfg3"], device, offset=rank * n)
+
+
+def time_steps(fn, restore, steps, stream):
+    """Per-step device time (ms) of fn() with restore() between steps, outside the events."""
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(steps)]
+    for i in range(steps):
+        restore()
+        ev[i][0].record(stream)
+        fn()
+        ev[i][1].record(stream)
+    torch.cuda.synchronize()
+    return [a.elapsed_time(b) for a, b in ev]
+
+
+def bench_single(args, B):
+    dev = torch.device("cuda:0")
+    stream = torch.cuda.current_stream(dev)
+    n = args.n or N_CFG3
+    pristine = cfg3_input(n, dev)
+    work = torch.empty_like(pristine)
+    sorter = B.Sorter(torch.float32, n, dev)
+    restore = lambda: work.copy_(pristine)  # noqa: E731
+    run = lambda: sorter(work)  # noqa: E731
+    for _ in range(args.warmup):
+        restore()
+        run()
+    torch.cuda.synchronize()
+    hbm_peak, peak_src = load_peaks()
+    launches0 = B.launch_count()
+    with ClockSampler(0) as clk:
+        torch.cuda.synchronize()
+        with B.profile() as prof:
+            times = time_steps(run, restore, args.steps, stream)
+        torch.cuda.synchronize()
+    launches = B.launch_count() - launches0
+    ms = sum(times) / len(times)
+    value = n / (ms / 1e3)
+
+    # roofline of the dominant kernel (onesweep pass): algorithmic bytes = read + write of
+    # every key once per pass: 2 * n * 4 B per launch.
+    pk = prof.get("onesweep_pass", {"ms": float("nan"), "launches": 1})
+    pass_ms = pk["ms"] / pk["launches"]
+    pass_bytes = 2 * n * 4
+    achieved = pass_bytes / (pass_ms / 1e3) / 1e9
+    # whole-sort fraction against the fixed 36 B/key model
+    sort_gbs = 36 * n / (ms / 1e3) / 1e9
+    kernel_share = {k: round(v["ms"] / sum(times), 4) for k, v in prof.items()}
+
+    # end to end: C-ABI with host buffers (H2D + sort + D2H inside the events)
+    e2e = None
+    if not args.quick or args.e2e:
+        host_pristine = pristine.cpu()
+        host = torch.empty_like(host_pristine).pin_memory()
+        e2e_steps = max(1, min(args.steps, 3))
+        times_e = []
+        for i in range(e2e_steps + 1):
+            host.copy_(host_pristine)
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+            sorter.sort_host(host, work)
+            b.record(stream)
+            torch.cuda.synchronize()
+            if i > 0:  # first one is a warm-up
+                times_e.append(a.elapsed_time(b))
+        e_ms = sum(times_e) / len(times_e)
+        e2e = {"value": n / (e_ms / 1e3), "unit": UNIT, "h2d_bytes_per_step": n * 4,
+               "d2h_bytes_per_step": n * 4, "ms_per_step": e_ms,
+               "note": "bsort_sort_host: pinned host keys -> H2D -> sort -> D2H, CUDA events"}
+        del host, host_pristine
+
+    # CPU baseline: the oracle on a bounded sample of the same workload
+    cpu = None
+    if not args.no_cpu:
+        sample_n = args.cpu_sample
+        sample = pristine[:sample_n].cpu().numpy()
+        secs = oracle_time(sample)
+        cpu = {"value": sample_n / secs, "unit": UNIT, "cores": cpu_cores_used(), "kind": "oracle",
+               "sample": f"first {sample_n} keys of the cfg3 input (same distribution), "
+                         f"single-threaded C R1 (Algorithms 1-5), {secs:.2f} s"}
+
+    extra = {}
+    if not args.quick:
+        extra = bench_extra(B, dev, stream, args)
+
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": 1, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "u32", "data": "synthetic",
+        "config": {"workload": "cfg3: n=2^30 f32 keys, half U[-1e6,1e6] + half N(0,1), 1% +-0.0, "
+                               "0.1% +-inf, no NaN, ascending, 1 GPU (BASELINE.json configs[2])",
+                   "n": n, "key": "f32", "direction": "ascending", "path": "one-sweep LSD, 4 x 8-bit passes",
+                   "l2": "inputs 4 GiB >> 126 MB L2 (no flush); input restored by D2D copy between "
+                         "steps outside the timed events", "parallelism": "single GPU"},
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
+                     "frac": achieved / hbm_peak, "traffic": load_traffic("onesweep_pass"),
+                     "kernel": "k_onesweep_pass", "algorithmic_bytes_per_launch": pass_bytes,
+                     "avg_launch_ms": pass_ms, "peak_source": peak_src,
+                     "whole_sort_36B_per_key_GBps": sort_gbs, "whole_sort_frac": sort_gbs / hbm_peak,
+                     "kernel_share_of_step": kernel_share},
+        "cpu_baseline": cpu,
+        "e2e": e2e,
+        "gpu_launches": launches,
+        "clocks": clk.summary(),
+        "step_ms": [round(t, 4) for t in times],
+    }
+    if extra:
+        line["configs"] = extra
+    return line
+
+
+def bench_extra(B, dev, stream, args):
+    """Secondary BASELINE.json configs (context; parity is in tests/)."""
+    import workloads as W
+    out = {}
+
+    def measure(name, x, desc, path_bytes_per_key, reps=5):
+        work = torch.empty_like(x)
+        s = B.Sorter(x.dtype, x.numel(), dev)
+        restore = lambda: work.copy_(x)  # noqa: E731
+        run = lambda: s(work, desc)  # noqa: E731
+        restore(); run(); torch.cuda.synchronize()  # noqa: E702
+        t = time_steps(run, restore, reps, stream)
+        ms = statistics.median(t)
+        n = x.numel()
+        hb, _ = load_peaks()
+        gbs = path_bytes_per_key * n / (ms / 1e3) / 1e9
+        out[name] = {"keys_per_s": n / (ms / 1e3), "ms": ms, "model_GBps": gbs,
+                     "model_bytes_per_key": path_bytes_per_key, "frac_of_hbm": gbs / hb}
+        del work, s
+
+    measure("cfg1_i32_2^20_asc", W.make("cfg1", dev), False, 36)
+    for dt, nm in ((torch.uint8, "u8"), (torch.int8, "i8"), (torch.int16, "i16")):
+        x = W.make("cfg2", dev, dtype=dt)
+        bpk = 2 * x.element_size()
+        measure(f"cfg2_{nm}_2^28_asc", x, False, bpk)
+        measure(f"cfg2_{nm}_2^28_desc", x, True, bpk)
+        del x
+    for layout in ("sorted", "reverse", "equal", "distinct16"):
+        x = W.make("cfg4", dev, layout=layout)
+        measure(f"cfg4_i32_2^30_{layout}", x, False, 36)
+        del x
+    for dt, nm in ((torch.int64, "i64"), (torch.float64, "f64")):
+        x = W.make("cfg5", dev, n=1 << 30, dtype=dt)
+        measure(f"cfg5_local_{nm}_2^30_1gpu", x, False, 136, reps=3)
+        del x
+    torch.cuda.empty_cache()
+    return out
+
+
+# ------------------------------------------------------------------------ multi-GPU (N>1)
+
+def bench_multi(args, B):
+    import torch.distributed as dist
+    rank, world = dist.get_rank(), dist.get_world_size()
+    local = int(os.environ.get("LOCAL_RANK", rank))
+    dev = torch.device("cuda", local)
+    torch.cuda.set_device(dev)
+    stream = torch.cuda.current_stream(dev)
+    n = args.n or N_CFG3
+    pristine = cfg3_input(n, dev, rank)
+    work = torch.empty_like(pristine)
+    restore = lambda: work.copy_(pristine)  # noqa: E731
+    run = lambda: B.sort_dist(work)  # noqa: E731
+    for _ in range(args.warmup):
+        restore()
+        run()
+    torch.cuda.synchronize()
+    dist.barrier()
+    launches0 = B.launch_count()
+    times = []
+    with ClockSampler(local) as clk:
+        for _ in range(args.steps):
+            restore()
+            torch.cuda.synchronize()
+            dist.barrier()
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+            run()
+            b.record(stream)
+            torch.cuda.synchronize()
+            times.append(a.elapsed_time(b))
+    launches = B.launch_count() - launches0
+    t = torch.tensor([sum(times)], dtype=torch.float64, device=dev)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms = t.item() / args.steps
+    total = n * world
+    if rank == 0:
+        hbm_peak, src = load_peaks()
+        line = {
+            "metric": METRIC, "value": total / (ms / 1e3), "unit": UNIT, "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "u32", "data": "synthetic",
+            "config": {"workload": f"cfg3 distribution, 2^30 f32 keys per rank x {world} ranks, "
+                                   "globally sorted shards (MSD top-16-bit split + NCCL all-to-all "
+                                   "+ local one-sweep LSD)", "n_per_rank": n,
+                       "parallelism": f"msd-a2a x{world}"},
+            "roofline": {"bound": "hbm", "achieved": None, "peak": hbm_peak, "unit": "GB/s",
+                         "frac": None, "traffic": None, "peak_source": src,
+                         "note": "per-kernel roofline is reported by the N=1 run"},
+            "cpu_baseline": None,
+            "e2e": None,
+            "gpu_launches": launches,
+            "clocks": clk.summary(),
+        }
+        print(json.dumps(line), flush=True)
+
+
+# ------------------------------------------------------------------------ reference arm
+
+def bench_reference(args):
+    """The CPU oracle timed on the box's host cores, on a bounded sample of the workload."""
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    import workloads as W
+    sample_n = args.ref_sample
+    x = W.mixed_f32(sample_n, W.SEEDS["cfg3"], "cpu").numpy()
+    for _ in range(args.warmup):
+        oracle_time(x)
+    secs = [oracle_time(x) for _ in range(args.steps)]
+    s = sum(secs) / len(secs)
+    value = sample_n / s
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": s * 1e3, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "u32", "data": "synthetic",
+        "config": {"workload": "cfg3: f32 keys, half U[-1e6,1e6] + half N(0,1), 1% +-0.0, 0.1% +-inf, "
+                               "ascending (bounded sample of the same distribution)",
+                   "n": sample_n, "parallelism": "single CPU thread"},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": 1, "kind": "oracle",
+                         "sample": f"{sample_n} keys of the cfg3 distribution (CPU-generated, same recipe)"},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--n", type=int, default=0, help="override keys (per rank)")
+    ap.add_argument("--quick", action="store_true", help="skip secondary configs and e2e")
+    ap.add_argument("--e2e", action="store_true", help="with --quick: still measure e2e")
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--cpu-sample", type=int, default=1 << 25)
+    ap.add_argument("--ref-sample", type=int, default=1 << 22)
+    args = ap.parse_args()
+    if args.warmup < 3 and args.impl == "ours":
+        args.warmup = 3
+
+    if args.impl == "reference":
+        bench_reference(args)
+        return
+
+    import paper_2603_08929_b200 as B
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl")
+        try:
+            bench_multi(args, B)
+        finally:
+            dist.destroy_process_group()
+        return
+    print(json.dumps(bench_single(args, B)), flush=True)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,155 @@
+/*
+ * bsort.h — C ABI of the B200-native bsort hot path (arxiv 2603.08929).
+ *
+ * What is computed.  bsort_sort() puts n keys of one of ten machine types into the order the
+ * paper defines (problem statement PAPER P:27 "a monotonically non-decreasing or
+ * non-increasing sequence"): numeric order for unsigned and two's-complement keys
+ * (Algorithms 2-3) and, for IEEE-754 keys, sign -> exponent -> mantissa order with
+ * negatives inverted (Algorithms 4-5 and Theorems 2-3), which places
+ * -NaN(larger payload first) < -inf < ... < -0 < +0 < ... < +inf < +NaN(larger payload last)
+ * (P:609-617).  Descending is exactly the reverse.  The order is a total order on bit
+ * patterns, so the output is unique and compared bit-for-bit (no float arithmetic on keys).
+ *
+ * How (not part of the contract): an order-preserving key transform fused into every kernel;
+ * 32/64-bit keys by a one-sweep LSD radix sort (8-bit digits); 8/16-bit keys by one counting
+ * pass.  See DESIGN.md.
+ *
+ * Conventions for every entry point:
+ *  - All sizes are 64-bit.  `stream` is a cudaStream_t passed as void* (NULL = legacy default
+ *    stream).  Work is enqueued on `stream`; calls return after enqueue (no host sync) unless
+ *    stated otherwise.  Asynchronous kernel faults surface at the caller's next sync.
+ *  - Device pointers must be device-accessible and aligned to the element size.  No other
+ *    alignment is required.
+ *  - Argument errors return before anything is enqueued and leave all buffers untouched.
+ *  - The library keeps no hidden state besides a device-property cache, the launch counter and
+ *    the optional profiler.  Concurrent calls on different streams with distinct workspaces
+ *    are safe.
+ *  - On BSORT_ERROR_CUDA, bsort_last_cuda_error() returns the raw cudaError_t (thread-local).
+ */
+#ifndef BSORT_H
+#define BSORT_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* Key types: Table II word sizes plus the unsigned variants. Values are ABI. */
+typedef enum {
+  BSORT_U8 = 0,
+  BSORT_I8 = 1,
+  BSORT_U16 = 2,
+  BSORT_I16 = 3,
+  BSORT_U32 = 4,
+  BSORT_I32 = 5,
+  BSORT_F32 = 6,
+  BSORT_U64 = 7,
+  BSORT_I64 = 8,
+  BSORT_F64 = 9
+} bsort_dtype_t;
+
+/* Sort direction: Algorithm 1's boolean `asc`. */
+typedef enum { BSORT_ASCENDING = 0, BSORT_DESCENDING = 1 } bsort_direction_t;
+
+typedef enum {
+  BSORT_SUCCESS = 0,
+  BSORT_ERROR_INVALID_ARGUMENT = 1,   /* NULL/misaligned pointer, bad enum, bad nranks/cuts  */
+  BSORT_ERROR_UNSUPPORTED_DTYPE = 2,  /* dtype not valid for this entry point               */
+  BSORT_ERROR_OUT_OF_MEMORY = 3,      /* cudaMallocAsync of the internal workspace failed    */
+  BSORT_ERROR_WORKSPACE_TOO_SMALL = 4,/* workspace_bytes < the *_workspace_bytes() figure    */
+  BSORT_ERROR_CUDA = 5                /* a CUDA runtime call or launch failed                */
+} bsort_status_t;
+
+/* ----------------------------------------------------------------------- single GPU */
+
+/* Bytes of scratch device memory bsort_sort_ws() needs for (dtype, n) on the CURRENT device.
+ * 0 for n <= 1.  32/64-bit keys: n*sizeof(key) ping-pong buffer + histograms + look-back
+ * descriptors; 8/16-bit keys: histogram only (the counting path is in place). */
+size_t bsort_workspace_bytes(bsort_dtype_t dtype, uint64_t n);
+
+/* Sort `n` keys at `dev_keys` in place.  Scratch is allocated with cudaMallocAsync on
+ * `stream` and released with cudaFreeAsync on the same stream. */
+bsort_status_t bsort_sort(bsort_dtype_t dtype, void* dev_keys, uint64_t n,
+                          bsort_direction_t direction, void* stream);
+
+/* As bsort_sort(), with caller-owned scratch: `workspace` (device, 256-byte aligned) of at
+ * least bsort_workspace_bytes(dtype, n) bytes.  The workspace must not be used by anything
+ * else until the enqueued work completes. */
+bsort_status_t bsort_sort_ws(bsort_dtype_t dtype, void* dev_keys, uint64_t n,
+                             bsort_direction_t direction, void* workspace,
+                             size_t workspace_bytes, void* stream);
+
+/* End-to-end form with HOST keys: enqueues host->device copy of `host_keys` into `dev_keys`
+ * (n keys, caller-owned), the sort, and the device->host copy back into `host_keys`.
+ * `host_keys` should be pinned (cudaHostAlloc / torch pin_memory) for the copies to be
+ * asynchronous; the caller synchronises `stream` before reading `host_keys`. */
+bsort_status_t bsort_sort_host(bsort_dtype_t dtype, void* host_keys, uint64_t n,
+                               bsort_direction_t direction, void* dev_keys, void* workspace,
+                               size_t workspace_bytes, void* stream);
+
+/* ------------------------------------------------------ multi-GPU building blocks (MSD)
+ * The distributed sort (BASELINE.json cfg5) is an MSD range partition on the top 16 bits of
+ * the transformed key (the paper's sign -> exponent -> mantissa hierarchy, makes
+ * the top bits of the key the most significant), one key exchange, and a local bsort_sort.
+ * The collectives themselves (all-reduce of the histogram, all-to-all of counts and keys)
+ * are issued by the caller over its process group (paper_2603_08929_b200.sort_dist does it
+ * with torch.distributed / NCCL); these calls are the compute steps around them. */
+
+#define BSORT_DIST_BINS 65536
+#define BSORT_DIST_MAX_RANKS 64
+
+/* dev_hist[b] (uint64, BSORT_DIST_BINS entries, overwritten) = number of the n keys at
+ * dev_keys whose transformed key (direction folded in) has top-16-bit value b.
+ * 32/64-bit dtypes only. */
+bsort_status_t bsort_dist_top_hist(bsort_dtype_t dtype, const void* dev_keys, uint64_t n,
+                                   bsort_direction_t direction, uint64_t* dev_hist,
+                                   void* stream);
+
+/* HOST function (no GPU).  From the global histogram (host, BSORT_DIST_BINS entries) pick
+ * cuts[0..nranks] (host): cuts[0] = 0, cuts[nranks] = BSORT_DIST_BINS and, for 0 < r < nranks,
+ * cuts[r] = the smallest bin b with sum(hist[0..b)) >= floor(r * total / nranks).  Rank r owns
+ * bins [cuts[r], cuts[r+1]).  cuts is non-decreasing. */
+bsort_status_t bsort_dist_splitters(const uint64_t* host_global_hist, int nranks,
+                                    uint32_t* host_cuts);
+
+/* HOST function.  send_counts[q] (host, nranks entries) = sum of local_hist over q's bins. */
+bsort_status_t bsort_dist_send_counts(const uint64_t* host_local_hist, const uint32_t* host_cuts,
+                                      int nranks, uint64_t* host_send_counts);
+
+size_t bsort_dist_partition_workspace_bytes(bsort_dtype_t dtype, uint64_t n, int nranks);
+
+/* Stable partition of the n keys at dev_in into dev_out (n keys, distinct from dev_in),
+ * grouped by destination rank q = the rank owning the key's top-16-bit bin under host_cuts
+ * (nranks+1 entries).  host_send_counts (nranks entries, from bsort_dist_send_counts on this
+ * rank's histogram, summing to n) fixes the bucket starts: bucket q begins at
+ * sum(send_counts[0..q)).  Keys keep their raw bits; within a bucket the input order is kept. */
+bsort_status_t bsort_dist_partition(bsort_dtype_t dtype, const void* dev_in, uint64_t n,
+                                    bsort_direction_t direction, const uint32_t* host_cuts,
+                                    const uint64_t* host_send_counts, int nranks, void* dev_out,
+                                    void* workspace, size_t workspace_bytes, void* stream);
+
+/* ----------------------------------------------------------------------- diagnostics */
+
+const char* bsort_status_string(bsort_status_t status);
+int bsort_last_cuda_error(void);          /* raw cudaError_t of the last failure (thread-local) */
+const char* bsort_version(void);
+
+/* Total number of kernels this library has launched since it was loaded (all threads). */
+uint64_t bsort_launch_count(void);
+
+/* Optional per-kernel timing with CUDA events recorded on the launching stream around every
+ * kernel this library launches.  bsort_profile_enable(1) clears and starts recording,
+ * bsort_profile_enable(0) stops.  bsort_profile_read() synchronises the recorded events and
+ * fills, per kernel kind (BSORT_PROF_KINDS entries), the summed milliseconds and launch count;
+ * returns the number of kinds.  Kind names: bsort_profile_kind_name(). */
+#define BSORT_PROF_KINDS 12
+void bsort_profile_enable(int on);
+int bsort_profile_read(double* ms_per_kind, uint64_t* launches_per_kind);
+const char* bsort_profile_kind_name(int kind);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* BSORT_H */

@@ -1,0 +1,212 @@
+"""bsort on B200: the hot path of arxiv 2603.08929 as sm_100a CUDA behind a C ABI.
+
+Thin Python layer over ``include/bsort.h`` (see ``_lib.py``).  PyTorch supplies device memory
+(the caching allocator owns every workspace), the current CUDA stream and, for the multi-GPU
+path, the process group.  All sorting work runs in ``libbsort.so``.
+
+Public API
+----------
+``sort_(t, descending=False)``        in-place sort of a contiguous CUDA tensor
+``sort(t, descending=False)``         sorted copy
+``Sorter(dtype, n, device)``          reusable workspace for repeated sorts (bench / serving)
+``sort_dist(t, group=None, ...)``     globally sorted shards over a process group (MSD + a2a)
+``profile()``                         per-kernel CUDA-event timing context manager
+"""
+from __future__ import annotations
+
+import contextlib
+import ctypes
+
+import numpy as np
+import torch
+
+from . import _lib
+from ._lib import BsortError, check, lib
+
+__all__ = ["sort_", "sort", "Sorter", "sort_host", "sort_dist", "dtype_code", "workspace_bytes",
+           "top_hist", "splitters", "send_counts", "partition", "profile", "launch_count",
+           "BsortError", "version"]
+
+_TORCH_CODES = {
+    torch.uint8: _lib.U8, torch.int8: _lib.I8, torch.uint16: _lib.U16, torch.int16: _lib.I16,
+    torch.uint32: _lib.U32, torch.int32: _lib.I32, torch.float32: _lib.F32,
+    torch.uint64: _lib.U64, torch.int64: _lib.I64, torch.float64: _lib.F64,
+}
+
+
+def version() -> str:
+    return lib.bsort_version().decode()
+
+
+def launch_count() -> int:
+    """Kernels launched by libbsort.so since it was loaded."""
+    return int(lib.bsort_launch_count())
+
+
+def dtype_code(dtype: torch.dtype) -> int:
+    try:
+        return _TORCH_CODES[dtype]
+    except KeyError:
+        raise TypeError(f"bsort: unsupported dtype {dtype}") from None
+
+
+def workspace_bytes(dtype: torch.dtype, n: int) -> int:
+    return int(lib.bsort_workspace_bytes(dtype_code(dtype), n))
+
+
+def _stream_ptr(device) -> ctypes.c_void_p:
+    return ctypes.c_void_p(torch.cuda.current_stream(device).cuda_stream)
+
+
+def _check_tensor(t: torch.Tensor):
+    if not isinstance(t, torch.Tensor) or not t.is_cuda:
+        raise TypeError("bsort: expected a CUDA tensor")
+    if not t.is_contiguous():
+        raise ValueError("bsort: tensor must be contiguous")
+
+
+def _workspace(nbytes: int, device) -> torch.Tensor:
+    # 256-byte alignment is guaranteed by the caching allocator (512-byte blocks).
+    return torch.empty(max(nbytes, 1), dtype=torch.uint8, device=device)
+
+
+def sort_(t: torch.Tensor, descending: bool = False) -> torch.Tensor:
+    """Sort ``t`` in place in the paper's order (bit-exact; -0 < +0, NaNs at the ends)."""
+    _check_tensor(t)
+    code = dtype_code(t.dtype)
+    n = t.numel()
+    if n <= 1:
+        return t
+    wsb = int(lib.bsort_workspace_bytes(code, n))
+    ws = _workspace(wsb, t.device)
+    check(lib.bsort_sort_ws(code, ctypes.c_void_p(t.data_ptr()), n, int(bool(descending)),
+                            ctypes.c_void_p(ws.data_ptr()), wsb, _stream_ptr(t.device)),
+          "bsort_sort_ws")
+    return t
+
+
+def sort(t: torch.Tensor, descending: bool = False) -> torch.Tensor:
+    return sort_(t.clone(), descending)
+
+
+class Sorter:
+    """Holds a workspace for repeated sorts of up to ``n`` keys of one dtype."""
+
+    def __init__(self, dtype: torch.dtype, n: int, device="cuda"):
+        self.dtype = dtype
+        self.code = dtype_code(dtype)
+        self.n = int(n)
+        self.device = torch.device(device)
+        self.ws_bytes = int(lib.bsort_workspace_bytes(self.code, self.n))
+        self.ws = _workspace(self.ws_bytes, self.device)
+
+    def __call__(self, t: torch.Tensor, descending: bool = False) -> torch.Tensor:
+        _check_tensor(t)
+        if t.dtype != self.dtype or t.numel() > self.n:
+            raise ValueError("Sorter: dtype mismatch or tensor larger than the workspace")
+        check(lib.bsort_sort_ws(self.code, ctypes.c_void_p(t.data_ptr()), t.numel(),
+                                int(bool(descending)), ctypes.c_void_p(self.ws.data_ptr()),
+                                self.ws_bytes, _stream_ptr(t.device)), "bsort_sort_ws")
+        return t
+
+    def sort_host(self, host: torch.Tensor, dev_buf: torch.Tensor, descending: bool = False):
+        """Enqueue H2D(host -> dev_buf), sort, D2H(dev_buf -> host) on the current stream."""
+        if host.is_cuda or not host.is_contiguous() or host.dtype != self.dtype:
+            raise ValueError("sort_host: need a contiguous host tensor of the Sorter dtype")
+        _check_tensor(dev_buf)
+        if dev_buf.numel() < host.numel() or host.numel() > self.n:
+            raise ValueError("sort_host: device buffer / workspace too small")
+        check(lib.bsort_sort_host(self.code, ctypes.c_void_p(host.data_ptr()), host.numel(),
+                                  int(bool(descending)), ctypes.c_void_p(dev_buf.data_ptr()),
+                                  ctypes.c_void_p(self.ws.data_ptr()), self.ws_bytes,
+                                  _stream_ptr(dev_buf.device)), "bsort_sort_host")
+        return host
+
+
+def sort_host(host: torch.Tensor, descending: bool = False, device="cuda") -> torch.Tensor:
+    """Sort a (preferably pinned) host tensor through the GPU; returns after completion."""
+    s = Sorter(host.dtype, host.numel(), device)
+    buf = torch.empty(max(host.numel(), 1), dtype=host.dtype, device=device)
+    s.sort_host(host, buf, descending)
+    torch.cuda.current_stream(torch.device(device)).synchronize()
+    return host
+
+
+# ---------------------------------------------------------------- MSD building blocks
+
+def top_hist(t: torch.Tensor, descending: bool = False) -> torch.Tensor:
+    """uint64[65536] device histogram of the top 16 bits of the transformed keys."""
+    _check_tensor(t)
+    h = torch.empty(_lib.DIST_BINS, dtype=torch.uint64, device=t.device)
+    check(lib.bsort_dist_top_hist(dtype_code(t.dtype), ctypes.c_void_p(t.data_ptr()), t.numel(),
+                                  int(bool(descending)), ctypes.c_void_p(h.data_ptr()),
+                                  _stream_ptr(t.device)), "bsort_dist_top_hist")
+    return h
+
+
+def _u64p(a: np.ndarray):
+    return a.ctypes.data_as(ctypes.POINTER(ctypes.c_uint64))
+
+
+def _u32p(a: np.ndarray):
+    return a.ctypes.data_as(ctypes.POINTER(ctypes.c_uint32))
+
+
+def splitters(global_hist: np.ndarray, nranks: int) -> np.ndarray:
+    """Host: cuts[0..nranks] (uint32) from the global histogram (see bsort.h)."""
+    h = np.ascontiguousarray(global_hist, dtype=np.uint64)
+    if h.size != _lib.DIST_BINS:
+        raise ValueError("histogram must have 65536 bins")
+    cuts = np.zeros(nranks + 1, dtype=np.uint32)
+    check(lib.bsort_dist_splitters(_u64p(h), nranks, _u32p(cuts)), "bsort_dist_splitters")
+    return cuts
+
+
+def send_counts(local_hist: np.ndarray, cuts: np.ndarray) -> np.ndarray:
+    h = np.ascontiguousarray(local_hist, dtype=np.uint64)
+    c = np.ascontiguousarray(cuts, dtype=np.uint32)
+    out = np.zeros(c.size - 1, dtype=np.uint64)
+    check(lib.bsort_dist_send_counts(_u64p(h), _u32p(c), c.size - 1, _u64p(out)),
+          "bsort_dist_send_counts")
+    return out
+
+
+def partition(t: torch.Tensor, cuts: np.ndarray, counts: np.ndarray,
+              descending: bool = False) -> torch.Tensor:
+    """Stable partition of ``t`` by destination rank (buckets in rank order)."""
+    _check_tensor(t)
+    code = dtype_code(t.dtype)
+    c = np.ascontiguousarray(cuts, dtype=np.uint32)
+    sc = np.ascontiguousarray(counts, dtype=np.uint64)
+    nranks = c.size - 1
+    out = torch.empty_like(t)
+    wsb = int(lib.bsort_dist_partition_workspace_bytes(code, t.numel(), nranks))
+    ws = _workspace(wsb, t.device)
+    check(lib.bsort_dist_partition(code, ctypes.c_void_p(t.data_ptr()), t.numel(),
+                                   int(bool(descending)), _u32p(c), _u64p(sc), nranks,
+                                   ctypes.c_void_p(out.data_ptr()), ctypes.c_void_p(ws.data_ptr()),
+                                   wsb, _stream_ptr(t.device)), "bsort_dist_partition")
+    return out
+
+
+from .dist import sort_dist  # noqa: E402  (needs the helpers above)
+
+
+# --------------------------------------------------------------------------- profiling
+
+@contextlib.contextmanager
+def profile():
+    """Record CUDA events around every libbsort kernel; yields a dict filled on exit with
+    {kind: {"ms": total_ms, "launches": count}} (events synchronised at exit)."""
+    result: dict = {}
+    lib.bsort_profile_enable(1)
+    try:
+        yield result
+    finally:
+        ms = (ctypes.c_double * _lib.PROF_KINDS)()
+        cnt = (ctypes.c_uint64 * _lib.PROF_KINDS)()
+        lib.bsort_profile_read(ms, cnt)
+        lib.bsort_profile_enable(0)
+        for k in range(_lib.PROF_KINDS):
+            if cnt[k]:
+                result[lib.bsort_profile_kind_name(k).decode()] = {"ms": ms[k], "launches": int(cnt[k])}

@@ -1,0 +1,83 @@
+"""ctypes binding of include/bsort.h (argument marshalling only).
+
+Every step of the sort runs in ``libbsort.so`` (sm_100a CUDA).  There is no fallback: if the
+library is missing or fails to load, importing this module raises.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libbsort.so")
+
+# bsort_dtype_t
+U8, I8, U16, I16, U32, I32, F32, U64, I64, F64 = range(10)
+DTYPE_NAMES = ["u8", "i8", "u16", "i16", "u32", "i32", "f32", "u64", "i64", "f64"]
+DTYPE_BYTES = [1, 1, 2, 2, 4, 4, 4, 8, 8, 8]
+ASCENDING, DESCENDING = 0, 1
+DIST_BINS = 65536
+DIST_MAX_RANKS = 64
+PROF_KINDS = 12
+
+SUCCESS = 0
+
+EXPORTS = [
+    "bsort_workspace_bytes", "bsort_sort", "bsort_sort_ws", "bsort_sort_host",
+    "bsort_dist_top_hist", "bsort_dist_splitters", "bsort_dist_send_counts",
+    "bsort_dist_partition_workspace_bytes", "bsort_dist_partition",
+    "bsort_status_string", "bsort_last_cuda_error", "bsort_version", "bsort_launch_count",
+    "bsort_profile_enable", "bsort_profile_read", "bsort_profile_kind_name",
+]
+
+
+class BsortError(RuntimeError):
+    def __init__(self, status: int, where: str):
+        msg = lib.bsort_status_string(status).decode()
+        extra = ""
+        if status == 5:
+            extra = f" (cudaError {lib.bsort_last_cuda_error()})"
+        super().__init__(f"{where}: {msg}{extra}")
+        self.status = status
+
+
+def _load():
+    if not os.path.exists(LIB_PATH):
+        raise ImportError(
+            f"bsort CUDA library not built: {LIB_PATH} missing (run `make lib` or "
+            "`python -c 'import __graft_entry__ as g; g.build()'`)")
+    L = ctypes.CDLL(LIB_PATH)
+    vp, u64, sz, i32 = ctypes.c_void_p, ctypes.c_uint64, ctypes.c_size_t, ctypes.c_int
+    u64p = ctypes.POINTER(ctypes.c_uint64)
+    u32p = ctypes.POINTER(ctypes.c_uint32)
+    sig = {
+        "bsort_workspace_bytes": (sz, [i32, u64]),
+        "bsort_sort": (i32, [i32, vp, u64, i32, vp]),
+        "bsort_sort_ws": (i32, [i32, vp, u64, i32, vp, sz, vp]),
+        "bsort_sort_host": (i32, [i32, vp, u64, i32, vp, vp, sz, vp]),
+        "bsort_dist_top_hist": (i32, [i32, vp, u64, i32, vp, vp]),
+        "bsort_dist_splitters": (i32, [u64p, i32, u32p]),
+        "bsort_dist_send_counts": (i32, [u64p, u32p, i32, u64p]),
+        "bsort_dist_partition_workspace_bytes": (sz, [i32, u64, i32]),
+        "bsort_dist_partition": (i32, [i32, vp, u64, i32, u32p, u64p, i32, vp, vp, sz, vp]),
+        "bsort_status_string": (ctypes.c_char_p, [i32]),
+        "bsort_last_cuda_error": (i32, []),
+        "bsort_version": (ctypes.c_char_p, []),
+        "bsort_launch_count": (u64, []),
+        "bsort_profile_enable": (None, [i32]),
+        "bsort_profile_read": (i32, [ctypes.POINTER(ctypes.c_double), u64p]),
+        "bsort_profile_kind_name": (ctypes.c_char_p, [i32]),
+    }
+    for name, (res, args) in sig.items():
+        f = getattr(L, name)
+        f.restype = res
+        f.argtypes = args
+    return L
+
+
+lib = _load()
+
+
+def check(status: int, where: str):
+    if status != SUCCESS:
+        raise BsortError(status, where)

@@ -1,0 +1,296 @@
+// api.cu — the extern "C" boundary (include/bsort.h): validation, path selection (§8 a2),
+// workspace handling, the host-only splitter math of the MSD partition, diagnostics.
+#include <atomic>
+#include <mutex>
+#include <vector>
+
+#include "paths.cuh"
+
+namespace bsort {
+
+static std::atomic<uint64_t> g_launches{0};
+static thread_local int t_last_err = 0;
+
+void count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
+void set_last_cuda_error(cudaError_t e) { t_last_err = (int)e; }
+
+int num_sms() {
+  static int cached[64] = {0};
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return 148;
+  if (cached[dev] == 0) {
+    int v = 0;
+    if (cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || v <= 0) v = 148;
+    cached[dev] = v;
+  }
+  return cached[dev];
+}
+
+bool dtype_info(bsort_dtype_t dt, DtypeInfo* o) {
+  switch (dt) {
+    case BSORT_U8: *o = {1, KIND_U}; return true;
+    case BSORT_I8: *o = {1, KIND_I}; return true;
+    case BSORT_U16: *o = {2, KIND_U}; return true;
+    case BSORT_I16: *o = {2, KIND_I}; return true;
+    case BSORT_U32: *o = {4, KIND_U}; return true;
+    case BSORT_I32: *o = {4, KIND_I}; return true;
+    case BSORT_F32: *o = {4, KIND_F}; return true;
+    case BSORT_U64: *o = {8, KIND_U}; return true;
+    case BSORT_I64: *o = {8, KIND_I}; return true;
+    case BSORT_F64: *o = {8, KIND_F}; return true;
+    default: return false;
+  }
+}
+
+// ------------------------------------------------------------------------- profiler
+namespace {
+struct ProfRec {
+  int kind;
+  cudaEvent_t a, b;
+};
+std::mutex g_prof_mu;
+bool g_prof_on = false;
+std::vector<ProfRec> g_prof_recs;
+std::vector<cudaEvent_t> g_event_pool;
+thread_local cudaEvent_t t_open_event = nullptr;
+
+cudaEvent_t take_event() {
+  if (!g_event_pool.empty()) {
+    cudaEvent_t e = g_event_pool.back();
+    g_event_pool.pop_back();
+    return e;
+  }
+  cudaEvent_t e = nullptr;
+  cudaEventCreate(&e);
+  return e;
+}
+}  // namespace
+
+void prof_begin(int, cudaStream_t s) {
+  std::lock_guard<std::mutex> g(g_prof_mu);
+  if (!g_prof_on) return;
+  t_open_event = take_event();
+  cudaEventRecord(t_open_event, s);
+}
+
+void prof_end(int kind, cudaStream_t s) {
+  std::lock_guard<std::mutex> g(g_prof_mu);
+  if (!g_prof_on || !t_open_event) return;
+  cudaEvent_t b = take_event();
+  cudaEventRecord(b, s);
+  g_prof_recs.push_back({kind, t_open_event, b});
+  t_open_event = nullptr;
+}
+
+}  // namespace bsort
+
+using namespace bsort;
+
+namespace {
+
+bool aligned_to(const void* p, int bytes) { return ((uintptr_t)p % (uintptr_t)bytes) == 0; }
+
+size_t workspace_bytes(const DtypeInfo& di, uint64_t n) {
+  if (n <= 1) return 0;
+  return di.bytes <= 2 ? counting_workspace_bytes(di.bytes, n) : lsd_workspace_bytes(di.bytes, n);
+}
+
+bsort_status_t validate(bsort_dtype_t dtype, const void* p, uint64_t n, bsort_direction_t dir, DtypeInfo* di) {
+  if (!dtype_info(dtype, di)) return BSORT_ERROR_UNSUPPORTED_DTYPE;
+  if (dir != BSORT_ASCENDING && dir != BSORT_DESCENDING) return BSORT_ERROR_INVALID_ARGUMENT;
+  if (n > 0 && p == nullptr) return BSORT_ERROR_INVALID_ARGUMENT;
+  if (n > 0 && !aligned_to(p, di->bytes)) return BSORT_ERROR_INVALID_ARGUMENT;
+  return BSORT_SUCCESS;
+}
+
+bsort_status_t sort_ws_impl(const DtypeInfo& di, void* keys, uint64_t n, bsort_direction_t dir, void* ws,
+                            size_t wsb, cudaStream_t s) {
+  if (n <= 1) return BSORT_SUCCESS;
+  if (ws == nullptr || !aligned_to(ws, 256)) return BSORT_ERROR_INVALID_ARGUMENT;
+  const bool desc = dir == BSORT_DESCENDING;
+  return di.bytes <= 2 ? counting_sort(di, keys, n, desc, ws, wsb, s) : lsd_sort(di, keys, n, desc, ws, wsb, s);
+}
+
+}  // namespace
+
+extern "C" {
+
+size_t bsort_workspace_bytes(bsort_dtype_t dtype, uint64_t n) {
+  DtypeInfo di;
+  if (!dtype_info(dtype, &di)) return 0;
+  return workspace_bytes(di, n);
+}
+
+bsort_status_t bsort_sort_ws(bsort_dtype_t dtype, void* dev_keys, uint64_t n, bsort_direction_t direction,
+                             void* workspace, size_t workspace_bytes_, void* stream) {
+  DtypeInfo di;
+  bsort_status_t st = validate(dtype, dev_keys, n, direction, &di);
+  if (st != BSORT_SUCCESS) return st;
+  if (n <= 1) return BSORT_SUCCESS;
+  if (workspace_bytes_ < workspace_bytes(di, n)) return BSORT_ERROR_WORKSPACE_TOO_SMALL;
+  return sort_ws_impl(di, dev_keys, n, direction, workspace, workspace_bytes_, (cudaStream_t)stream);
+}
+
+bsort_status_t bsort_sort(bsort_dtype_t dtype, void* dev_keys, uint64_t n, bsort_direction_t direction,
+                          void* stream) {
+  DtypeInfo di;
+  bsort_status_t st = validate(dtype, dev_keys, n, direction, &di);
+  if (st != BSORT_SUCCESS || n <= 1) return st;
+  cudaStream_t s = (cudaStream_t)stream;
+  const size_t wsb = workspace_bytes(di, n);
+  void* ws = nullptr;
+  cudaError_t e = cudaMallocAsync(&ws, wsb, s);
+  if (e != cudaSuccess) {
+    set_last_cuda_error(e);
+    cudaGetLastError();
+    return BSORT_ERROR_OUT_OF_MEMORY;
+  }
+  st = sort_ws_impl(di, dev_keys, n, direction, ws, wsb, s);
+  e = cudaFreeAsync(ws, s);
+  if (st == BSORT_SUCCESS && e != cudaSuccess) {
+    set_last_cuda_error(e);
+    return BSORT_ERROR_CUDA;
+  }
+  return st;
+}
+
+bsort_status_t bsort_sort_host(bsort_dtype_t dtype, void* host_keys, uint64_t n, bsort_direction_t direction,
+                               void* dev_keys, void* workspace, size_t workspace_bytes_, void* stream) {
+  DtypeInfo di;
+  bsort_status_t st = validate(dtype, dev_keys, n, direction, &di);
+  if (st != BSORT_SUCCESS) return st;
+  if (n > 0 && host_keys == nullptr) return BSORT_ERROR_INVALID_ARGUMENT;
+  if (n == 0) return BSORT_SUCCESS;
+  if (n > 1 && workspace_bytes_ < workspace_bytes(di, n)) return BSORT_ERROR_WORKSPACE_TOO_SMALL;
+  cudaStream_t s = (cudaStream_t)stream;
+  const size_t bytes = (size_t)n * di.bytes;
+  prof_begin(PROF_H2D, s);
+  BSORT_CUDA(cudaMemcpyAsync(dev_keys, host_keys, bytes, cudaMemcpyHostToDevice, s));
+  prof_end(PROF_H2D, s);
+  st = sort_ws_impl(di, dev_keys, n, direction, workspace, workspace_bytes_, s);
+  if (st != BSORT_SUCCESS) return st;
+  prof_begin(PROF_D2H, s);
+  BSORT_CUDA(cudaMemcpyAsync(host_keys, dev_keys, bytes, cudaMemcpyDeviceToHost, s));
+  prof_end(PROF_D2H, s);
+  return BSORT_SUCCESS;
+}
+
+// ------------------------------------------------------------------------ distributed
+
+bsort_status_t bsort_dist_top_hist(bsort_dtype_t dtype, const void* dev_keys, uint64_t n,
+                                   bsort_direction_t direction, uint64_t* dev_hist, void* stream) {
+  DtypeInfo di;
+  bsort_status_t st = validate(dtype, dev_keys, n, direction, &di);
+  if (st != BSORT_SUCCESS) return st;
+  if (di.bytes < 4) return BSORT_ERROR_UNSUPPORTED_DTYPE;
+  if (dev_hist == nullptr || !aligned_to(dev_hist, 8)) return BSORT_ERROR_INVALID_ARGUMENT;
+  return dist_top_hist(di, dev_keys, n, direction == BSORT_DESCENDING, dev_hist, (cudaStream_t)stream);
+}
+
+bsort_status_t bsort_dist_splitters(const uint64_t* hist, int nranks, uint32_t* cuts) {
+  if (!hist || !cuts || nranks < 1 || nranks > BSORT_DIST_MAX_RANKS) return BSORT_ERROR_INVALID_ARGUMENT;
+  unsigned __int128 total = 0;
+  for (int b = 0; b < BSORT_DIST_BINS; ++b) total += hist[b];
+  cuts[0] = 0;
+  cuts[nranks] = BSORT_DIST_BINS;
+  uint64_t prefix = 0;  // sum(hist[0..b))
+  int b = 0;
+  for (int r = 1; r < nranks; ++r) {
+    const uint64_t target = (uint64_t)((total * (unsigned __int128)r) / (unsigned __int128)nranks);
+    while (b < BSORT_DIST_BINS && prefix < target) prefix += hist[b++];
+    cuts[r] = (uint32_t)b;
+  }
+  return BSORT_SUCCESS;
+}
+
+bsort_status_t bsort_dist_send_counts(const uint64_t* local_hist, const uint32_t* cuts, int nranks,
+                                      uint64_t* send_counts) {
+  if (!local_hist || !cuts || !send_counts || nranks < 1 || nranks > BSORT_DIST_MAX_RANKS)
+    return BSORT_ERROR_INVALID_ARGUMENT;
+  if (cuts[0] != 0 || cuts[nranks] != BSORT_DIST_BINS) return BSORT_ERROR_INVALID_ARGUMENT;
+  for (int q = 0; q < nranks; ++q) {
+    if (cuts[q] > cuts[q + 1]) return BSORT_ERROR_INVALID_ARGUMENT;
+    uint64_t c = 0;
+    for (uint32_t b = cuts[q]; b < cuts[q + 1]; ++b) c += local_hist[b];
+    send_counts[q] = c;
+  }
+  return BSORT_SUCCESS;
+}
+
+size_t bsort_dist_partition_workspace_bytes(bsort_dtype_t dtype, uint64_t n, int nranks) {
+  DtypeInfo di;
+  if (!dtype_info(dtype, &di) || di.bytes < 4) return 0;
+  return dist_partition_workspace_bytes(di.bytes, n, nranks);
+}
+
+bsort_status_t bsort_dist_partition(bsort_dtype_t dtype, const void* dev_in, uint64_t n,
+                                    bsort_direction_t direction, const uint32_t* cuts,
+                                    const uint64_t* send_counts, int nranks, void* dev_out, void* workspace,
+                                    size_t workspace_bytes_, void* stream) {
+  DtypeInfo di;
+  bsort_status_t st = validate(dtype, dev_in, n, direction, &di);
+  if (st != BSORT_SUCCESS) return st;
+  if (di.bytes < 4) return BSORT_ERROR_UNSUPPORTED_DTYPE;
+  if (!cuts || !send_counts || nranks < 1 || nranks > BSORT_DIST_MAX_RANKS) return BSORT_ERROR_INVALID_ARGUMENT;
+  if (cuts[0] != 0 || cuts[nranks] != BSORT_DIST_BINS) return BSORT_ERROR_INVALID_ARGUMENT;
+  for (int q = 0; q < nranks; ++q)
+    if (cuts[q] > cuts[q + 1]) return BSORT_ERROR_INVALID_ARGUMENT;
+  if (n == 0) return BSORT_SUCCESS;
+  if (!dev_out || !aligned_to(dev_out, di.bytes) || dev_out == dev_in) return BSORT_ERROR_INVALID_ARGUMENT;
+  if (!workspace || !aligned_to(workspace, 256)) return BSORT_ERROR_INVALID_ARGUMENT;
+  return dist_partition(di, dev_in, n, direction == BSORT_DESCENDING, cuts, send_counts, nranks, dev_out,
+                        workspace, workspace_bytes_, (cudaStream_t)stream);
+}
+
+// ------------------------------------------------------------------------ diagnostics
+
+const char* bsort_status_string(bsort_status_t s) {
+  switch (s) {
+    case BSORT_SUCCESS: return "success";
+    case BSORT_ERROR_INVALID_ARGUMENT: return "invalid argument";
+    case BSORT_ERROR_UNSUPPORTED_DTYPE: return "unsupported dtype";
+    case BSORT_ERROR_OUT_OF_MEMORY: return "out of device memory";
+    case BSORT_ERROR_WORKSPACE_TOO_SMALL: return "workspace too small";
+    case BSORT_ERROR_CUDA: return "CUDA error";
+    default: return "unknown status";
+  }
+}
+
+int bsort_last_cuda_error(void) { return t_last_err; }
+const char* bsort_version(void) { return "bsort-b200 0.1 (sm_100a)"; }
+uint64_t bsort_launch_count(void) { return g_launches.load(); }
+
+void bsort_profile_enable(int on) {
+  std::lock_guard<std::mutex> g(g_prof_mu);
+  for (auto& r : g_prof_recs) {
+    g_event_pool.push_back(r.a);
+    g_event_pool.push_back(r.b);
+  }
+  g_prof_recs.clear();
+  g_prof_on = on != 0;
+}
+
+int bsort_profile_read(double* ms, uint64_t* launches) {
+  std::lock_guard<std::mutex> g(g_prof_mu);
+  for (int k = 0; k < BSORT_PROF_KINDS; ++k) {
+    if (ms) ms[k] = 0.0;
+    if (launches) launches[k] = 0;
+  }
+  for (auto& r : g_prof_recs) {
+    cudaEventSynchronize(r.b);
+    float t = 0.f;
+    cudaEventElapsedTime(&t, r.a, r.b);
+    if (ms) ms[r.kind] += t;
+    if (launches) launches[r.kind] += 1;
+  }
+  return BSORT_PROF_KINDS;
+}
+
+const char* bsort_profile_kind_name(int k) {
+  static const char* names[BSORT_PROF_KINDS] = {"memset", "onesweep_hist", "plan_scan", "onesweep_pass",
+                                                "copy_back", "count_hist", "count_scan", "count_fill",
+                                                "dist_tophist", "dist_partition", "h2d", "d2h"};
+  return (k >= 0 && k < BSORT_PROF_KINDS) ? names[k] : "?";
+}
+
+}  // extern "C"

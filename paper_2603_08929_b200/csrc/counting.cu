@@ -1,0 +1,325 @@
+// counting.cu — a6: the small-word counting path for 8/16-bit keys (BASELINE.json cfg2).
+//
+// Keys of w <= 16 bits are sorted by one histogram over all 2^w transformed values followed by
+// a regeneration of the array from the bin prefix (Theorem 5's in-place property, P:761-775,
+// is kept: O(2^w) auxiliary counters, no second key buffer).  Exact because equal transformed
+// keys are equal bit patterns (the transform is a bijection), so the multiset of bins IS the
+// multiset of keys.
+//
+//   k_count_hist8   256 lane-banked counters per CTA (bank = lane => conflict-free smem
+//                   atomics), one read of the keys with 128-bit loads, flush to 256 global u64.
+//   k_count_fill8   every CTA scans the 256 counts in smem; each thread regenerates 16-byte
+//                   output vectors (binary search of the first key's bin, 128-bit stores).
+//   k_count_hist16  65536 bins do not fit one CTA's smem as u32, so CTA pairs split the bin
+//                   range in two halves of 32768 (128 KB each) and both read the same key
+//                   chunk (the second read hits L2); per-chunk partial histograms are written
+//                   without atomics.
+//   k_count_reduce16 sums the partials per bin, scans 256-bin blocks.
+//   k_count_fill16  two-level search (block prefix in smem, bin prefix in L2), 128-bit stores.
+#include "paths.cuh"
+#include "scan.cuh"
+
+namespace bsort {
+namespace {
+
+constexpr int CNT_THREADS = 1024;
+constexpr int FILL_THREADS = 256;
+constexpr int BINS16 = 65536;
+
+__device__ __forceinline__ uint4 ldg_stream(const uint4* p) {
+  uint4 r;
+  asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+               : "l"(p));
+  return r;
+}
+
+// ------------------------------------------------------------------------------ 8-bit
+
+template <uint32_t X>
+__global__ void __launch_bounds__(CNT_THREADS, 2)
+    k_count_hist8(const uint8_t* __restrict__ keys, uint64_t n, unsigned long long* __restrict__ hist) {
+  __shared__ uint32_t h[256 * 32];
+  for (int i = threadIdx.x; i < 256 * 32; i += CNT_THREADS) h[i] = 0;
+  __syncthreads();
+  const uint32_t lane = threadIdx.x & 31;
+  const uint64_t T = (uint64_t)gridDim.x * CNT_THREADS;
+  const uint64_t gt = (uint64_t)blockIdx.x * CNT_THREADS + threadIdx.x;
+  const uint64_t head = min64(n, (16 - ((uintptr_t)keys & 15)) & 15);
+  auto add = [&](uint32_t bin) { atomicAdd(&h[(bin << 5) | lane], 1u); };
+  auto word = [&](uint32_t w) {
+    w ^= X;
+    add(w & 0xFF);
+    add((w >> 8) & 0xFF);
+    add((w >> 16) & 0xFF);
+    add(w >> 24);
+  };
+  auto vec = [&](uint4 q) {
+    word(q.x);
+    word(q.y);
+    word(q.z);
+    word(q.w);
+  };
+  for (uint64_t i = gt; i < head; i += T) add((keys[i] ^ X) & 0xFF);
+  const uint4* v = reinterpret_cast<const uint4*>(keys + head);
+  const uint64_t nv = (n - head) >> 4;
+  uint64_t i = gt;
+  for (; i + 3 * T < nv; i += 4 * T) {
+    uint4 q0 = ldg_stream(v + i), q1 = ldg_stream(v + i + T);
+    uint4 q2 = ldg_stream(v + i + 2 * T), q3 = ldg_stream(v + i + 3 * T);
+    vec(q0);
+    vec(q1);
+    vec(q2);
+    vec(q3);
+  }
+  for (; i < nv; i += T) vec(ldg_stream(v + i));
+  for (uint64_t j = head + (nv << 4) + gt; j < n; j += T) add((keys[j] ^ X) & 0xFF);
+  __syncthreads();
+  for (int b = threadIdx.x; b < 256; b += CNT_THREADS) {
+    uint32_t s = 0;
+#pragma unroll 8
+    for (int l = 0; l < 32; ++l) s += h[(b << 5) | ((l + b) & 31)];
+    if (s) atomicAdd(&hist[b], (unsigned long long)s);
+  }
+}
+
+template <uint32_t X>
+__global__ void __launch_bounds__(FILL_THREADS)
+    k_count_fill8(uint8_t* __restrict__ keys, uint64_t n, const unsigned long long* __restrict__ hist) {
+  __shared__ unsigned long long pre[257];
+  __shared__ unsigned long long wt[FILL_THREADS / 32 + 1];
+  unsigned long long ex = block_exclusive_scan<FILL_THREADS>(hist[threadIdx.x], wt,
+                                                             (unsigned long long*)nullptr);
+  pre[threadIdx.x] = ex;
+  if (threadIdx.x == 0) pre[256] = n;
+  __syncthreads();
+  // largest b in [0, 256) with pre[b] <= p  (pre[0] = 0 <= p < n = pre[256])
+  auto bin_of = [&](uint64_t p) -> uint32_t {
+    uint32_t lo = 0, hi = 256;
+    while (hi - lo > 1) {
+      uint32_t mid = (lo + hi) >> 1;
+      if (pre[mid] <= p) lo = mid; else hi = mid;
+    }
+    return lo;
+  };
+  const uint64_t T = (uint64_t)gridDim.x * FILL_THREADS;
+  const uint64_t gt = (uint64_t)blockIdx.x * FILL_THREADS + threadIdx.x;
+  const uint64_t head = min64(n, (16 - ((uintptr_t)keys & 15)) & 15);
+  for (uint64_t i = gt; i < head; i += T) keys[i] = uint8_t(bin_of(i) ^ X);
+  uint4* v = reinterpret_cast<uint4*>(keys + head);
+  const uint64_t nv = (n - head) >> 4;
+  for (uint64_t i = gt; i < nv; i += T) {
+    const uint64_t p0 = head + (i << 4);
+    uint32_t b = bin_of(p0);
+    uint64_t next = pre[b + 1];
+    uint4 q;
+    if (next >= p0 + 16) {
+      uint32_t w = (b * 0x01010101u) ^ X;
+      q = make_uint4(w, w, w, w);
+    } else {
+      uint32_t w[4] = {0, 0, 0, 0};
+#pragma unroll
+      for (int j = 0; j < 16; ++j) {
+        if (next <= p0 + j) {
+          b = bin_of(p0 + j);
+          next = pre[b + 1];
+        }
+        w[j >> 2] |= b << ((j & 3) * 8);
+      }
+      q = make_uint4(w[0] ^ X, w[1] ^ X, w[2] ^ X, w[3] ^ X);
+    }
+    v[i] = q;
+  }
+  for (uint64_t j = head + (nv << 4) + gt; j < n; j += T) keys[j] = uint8_t(bin_of(j) ^ X);
+}
+
+// ----------------------------------------------------------------------------- 16-bit
+
+template <uint32_t X>
+__global__ void __launch_bounds__(CNT_THREADS, 1)
+    k_count_hist16(const uint16_t* __restrict__ keys, uint64_t n, uint32_t* __restrict__ partial) {
+  extern __shared__ uint32_t h16[];  // 32768 counters: this CTA's half of the bin range
+  const uint32_t half = blockIdx.x & 1;
+  const uint32_t chunk = blockIdx.x >> 1;
+  const uint32_t pairs = gridDim.x >> 1;
+  for (int i = threadIdx.x; i < BINS16 / 2; i += CNT_THREADS) h16[i] = 0;
+  __syncthreads();
+  auto add = [&](uint32_t k) {
+    if ((k >> 15) == half) atomicAdd(&h16[k & 0x7FFF], 1u);
+  };
+  auto vec = [&](uint4 q) {
+    uint32_t w[4] = {q.x ^ X, q.y ^ X, q.z ^ X, q.w ^ X};
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      add(w[j] & 0xFFFF);
+      add(w[j] >> 16);
+    }
+  };
+  const uint64_t head = min64(n, ((16 - ((uintptr_t)keys & 15)) & 15) >> 1);
+  const uint4* v = reinterpret_cast<const uint4*>(keys + head);
+  const uint64_t nv = (n - head) >> 3;
+  const uint64_t per = (nv + pairs - 1) / pairs;
+  const uint64_t vs = min64(nv, (uint64_t)chunk * per);
+  const uint64_t ve = min64(nv, vs + per);
+  if (chunk == 0)
+    for (uint64_t i = threadIdx.x; i < head; i += CNT_THREADS) add((keys[i] ^ X) & 0xFFFF);
+  if (chunk == pairs - 1)
+    for (uint64_t i = head + (nv << 3) + threadIdx.x; i < n; i += CNT_THREADS) add((keys[i] ^ X) & 0xFFFF);
+  uint64_t i = vs + threadIdx.x;
+  for (; i + 3 * CNT_THREADS < ve; i += 4 * CNT_THREADS) {
+    uint4 q0 = ldg_stream(v + i), q1 = ldg_stream(v + i + CNT_THREADS);
+    uint4 q2 = ldg_stream(v + i + 2 * CNT_THREADS), q3 = ldg_stream(v + i + 3 * CNT_THREADS);
+    vec(q0);
+    vec(q1);
+    vec(q2);
+    vec(q3);
+  }
+  for (; i < ve; i += CNT_THREADS) vec(ldg_stream(v + i));
+  __syncthreads();
+  uint32_t* dst = partial + (uint64_t)chunk * BINS16 + half * (BINS16 / 2);
+  for (int b = threadIdx.x; b < BINS16 / 2; b += CNT_THREADS) dst[b] = h16[b];
+}
+
+// grid = 256 blocks x 256 threads: bin b = 256*block + thread.
+__global__ void __launch_bounds__(256)
+    k_count_reduce16(const uint32_t* __restrict__ partial, int pairs,
+                     unsigned long long* __restrict__ local_excl, unsigned long long* __restrict__ blk_total) {
+  __shared__ unsigned long long wt[256 / 32 + 1];
+  const uint32_t b = blockIdx.x * 256 + threadIdx.x;
+  unsigned long long s = 0;
+  for (int c = 0; c < pairs; ++c) s += partial[(uint64_t)c * BINS16 + b];
+  unsigned long long tot;
+  unsigned long long ex = block_exclusive_scan<256>(s, wt, &tot);
+  local_excl[b] = ex;
+  if (threadIdx.x == 0) blk_total[blockIdx.x] = tot;
+}
+
+template <uint32_t X>
+__global__ void __launch_bounds__(FILL_THREADS)
+    k_count_fill16(uint16_t* __restrict__ keys, uint64_t n, const unsigned long long* __restrict__ local_excl,
+                   const unsigned long long* __restrict__ blk_total) {
+  __shared__ unsigned long long cpre[257];
+  __shared__ unsigned long long wt[FILL_THREADS / 32 + 1];
+  unsigned long long ex = block_exclusive_scan<FILL_THREADS>(blk_total[threadIdx.x], wt,
+                                                             (unsigned long long*)nullptr);
+  cpre[threadIdx.x] = ex;
+  if (threadIdx.x == 0) cpre[256] = n;
+  __syncthreads();
+  auto prefix_of = [&](uint32_t b) -> uint64_t {
+    return b >= (uint32_t)BINS16 ? n : cpre[b >> 8] + local_excl[b];
+  };
+  auto bin_of = [&](uint64_t p) -> uint32_t {
+    uint32_t lo = 0, hi = 256;
+    while (hi - lo > 1) {
+      uint32_t mid = (lo + hi) >> 1;
+      if (cpre[mid] <= p) lo = mid; else hi = mid;
+    }
+    const uint64_t base = cpre[lo];
+    uint32_t blo = lo << 8, bhi = blo + 256;
+    while (bhi - blo > 1) {
+      uint32_t mid = (blo + bhi) >> 1;
+      if (base + local_excl[mid] <= p) blo = mid; else bhi = mid;
+    }
+    return blo;
+  };
+  const uint64_t T = (uint64_t)gridDim.x * FILL_THREADS;
+  const uint64_t gt = (uint64_t)blockIdx.x * FILL_THREADS + threadIdx.x;
+  const uint64_t head = min64(n, ((16 - ((uintptr_t)keys & 15)) & 15) >> 1);
+  for (uint64_t i = gt; i < head; i += T) keys[i] = uint16_t(bin_of(i) ^ X);
+  uint4* v = reinterpret_cast<uint4*>(keys + head);
+  const uint64_t nv = (n - head) >> 3;
+  for (uint64_t i = gt; i < nv; i += T) {
+    const uint64_t p0 = head + (i << 3);
+    uint32_t b = bin_of(p0);
+    uint64_t next = prefix_of(b + 1);
+    uint4 q;
+    if (next >= p0 + 8) {
+      uint32_t w = (b * 0x00010001u) ^ X;
+      q = make_uint4(w, w, w, w);
+    } else {
+      uint32_t w[4] = {0, 0, 0, 0};
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        if (next <= p0 + j) {
+          b = bin_of(p0 + j);
+          next = prefix_of(b + 1);
+        }
+        w[j >> 1] |= b << ((j & 1) * 16);
+      }
+      q = make_uint4(w[0] ^ X, w[1] ^ X, w[2] ^ X, w[3] ^ X);
+    }
+    v[i] = q;
+  }
+  for (uint64_t j = head + (nv << 3) + gt; j < n; j += T) keys[j] = uint16_t(bin_of(j) ^ X);
+}
+
+// ------------------------------------------------------------------------ host launch
+
+int fill_grid(uint64_t vectors) {
+  uint64_t want = (vectors + FILL_THREADS - 1) / FILL_THREADS;
+  uint64_t cap = (uint64_t)num_sms() * 8;
+  return (int)max64(1, min64(want, cap));
+}
+
+template <uint32_t X>
+bsort_status_t run8(uint8_t* keys, uint64_t n, void* ws, cudaStream_t s) {
+  auto* hist = reinterpret_cast<unsigned long long*>(ws);
+  BSORT_LAUNCH(PROF_MEMSET, s, cudaMemsetAsync(hist, 0, 256 * sizeof(unsigned long long), s));
+  const int grid = num_sms() * 2;
+  BSORT_LAUNCH(PROF_COUNT_HIST, s, k_count_hist8<X><<<grid, CNT_THREADS, 0, s>>>(keys, n, hist));
+  BSORT_LAUNCH(PROF_COUNT_FILL, s,
+               k_count_fill8<X><<<fill_grid(n / 16 + 1), FILL_THREADS, 0, s>>>(keys, n, hist));
+  return BSORT_SUCCESS;
+}
+
+int pairs16() { return max(1, num_sms() / 2); }
+
+template <uint32_t X>
+bsort_status_t run16(uint16_t* keys, uint64_t n, void* ws, cudaStream_t s) {
+  const int pairs = pairs16();
+  auto* local_excl = reinterpret_cast<unsigned long long*>(ws);
+  auto* blk_total = local_excl + BINS16;
+  auto* partial = reinterpret_cast<uint32_t*>(blk_total + 256);
+  const int smem = (BINS16 / 2) * sizeof(uint32_t);
+  static bool attr_set = false;  // idempotent; benign race
+  if (!attr_set) {
+    BSORT_CUDA(cudaFuncSetAttribute(k_count_hist16<X>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    attr_set = true;
+  }
+  BSORT_LAUNCH(PROF_COUNT_HIST, s,
+               k_count_hist16<X><<<2 * pairs, CNT_THREADS, smem, s>>>(keys, n, partial));
+  BSORT_LAUNCH(PROF_COUNT_SCAN, s,
+               k_count_reduce16<<<256, 256, 0, s>>>(partial, pairs, local_excl, blk_total));
+  BSORT_LAUNCH(PROF_COUNT_FILL, s,
+               k_count_fill16<X><<<fill_grid(n / 8 + 1), FILL_THREADS, 0, s>>>(keys, n, local_excl, blk_total));
+  return BSORT_SUCCESS;
+}
+
+}  // namespace
+
+size_t counting_workspace_bytes(int bytes, uint64_t n) {
+  if (n <= 1) return 0;
+  if (bytes == 1) return 256 * sizeof(unsigned long long);
+  return (BINS16 + 256) * sizeof(unsigned long long) + (size_t)pairs16() * BINS16 * sizeof(uint32_t);
+}
+
+bsort_status_t counting_sort(const DtypeInfo& di, void* keys, uint64_t n, bool desc, void* ws,
+                             size_t ws_bytes, cudaStream_t s) {
+  if (ws_bytes < counting_workspace_bytes(di.bytes, n)) return BSORT_ERROR_WORKSPACE_TOO_SMALL;
+  auto* k8 = static_cast<uint8_t*>(keys);
+  auto* k16 = static_cast<uint16_t*>(keys);
+  if (di.bytes == 1) {
+    if (di.kind == KIND_U)
+      return desc ? run8<packed_xor<KIND_U, true, 1>()>(k8, n, ws, s)
+                  : run8<packed_xor<KIND_U, false, 1>()>(k8, n, ws, s);
+    return desc ? run8<packed_xor<KIND_I, true, 1>()>(k8, n, ws, s)
+                : run8<packed_xor<KIND_I, false, 1>()>(k8, n, ws, s);
+  }
+  if (di.kind == KIND_U)
+    return desc ? run16<packed_xor<KIND_U, true, 2>()>(k16, n, ws, s)
+                : run16<packed_xor<KIND_U, false, 2>()>(k16, n, ws, s);
+  return desc ? run16<packed_xor<KIND_I, true, 2>()>(k16, n, ws, s)
+              : run16<packed_xor<KIND_I, false, 2>()>(k16, n, ws, s);
+}
+
+}  // namespace bsort

@@ -1,0 +1,278 @@
+// lsd.cu — host orchestration of the 32/64-bit one-sweep LSD path (§8 rows a2-a5).
+//
+//   memset(hist) -> k_onesweep_hist -> k_plan -> P x { memset(look-back) ; k_onesweep_pass }
+//   -> k_copy_back (no-op unless an odd number of passes executed)
+// Everything is stream-ordered on the caller's stream; no host synchronisation.
+#include "onesweep.cuh"
+#include "paths.cuh"
+
+namespace bsort {
+namespace {
+
+// Tile configuration per key width (tuned on B200).
+template <typename U> struct PassCfg;
+template <> struct PassCfg<uint32_t> {
+  static constexpr int THREADS = 512, ITEMS = 16, MINB = 2;
+};
+template <> struct PassCfg<unsigned long long> {
+  static constexpr int THREADS = 384, ITEMS = 12, MINB = 2;
+};
+
+template <typename U> constexpr int hist_lanes() { return sizeof(U) == 4 ? 32 : 16; }
+
+struct LsdLayout {
+  size_t scratch, ghist, bases, plan, counters, lookback, total;
+};
+
+template <typename U>
+LsdLayout lsd_layout(uint64_t n) {
+  using C = PassCfg<U>;
+  constexpr uint64_t TILE = (uint64_t)C::THREADS * C::ITEMS;
+  constexpr int P = sizeof(U);
+  const uint64_t tiles = (n + TILE - 1) / TILE;
+  const size_t desc = (n <= (1ull << 30)) ? 4 : 8;
+  LsdLayout l;
+  size_t off = 0;
+  l.scratch = off;  off = align_up(off + n * sizeof(U), 256);
+  l.ghist = off;    off = align_up(off + P * 256 * 8, 256);
+  l.bases = off;    off = align_up(off + P * 256 * 8, 256);
+  l.plan = off;     off = align_up(off + sizeof(PassPlan), 256);
+  l.counters = off; off = align_up(off + 8 * 4, 256);
+  l.lookback = off; off = align_up(off + tiles * 256 * desc, 256);
+  l.total = off;
+  return l;
+}
+
+template <typename U, typename DescT, typename DigitF>
+bsort_status_t launch_pass(const U* a, U* b, uint64_t n, DigitF digit, const unsigned long long* bases,
+                           DescT* lookback, uint32_t* counter, const PassPlan* plan, int pass,
+                           cudaStream_t s) {
+  using C = PassCfg<U>;
+  using L = PassSmem<C::THREADS, C::ITEMS, U>;
+  auto kern = k_onesweep_pass<U, C::THREADS, C::ITEMS, C::MINB, DescT, DigitF>;
+  static int occ = 0;  // per instantiation; benign race (idempotent)
+  if (occ == 0) {
+    BSORT_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L::bytes));
+    int o = 0;
+    BSORT_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, kern, C::THREADS, L::bytes));
+    occ = o > 0 ? o : 1;
+  }
+  const uint64_t tiles = (n + L::TILE - 1) / L::TILE;
+  const uint64_t grid = min64(tiles, (uint64_t)num_sms() * occ);
+  BSORT_LAUNCH(PROF_PASS, s,
+               kern<<<(unsigned)grid, C::THREADS, L::bytes, s>>>(a, b, n, digit, bases, lookback, counter,
+                                                                 (uint32_t)tiles, plan, pass));
+  return BSORT_SUCCESS;
+}
+
+template <int KIND, bool DESC, typename U, typename DescT>
+bsort_status_t lsd_run(U* keys, uint64_t n, unsigned char* ws, cudaStream_t s) {
+  using C = PassCfg<U>;
+  constexpr int P = sizeof(U);
+  constexpr int LANES = hist_lanes<U>();
+  constexpr uint64_t TILE = (uint64_t)C::THREADS * C::ITEMS;
+  const LsdLayout l = lsd_layout<U>(n);
+  U* scratch = reinterpret_cast<U*>(ws + l.scratch);
+  auto* ghist = reinterpret_cast<unsigned long long*>(ws + l.ghist);
+  auto* bases = reinterpret_cast<unsigned long long*>(ws + l.bases);
+  auto* plan = reinterpret_cast<PassPlan*>(ws + l.plan);
+  auto* counters = reinterpret_cast<uint32_t*>(ws + l.counters);
+  auto* lookback = reinterpret_cast<DescT*>(ws + l.lookback);
+  const uint64_t tiles = (n + TILE - 1) / TILE;
+
+  BSORT_LAUNCH(PROF_MEMSET, s, cudaMemsetAsync(ghist, 0, P * 256 * 8, s));
+  auto hk = k_onesweep_hist<KIND, DESC, U, LANES>;
+  constexpr int hsmem = P * 256 * LANES * 4;
+  static bool hattr = false;
+  if (!hattr) {
+    BSORT_CUDA(cudaFuncSetAttribute(hk, cudaFuncAttributeMaxDynamicSharedMemorySize, hsmem));
+    hattr = true;
+  }
+  BSORT_LAUNCH(PROF_HIST, s, hk<<<num_sms(), HIST_THREADS, hsmem, s>>>(keys, n, ghist));
+  BSORT_LAUNCH(PROF_SCAN, s, k_plan<<<1, 256, 0, s>>>(ghist, n, P, bases, plan, counters));
+  for (int p = 0; p < P; ++p) {
+    BSORT_LAUNCH(PROF_MEMSET, s, cudaMemsetAsync(lookback, 0, tiles * 256 * sizeof(DescT), s));
+    bsort_status_t st = launch_pass<U, DescT>(keys, scratch, n, RadixDigit<KIND, DESC, U>{8 * p},
+                                              bases + p * 256, lookback, counters + p, plan, p, s);
+    if (st != BSORT_SUCCESS) return st;
+  }
+  const int cgrid = (int)min64((n + 255) / 256, (uint64_t)num_sms() * 16);
+  BSORT_LAUNCH(PROF_COPY, s, k_copy_back<U><<<cgrid, 256, 0, s>>>(keys, scratch, n, plan));
+  return BSORT_SUCCESS;
+}
+
+template <int KIND, bool DESC, typename U>
+bsort_status_t lsd_dispatch_desc(U* keys, uint64_t n, unsigned char* ws, cudaStream_t s) {
+  if (n <= (1ull << 30)) return lsd_run<KIND, DESC, U, uint32_t>(keys, n, ws, s);
+  return lsd_run<KIND, DESC, U, unsigned long long>(keys, n, ws, s);
+}
+
+template <typename U>
+bsort_status_t lsd_dispatch(int kind, bool desc, U* keys, uint64_t n, unsigned char* ws, cudaStream_t s) {
+  switch (kind) {
+    case KIND_U:
+      return desc ? lsd_dispatch_desc<KIND_U, true>(keys, n, ws, s) : lsd_dispatch_desc<KIND_U, false>(keys, n, ws, s);
+    case KIND_I:
+      return desc ? lsd_dispatch_desc<KIND_I, true>(keys, n, ws, s) : lsd_dispatch_desc<KIND_I, false>(keys, n, ws, s);
+    default:
+      return desc ? lsd_dispatch_desc<KIND_F, true>(keys, n, ws, s) : lsd_dispatch_desc<KIND_F, false>(keys, n, ws, s);
+  }
+}
+
+}  // namespace
+
+size_t lsd_workspace_bytes(int bytes, uint64_t n) {
+  if (n <= 1) return 0;
+  return bytes == 4 ? lsd_layout<uint32_t>(n).total : lsd_layout<unsigned long long>(n).total;
+}
+
+bsort_status_t lsd_sort(const DtypeInfo& di, void* keys, uint64_t n, bool desc, void* ws, size_t ws_bytes,
+                        cudaStream_t s) {
+  if (ws_bytes < lsd_workspace_bytes(di.bytes, n)) return BSORT_ERROR_WORKSPACE_TOO_SMALL;
+  auto* w = static_cast<unsigned char*>(ws);
+  if (di.bytes == 4) return lsd_dispatch<uint32_t>(di.kind, desc, static_cast<uint32_t*>(keys), n, w, s);
+  return lsd_dispatch<unsigned long long>(di.kind, desc, static_cast<unsigned long long*>(keys), n, w, s);
+}
+
+// ---------------------------------------------------------------- MSD partition (a7, a9)
+
+namespace {
+constexpr int TOP_BINS = BSORT_DIST_BINS;
+
+// Top-16-bit histogram of the transformed keys: 65536 u32 bins do not fit next to a useful
+// occupancy, so each CTA counts into a 16-bit-index smem table of 32768 u32 for its half of
+// the bins (CTA pairs, as in the 16-bit counting path) and flushes with global atomics.
+template <int KIND, bool DESC, typename U>
+__global__ void __launch_bounds__(1024, 1)
+    k_dist_tophist(const U* __restrict__ keys, uint64_t n, unsigned long long* __restrict__ hist) {
+  extern __shared__ uint32_t th[];
+  const uint32_t half = blockIdx.x & 1;
+  const uint32_t chunk = blockIdx.x >> 1;
+  const uint32_t pairs = gridDim.x >> 1;
+  for (int i = threadIdx.x; i < TOP_BINS / 2; i += 1024) th[i] = 0;
+  __syncthreads();
+  const uint64_t per = (n + pairs - 1) / pairs;
+  const uint64_t s0 = min64(n, (uint64_t)chunk * per), s1 = min64(n, s0 + per);
+  for (uint64_t i = s0 + threadIdx.x; i < s1; i += 1024) {
+    const uint32_t b = uint32_t(key_encode<KIND, DESC>(keys[i]) >> (sizeof(U) * 8 - 16));
+    if ((b >> 15) == half) atomicAdd(&th[b & 0x7FFF], 1u);
+  }
+  __syncthreads();
+  for (int b = threadIdx.x; b < TOP_BINS / 2; b += 1024)
+    if (th[b]) atomicAdd(&hist[half * (TOP_BINS / 2) + b], (unsigned long long)th[b]);
+}
+
+template <int KIND, bool DESC, typename U>
+bsort_status_t tophist_run(const U* keys, uint64_t n, uint64_t* hist, cudaStream_t s) {
+  auto* h = reinterpret_cast<unsigned long long*>(hist);
+  BSORT_LAUNCH(PROF_MEMSET, s, cudaMemsetAsync(h, 0, TOP_BINS * 8, s));
+  if (n == 0) return BSORT_SUCCESS;
+  auto k = k_dist_tophist<KIND, DESC, U>;
+  constexpr int smem = TOP_BINS / 2 * 4;
+  static bool attr = false;
+  if (!attr) {
+    BSORT_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    attr = true;
+  }
+  const int pairs = max(1, num_sms() / 2);
+  BSORT_LAUNCH(PROF_DIST_HIST, s, k<<<2 * pairs, 1024, smem, s>>>(keys, n, h));
+  return BSORT_SUCCESS;
+}
+
+template <typename U>
+size_t part_layout(uint64_t n, size_t* counters_off, size_t* bases_off, size_t* lb_off) {
+  using L = PassSmem<PassCfg<U>::THREADS, PassCfg<U>::ITEMS, U>;
+  const uint64_t tiles = (n + L::TILE - 1) / L::TILE;
+  const size_t desc = (n < (1ull << 30)) ? 4 : 8;
+  size_t off = 0;
+  *counters_off = off; off = align_up(off + 64, 256);
+  *bases_off = off;    off = align_up(off + 256 * 8, 256);
+  *lb_off = off;       off = align_up(off + tiles * 256 * desc, 256);
+  return off;
+}
+
+template <int KIND, bool DESC, typename U, typename DescT>
+bsort_status_t part_run(const U* in, uint64_t n, const uint32_t* cuts, int nranks, U* out, unsigned char* ws,
+                        const unsigned long long* host_bases, cudaStream_t s) {
+  size_t co, bo, lo;
+  part_layout<U>(n, &co, &bo, &lo);
+  using L = PassSmem<PassCfg<U>::THREADS, PassCfg<U>::ITEMS, U>;
+  const uint64_t tiles = (n + L::TILE - 1) / L::TILE;
+  auto* counter = reinterpret_cast<uint32_t*>(ws + co);
+  auto* bases = reinterpret_cast<unsigned long long*>(ws + bo);
+  auto* lb = reinterpret_cast<DescT*>(ws + lo);
+  BSORT_LAUNCH(PROF_MEMSET, s, cudaMemsetAsync(ws, 0, lo + tiles * 256 * sizeof(DescT), s));
+  // bases: exclusive offsets of each destination bucket (computed on the host from the local
+  // histogram by the caller's send counts; pageable copy is staged before return).
+  BSORT_CUDA(cudaMemcpyAsync(bases, host_bases, 256 * 8, cudaMemcpyHostToDevice, s));
+  RankDigit<KIND, DESC, U> dg;
+  for (int q = 0; q <= nranks; ++q) dg.cuts[q] = cuts[q];
+  for (int q = nranks + 1; q <= BSORT_DIST_MAX_RANKS; ++q) dg.cuts[q] = TOP_BINS;
+  dg.nranks = nranks;
+  // The digit functor's invalid-tail digit is 255 > any rank; bases beyond nranks are unused.
+  return launch_pass<U, DescT>(in, out, n, dg, bases, lb, counter, nullptr, 0, s);
+}
+
+}  // namespace
+
+bsort_status_t dist_top_hist(const DtypeInfo& di, const void* keys, uint64_t n, bool desc, uint64_t* hist,
+                             cudaStream_t s) {
+#define TOPH(U_)                                                                                                  \
+  switch (di.kind) {                                                                                              \
+    case KIND_U: return desc ? tophist_run<KIND_U, true>((const U_*)keys, n, hist, s)                             \
+                             : tophist_run<KIND_U, false>((const U_*)keys, n, hist, s);                           \
+    case KIND_I: return desc ? tophist_run<KIND_I, true>((const U_*)keys, n, hist, s)                             \
+                             : tophist_run<KIND_I, false>((const U_*)keys, n, hist, s);                           \
+    default: return desc ? tophist_run<KIND_F, true>((const U_*)keys, n, hist, s)                                 \
+                         : tophist_run<KIND_F, false>((const U_*)keys, n, hist, s);                               \
+  }
+  if (di.bytes == 4) { TOPH(uint32_t) }
+  TOPH(unsigned long long)
+#undef TOPH
+}
+
+size_t dist_partition_workspace_bytes(int bytes, uint64_t n, int nranks) {
+  (void)nranks;
+  size_t a, b, c;
+  return bytes == 4 ? part_layout<uint32_t>(n, &a, &b, &c) : part_layout<unsigned long long>(n, &a, &b, &c);
+}
+
+bsort_status_t dist_partition(const DtypeInfo& di, const void* in, uint64_t n, bool desc, const uint32_t* cuts,
+                              const uint64_t* send_counts, int nranks, void* out, void* ws, size_t ws_bytes,
+                              cudaStream_t s) {
+  if (ws_bytes < dist_partition_workspace_bytes(di.bytes, n, nranks)) return BSORT_ERROR_WORKSPACE_TOO_SMALL;
+  if (n == 0) return BSORT_SUCCESS;
+  unsigned long long hb[256];
+  unsigned long long acc = 0;
+  for (int q = 0; q < 256; ++q) {
+    hb[q] = acc;
+    if (q < nranks) acc += send_counts[q];
+  }
+  if (acc != n) return BSORT_ERROR_INVALID_ARGUMENT;
+  auto* w = static_cast<unsigned char*>(ws);
+  const bool d64 = n >= (1ull << 30);
+#define PART(U_)                                                                                                  \
+  {                                                                                                               \
+    const U_* i_ = static_cast<const U_*>(in);                                                                    \
+    U_* o_ = static_cast<U_*>(out);                                                                               \
+    switch (di.kind * 2 + (desc ? 1 : 0)) {                                                                       \
+      case 0: return d64 ? part_run<KIND_U, false, U_, unsigned long long>(i_, n, cuts, nranks, o_, w, hb, s)     \
+                         : part_run<KIND_U, false, U_, uint32_t>(i_, n, cuts, nranks, o_, w, hb, s);              \
+      case 1: return d64 ? part_run<KIND_U, true, U_, unsigned long long>(i_, n, cuts, nranks, o_, w, hb, s)      \
+                         : part_run<KIND_U, true, U_, uint32_t>(i_, n, cuts, nranks, o_, w, hb, s);               \
+      case 2: return d64 ? part_run<KIND_I, false, U_, unsigned long long>(i_, n, cuts, nranks, o_, w, hb, s)     \
+                         : part_run<KIND_I, false, U_, uint32_t>(i_, n, cuts, nranks, o_, w, hb, s);              \
+      case 3: return d64 ? part_run<KIND_I, true, U_, unsigned long long>(i_, n, cuts, nranks, o_, w, hb, s)      \
+                         : part_run<KIND_I, true, U_, uint32_t>(i_, n, cuts, nranks, o_, w, hb, s);               \
+      case 4: return d64 ? part_run<KIND_F, false, U_, unsigned long long>(i_, n, cuts, nranks, o_, w, hb, s)     \
+                         : part_run<KIND_F, false, U_, uint32_t>(i_, n, cuts, nranks, o_, w, hb, s);              \
+      default: return d64 ? part_run<KIND_F, true, U_, unsigned long long>(i_, n, cuts, nranks, o_, w, hb, s)     \
+                          : part_run<KIND_F, true, U_, uint32_t>(i_, n, cuts, nranks, o_, w, hb, s);              \
+    }                                                                                                             \
+  }
+  if (di.bytes == 4) PART(uint32_t)
+  PART(unsigned long long)
+#undef PART
+}
+
+}  // namespace bsort

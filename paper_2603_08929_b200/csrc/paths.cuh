@@ -1,0 +1,32 @@
+// paths.cuh — host entry points of the two sort paths (internal, not ABI).
+#pragma once
+#include "common.cuh"
+
+namespace bsort {
+
+struct DtypeInfo {
+  int bytes;  // key width in bytes
+  int kind;   // KIND_U / KIND_I / KIND_F
+};
+bool dtype_info(bsort_dtype_t dt, DtypeInfo* out);
+
+// a6: 8/16-bit counting path (in place).
+size_t counting_workspace_bytes(int bytes, uint64_t n);
+bsort_status_t counting_sort(const DtypeInfo& di, void* keys, uint64_t n, bool desc, void* ws,
+                             size_t ws_bytes, cudaStream_t s);
+
+// a3-a5: 32/64-bit one-sweep LSD path.
+size_t lsd_workspace_bytes(int bytes, uint64_t n);
+bsort_status_t lsd_sort(const DtypeInfo& di, void* keys, uint64_t n, bool desc, void* ws,
+                        size_t ws_bytes, cudaStream_t s);
+
+// a7/a9: distributed building blocks.
+bsort_status_t dist_top_hist(const DtypeInfo& di, const void* keys, uint64_t n, bool desc,
+                             uint64_t* dev_hist, cudaStream_t s);
+size_t dist_partition_workspace_bytes(int bytes, uint64_t n, int nranks);
+bsort_status_t dist_partition(const DtypeInfo& di, const void* in, uint64_t n, bool desc,
+                              const uint32_t* cuts, const uint64_t* send_counts, int nranks,
+                              void* out, void* ws,
+                              size_t ws_bytes, cudaStream_t s);
+
+}  // namespace bsort

@@ -1,0 +1,180 @@
+"""GPU parity: the CUDA path (through the C ABI) vs the CPU oracle, bit for bit.
+
+Every case generates a seeded input on the device, copies it to the host for the oracle
+(R1, oracle/), sorts on the GPU with paper_2603_08929_b200 (ctypes -> libbsort.so), copies
+back and compares raw bytes.  Sizes span several tiles with ragged tails; edge cases cover
+n in {0, 1, 2}, misaligned pointers, all-equal input (every digit trivial), odd numbers of
+executed LSD passes, NaN payloads of both signs, +-0, +-inf and subnormals.
+"""
+import numpy as np
+import pytest
+import torch
+
+import oracle
+import workloads as W
+
+pytestmark = pytest.mark.gpu
+
+ALL = [torch.uint8, torch.int8, torch.uint16, torch.int16, torch.uint32, torch.int32,
+       torch.float32, torch.uint64, torch.int64, torch.float64]
+NP = {torch.uint8: np.uint8, torch.int8: np.int8, torch.uint16: np.uint16, torch.int16: np.int16,
+      torch.uint32: np.uint32, torch.int32: np.int32, torch.float32: np.float32,
+      torch.uint64: np.uint64, torch.int64: np.int64, torch.float64: np.float64}
+TILE = {1: 0, 2: 0, 4: 512 * 16, 8: 384 * 12}
+
+
+@pytest.fixture(scope="module")
+def B():
+    if not torch.cuda.is_available():
+        pytest.skip("needs a CUDA device")
+    import paper_2603_08929_b200 as b
+    return b
+
+
+SIGNED = {torch.uint16: torch.int16, torch.uint32: torch.int32, torch.uint64: torch.int64}
+
+
+def sview(t: torch.Tensor) -> torch.Tensor:
+    """Same bits with a dtype every torch op supports (uint16/32/64 have few kernels)."""
+    return t.view(SIGNED.get(t.dtype, t.dtype))
+
+
+def host(t: torch.Tensor) -> np.ndarray:
+    return sview(t).cpu().numpy().view(NP[t.dtype])
+
+
+def gen(dtype, n, seed):
+    if dtype.is_floating_point:
+        return W.special_mix(dtype, n, seed, "cuda")
+    return W.uniform_int(dtype, n, seed, "cuda")
+
+
+def check_equal(B, t, descending, what=""):
+    ref = oracle.sort_native(host(t), descending=descending)
+    B.sort_(t, descending=descending)
+    torch.cuda.synchronize()
+    got = host(t)
+    if got.tobytes() != ref.tobytes():
+        bad = np.flatnonzero(got.view(np.uint8) != ref.view(np.uint8))
+        raise AssertionError(f"{what}: mismatch at byte {bad[:5]} of {got.nbytes}")
+
+
+def sizes_for(dtype):
+    es = torch.empty(0, dtype=dtype).element_size()
+    base = [0, 1, 2, 3, 31, 1000, 4099, 65537]
+    if TILE[es]:
+        T = TILE[es]
+        base += [T - 1, T, T + 1, 3 * T + 17]
+    return base
+
+
+@pytest.mark.parametrize("dtype", ALL, ids=lambda d: str(d).split(".")[-1])
+@pytest.mark.parametrize("descending", [False, True], ids=["asc", "desc"])
+def test_random_sizes(B, dtype, descending):
+    for n in sizes_for(dtype):
+        check_equal(B, gen(dtype, n, 1000 + n), descending, f"{dtype} n={n}")
+
+
+@pytest.mark.parametrize("dtype", ALL, ids=lambda d: str(d).split(".")[-1])
+def test_medium_size(B, dtype):
+    n = (1 << 20) + 12345
+    for desc in (False, True):
+        check_equal(B, gen(dtype, n, 77), desc, f"{dtype} n={n}")
+
+
+@pytest.mark.parametrize("dtype", ALL, ids=lambda d: str(d).split(".")[-1])
+def test_misaligned_pointer(B, dtype):
+    base = gen(dtype, 50001, 5)
+    for off in (1, 3):
+        view = base[off:off + 40000]
+        assert view.data_ptr() % 16 != 0 or off == 0
+        ref = oracle.sort_native(host(view), descending=False)
+        before = host(base).copy()
+        B.sort_(view)
+        torch.cuda.synchronize()
+        assert host(view).tobytes() == ref.tobytes()
+        after = host(base)
+        assert after[:off].tobytes() == before[:off].tobytes()  # neighbours untouched
+        assert after[off + 40000:].tobytes() == before[off + 40000:].tobytes()
+
+
+@pytest.mark.parametrize("dtype", ALL, ids=lambda d: str(d).split(".")[-1])
+def test_all_equal_and_few_distinct(B, dtype):
+    n = 3 * 8192 + 5
+    x = sview(gen(dtype, 1, 9)).repeat(n).view(dtype)
+    check_equal(B, x.clone(), False, "all equal")
+    check_equal(B, x.clone(), True, "all equal desc")
+    idx = W.bits(n, 3, "cuda")
+    table = sview(gen(dtype, 16, 10))
+    y = table[((idx >> 60) & 15)].view(dtype)
+    check_equal(B, y, False, "16 distinct")
+
+
+@pytest.mark.parametrize("dtype,bits", [(torch.uint32, 24), (torch.uint32, 8), (torch.int64, 40),
+                                        (torch.uint64, 56), (torch.uint64, 8)])
+def test_trivial_digits_odd_pass_count(B, dtype, bits):
+    """Keys confined to the low `bits` bits: the top digits are trivial and skipped on the
+    device; an odd number of executed passes ends in the scratch buffer (final copy)."""
+    n = 100003
+    r = W.bits(n, 21, "cuda") & ((1 << bits) - 1)
+    x = r.to(torch.int64).view(torch.uint64) if dtype == torch.uint64 else r.to(
+        torch.int64 if dtype == torch.int64 else torch.int32)
+    if dtype == torch.uint32:
+        x = r.to(torch.int32).view(torch.uint32)
+    for desc in (False, True):
+        check_equal(B, x.clone(), desc, f"{dtype} {bits} bits")
+
+
+@pytest.mark.parametrize("layout", ["sorted", "reverse", "equal", "distinct16"])
+def test_cfg4_layouts_scaled(B, layout):
+    x = W.make("cfg4", "cuda", n=(1 << 21) + 7, layout=layout)
+    check_equal(B, x, False, layout)
+
+
+def test_cfg1_full(B):
+    """BASELINE.json cfg1 at full size: oracle parity on all 2^20 keys."""
+    check_equal(B, W.make("cfg1", "cuda"), False, "cfg1")
+
+
+def test_cfg3_scaled(B):
+    x = W.make("cfg3", "cuda", n=(1 << 22) + 3)
+    check_equal(B, x.clone(), False, "cfg3")
+    check_equal(B, x.clone(), True, "cfg3 desc")
+
+
+@pytest.mark.parametrize("dtype", [torch.uint8, torch.int8, torch.int16, torch.uint16])
+def test_cfg2_scaled(B, dtype):
+    x = W.make("cfg2", "cuda", n=(1 << 22) + 9, dtype=dtype)
+    for desc in (False, True):
+        check_equal(B, x.clone(), desc, f"cfg2 {dtype}")
+
+
+def test_cfg5_scaled_local(B):
+    for dt in (torch.int64, torch.float64):
+        x = W.make("cfg5", "cuda", n=(1 << 21) + 1, dtype=dt)
+        check_equal(B, x, False, f"cfg5 local {dt}")
+
+
+def test_sort_host_roundtrip(B):
+    x = gen(torch.float32, 300001, 8).cpu().pin_memory()
+    ref = oracle.sort_native(x.numpy(), descending=True)
+    B.sort_host(x, descending=True)
+    assert x.numpy().tobytes() == ref.tobytes()
+
+
+def test_errors_raise(B):
+    t = torch.zeros(10, dtype=torch.float16, device="cuda")
+    with pytest.raises(TypeError):
+        B.sort_(t)
+    with pytest.raises(TypeError):
+        B.sort_(torch.zeros(10))  # CPU tensor: no fallback
+    with pytest.raises(ValueError):
+        B.sort_(torch.zeros(10, 2, device="cuda").t())
+
+
+def test_launch_counter_moves(B):
+    x = gen(torch.int32, 10000, 1)
+    c0 = B.launch_count()
+    B.sort_(x)
+    torch.cuda.synchronize()
+    assert B.launch_count() - c0 >= 6  # hist + plan + 4 passes (+ memsets, copy)
