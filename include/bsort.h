@@ -120,11 +120,13 @@ bsort_status_t bsort_dist_send_counts(const uint64_t* host_local_hist, const uin
 
 size_t bsort_dist_partition_workspace_bytes(bsort_dtype_t dtype, uint64_t n, int nranks);
 
-/* Stable partition of the n keys at dev_in into dev_out (n keys, distinct from dev_in),
- * grouped by destination rank q = the rank owning the key's top-16-bit bin under host_cuts
- * (nranks+1 entries).  host_send_counts (nranks entries, from bsort_dist_send_counts on this
- * rank's histogram, summing to n) fixes the bucket starts: bucket q begins at
- * sum(send_counts[0..q)).  Keys keep their raw bits; within a bucket the input order is kept. */
+/* Partition of the n keys at dev_in into dev_out (n keys, distinct from dev_in), grouped by
+ * destination rank q = the rank owning the key's top-16-bit bin under host_cuts (nranks+1
+ * entries).  host_send_counts (nranks entries, from bsort_dist_send_counts on this rank's
+ * histogram, summing to n) fixes the bucket starts: bucket q begins at sum(send_counts[0..q)).
+ * Keys keep their raw bits.  The order inside a bucket is unspecified (every rank sorts what it
+ * receives, so the MSD step needs no stability).  Returns BSORT_ERROR_INVALID_ARGUMENT if the
+ * send counts do not sum to n. */
 bsort_status_t bsort_dist_partition(bsort_dtype_t dtype, const void* dev_in, uint64_t n,
                                     bsort_direction_t direction, const uint32_t* host_cuts,
                                     const uint64_t* host_send_counts, int nranks, void* dev_out,

@@ -3,6 +3,8 @@
 //   memset(hist) -> k_onesweep_hist -> k_plan -> P x { memset(look-back) ; k_onesweep_pass }
 //   -> k_copy_back (no-op unless an odd number of passes executed)
 // Everything is stream-ordered on the caller's stream; no host synchronisation.
+#include <type_traits>
+
 #include "onesweep.cuh"
 #include "paths.cuh"
 
@@ -12,16 +14,16 @@ namespace {
 // Tile configuration per key width (tuned on B200).
 template <typename U> struct PassCfg;
 template <> struct PassCfg<uint32_t> {
-  static constexpr int THREADS = 512, ITEMS = 16, MINB = 2;
+  static constexpr int THREADS = 512, ITEMS = 16, MINB = 2, LBG = 8;
 };
 template <> struct PassCfg<unsigned long long> {
-  static constexpr int THREADS = 384, ITEMS = 12, MINB = 2;
+  static constexpr int THREADS = 384, ITEMS = 12, MINB = 2, LBG = 8;
 };
 
 template <typename U> constexpr int hist_lanes() { return sizeof(U) == 4 ? 32 : 16; }
 
 struct LsdLayout {
-  size_t scratch, ghist, bases, plan, counters, lookback, total;
+  size_t scratch, ghist, bases, gcount, plan, counters, lookback, total;
 };
 
 template <typename U>
@@ -36,6 +38,7 @@ LsdLayout lsd_layout(uint64_t n) {
   l.scratch = off;  off = align_up(off + n * sizeof(U), 256);
   l.ghist = off;    off = align_up(off + P * 256 * 8, 256);
   l.bases = off;    off = align_up(off + P * 256 * 8, 256);
+  l.gcount = off;   off = align_up(off + P * 256 * 8, 256);
   l.plan = off;     off = align_up(off + sizeof(PassPlan), 256);
   l.counters = off; off = align_up(off + 8 * 4, 256);
   l.lookback = off; off = align_up(off + tiles * 256 * desc, 256);
@@ -43,13 +46,13 @@ LsdLayout lsd_layout(uint64_t n) {
   return l;
 }
 
-template <typename U, typename DescT, typename DigitF>
-bsort_status_t launch_pass(const U* a, U* b, uint64_t n, DigitF digit, const unsigned long long* bases,
-                           DescT* lookback, uint32_t* counter, const PassPlan* plan, int pass,
-                           cudaStream_t s) {
+template <typename U, bool BULK, int RANK, typename DescT, typename DigitF>
+bsort_status_t launch_pass_t(const U* a, U* b, uint64_t n, DigitF digit, const unsigned long long* bases,
+                             DescT* lookback, unsigned long long* gcount, uint32_t* counter, const PassPlan* plan,
+                             int pass, cudaStream_t s) {
   using C = PassCfg<U>;
-  using L = PassSmem<C::THREADS, C::ITEMS, U>;
-  auto kern = k_onesweep_pass<U, C::THREADS, C::ITEMS, C::MINB, DescT, DigitF>;
+  using L = PassSmem<C::THREADS, C::ITEMS, U, RANK>;
+  auto kern = k_onesweep_pass<U, C::THREADS, C::ITEMS, C::MINB, BULK, DescT, DigitF, RANK, C::LBG>;
   static int occ = 0;  // per instantiation; benign race (idempotent)
   if (occ == 0) {
     BSORT_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L::bytes));
@@ -58,10 +61,28 @@ bsort_status_t launch_pass(const U* a, U* b, uint64_t n, DigitF digit, const uns
     occ = o > 0 ? o : 1;
   }
   const uint64_t tiles = (n + L::TILE - 1) / L::TILE;
+  // persistent grid: every CTA resident at once (look-back forward progress)
   const uint64_t grid = min64(tiles, (uint64_t)num_sms() * occ);
   BSORT_LAUNCH(PROF_PASS, s,
-               kern<<<(unsigned)grid, C::THREADS, L::bytes, s>>>(a, b, n, digit, bases, lookback, counter,
+               kern<<<(unsigned)grid, C::THREADS, L::bytes, s>>>(a, b, n, digit, bases, lookback, gcount, counter,
                                                                  (uint32_t)tiles, plan, pass));
+  return BSORT_SUCCESS;
+}
+
+// TMA bulk prefetch needs 16-byte aligned sources: both ping-pong buffers (the scratch buffer
+// always is; the caller's array may be only element-aligned).
+template <typename U, int RANK, typename DescT, typename DigitF>
+bsort_status_t launch_pass(const U* a, U* b, uint64_t n, DigitF digit, const unsigned long long* bases,
+                           DescT* lookback, unsigned long long* gcount, uint32_t* counter, const PassPlan* plan,
+                           int pass, cudaStream_t s) {
+  const bool aligned = ((uintptr_t)a % 16 == 0) && (plan == nullptr || (uintptr_t)b % 16 == 0);
+  if (aligned)
+    return launch_pass_t<U, true, RANK, DescT>(a, b, n, digit, bases, lookback, gcount, counter, plan, pass, s);
+  return launch_pass_t<U, false, RANK, DescT>(a, b, n, digit, bases, lookback, gcount, counter, plan, pass, s);
+}
+
+bsort_status_t memset_async(void* p, size_t bytes, cudaStream_t s) {
+  BSORT_LAUNCH(PROF_MEMSET, s, cudaMemsetAsync(p, 0, bytes, s));
   return BSORT_SUCCESS;
 }
 
@@ -75,6 +96,7 @@ bsort_status_t lsd_run(U* keys, uint64_t n, unsigned char* ws, cudaStream_t s) {
   U* scratch = reinterpret_cast<U*>(ws + l.scratch);
   auto* ghist = reinterpret_cast<unsigned long long*>(ws + l.ghist);
   auto* bases = reinterpret_cast<unsigned long long*>(ws + l.bases);
+  auto* gcount = reinterpret_cast<unsigned long long*>(ws + l.gcount);
   auto* plan = reinterpret_cast<PassPlan*>(ws + l.plan);
   auto* counters = reinterpret_cast<uint32_t*>(ws + l.counters);
   auto* lookback = reinterpret_cast<DescT*>(ws + l.lookback);
@@ -89,13 +111,37 @@ bsort_status_t lsd_run(U* keys, uint64_t n, unsigned char* ws, cudaStream_t s) {
     hattr = true;
   }
   BSORT_LAUNCH(PROF_HIST, s, hk<<<num_sms(), HIST_THREADS, hsmem, s>>>(keys, n, ghist));
-  BSORT_LAUNCH(PROF_SCAN, s, k_plan<<<1, 256, 0, s>>>(ghist, n, P, bases, plan, counters));
-  for (int p = 0; p < P; ++p) {
-    BSORT_LAUNCH(PROF_MEMSET, s, cudaMemsetAsync(lookback, 0, tiles * 256 * sizeof(DescT), s));
-    bsort_status_t st = launch_pass<U, DescT>(keys, scratch, n, RadixDigit<KIND, DESC, U>{8 * p},
-                                              bases + p * 256, lookback, counters + p, plan, p, s);
-    if (st != BSORT_SUCCESS) return st;
+  BSORT_LAUNCH(PROF_SCAN, s, k_plan<<<1, 256, 0, s>>>(ghist, n, P, bases, plan, counters, gcount));
+  bsort_status_t st = BSORT_SUCCESS;
+  auto one_pass = [&](auto shift_c) {
+    constexpr int SH = decltype(shift_c)::value;
+    constexpr int p = SH / 8;
+    if (p >= P || st != BSORT_SUCCESS) return;
+    if constexpr (p > 0) {
+      st = memset_async(lookback, tiles * 256 * sizeof(DescT), s);
+      if (st != BSORT_SUCCESS) return;
+    }
+    // The first LSD pass may order equal digits arbitrarily (the input order carries no
+    // information); every later pass must be stable.
+    if constexpr (p == 0)
+      st = launch_pass<U, RANK_UNSTABLE, DescT>(keys, scratch, n, RadixDigit<KIND, DESC, U, SH>{}, bases, lookback,
+                                                gcount, counters, plan, p, s);
+    else
+      st = launch_pass<U, RANK_ATOMIC_OR, DescT>(keys, scratch, n, RadixDigit<KIND, DESC, U, SH>{},
+                                                 bases + p * 256, lookback, gcount + p * 256, counters + p,
+                                                 plan, p, s);
+  };
+  one_pass(std::integral_constant<int, 0>{});
+  one_pass(std::integral_constant<int, 8>{});
+  one_pass(std::integral_constant<int, 16>{});
+  one_pass(std::integral_constant<int, 24>{});
+  if constexpr (P == 8) {
+    one_pass(std::integral_constant<int, 32>{});
+    one_pass(std::integral_constant<int, 40>{});
+    one_pass(std::integral_constant<int, 48>{});
+    one_pass(std::integral_constant<int, 56>{});
   }
+  if (st != BSORT_SUCCESS) return st;
   const int cgrid = (int)min64((n + 255) / 256, (uint64_t)num_sms() * 16);
   BSORT_LAUNCH(PROF_COPY, s, k_copy_back<U><<<cgrid, 256, 0, s>>>(keys, scratch, n, plan));
   return BSORT_SUCCESS;
@@ -179,38 +225,35 @@ bsort_status_t tophist_run(const U* keys, uint64_t n, uint64_t* hist, cudaStream
   return BSORT_SUCCESS;
 }
 
-template <typename U>
-size_t part_layout(uint64_t n, size_t* counters_off, size_t* bases_off, size_t* lb_off) {
-  using L = PassSmem<PassCfg<U>::THREADS, PassCfg<U>::ITEMS, U>;
-  const uint64_t tiles = (n + L::TILE - 1) / L::TILE;
-  const size_t desc = (n < (1ull << 30)) ? 4 : 8;
+// Workspace of the MSD partition: tile counter, bucket bases, per-bucket running counts.  The
+// partition is an unstable pass (order inside a destination bucket is irrelevant: every rank
+// sorts what it receives), so it needs no look-back array.
+size_t part_layout(size_t* counters_off, size_t* bases_off, size_t* gcount_off) {
   size_t off = 0;
   *counters_off = off; off = align_up(off + 64, 256);
   *bases_off = off;    off = align_up(off + 256 * 8, 256);
-  *lb_off = off;       off = align_up(off + tiles * 256 * desc, 256);
+  *gcount_off = off;   off = align_up(off + 256 * 8, 256);
   return off;
 }
 
-template <int KIND, bool DESC, typename U, typename DescT>
+template <int KIND, bool DESC, typename U>
 bsort_status_t part_run(const U* in, uint64_t n, const uint32_t* cuts, int nranks, U* out, unsigned char* ws,
                         const unsigned long long* host_bases, cudaStream_t s) {
-  size_t co, bo, lo;
-  part_layout<U>(n, &co, &bo, &lo);
-  using L = PassSmem<PassCfg<U>::THREADS, PassCfg<U>::ITEMS, U>;
-  const uint64_t tiles = (n + L::TILE - 1) / L::TILE;
+  size_t co, bo, go;
+  const size_t total = part_layout(&co, &bo, &go);
   auto* counter = reinterpret_cast<uint32_t*>(ws + co);
   auto* bases = reinterpret_cast<unsigned long long*>(ws + bo);
-  auto* lb = reinterpret_cast<DescT*>(ws + lo);
-  BSORT_LAUNCH(PROF_MEMSET, s, cudaMemsetAsync(ws, 0, lo + tiles * 256 * sizeof(DescT), s));
-  // bases: exclusive offsets of each destination bucket (computed on the host from the local
-  // histogram by the caller's send counts; pageable copy is staged before return).
+  auto* gcount = reinterpret_cast<unsigned long long*>(ws + go);
+  BSORT_LAUNCH(PROF_MEMSET, s, cudaMemsetAsync(ws, 0, total, s));
+  // bases: exclusive offsets of each destination bucket (from the caller's send counts; the
+  // pageable copy is staged before cudaMemcpyAsync returns).
   BSORT_CUDA(cudaMemcpyAsync(bases, host_bases, 256 * 8, cudaMemcpyHostToDevice, s));
   RankDigit<KIND, DESC, U> dg;
   for (int q = 0; q <= nranks; ++q) dg.cuts[q] = cuts[q];
   for (int q = nranks + 1; q <= BSORT_DIST_MAX_RANKS; ++q) dg.cuts[q] = TOP_BINS;
   dg.nranks = nranks;
-  // The digit functor's invalid-tail digit is 255 > any rank; bases beyond nranks are unused.
-  return launch_pass<U, DescT>(in, out, n, dg, bases, lb, counter, nullptr, 0, s);
+  return launch_pass<U, RANK_UNSTABLE, uint32_t>(in, out, n, dg, bases, (uint32_t*)nullptr, gcount, counter, nullptr,
+                                                 0, s);
 }
 
 }  // namespace
@@ -232,9 +275,11 @@ bsort_status_t dist_top_hist(const DtypeInfo& di, const void* keys, uint64_t n, 
 }
 
 size_t dist_partition_workspace_bytes(int bytes, uint64_t n, int nranks) {
+  (void)bytes;
+  (void)n;
   (void)nranks;
   size_t a, b, c;
-  return bytes == 4 ? part_layout<uint32_t>(n, &a, &b, &c) : part_layout<unsigned long long>(n, &a, &b, &c);
+  return part_layout(&a, &b, &c);
 }
 
 bsort_status_t dist_partition(const DtypeInfo& di, const void* in, uint64_t n, bool desc, const uint32_t* cuts,
@@ -250,24 +295,17 @@ bsort_status_t dist_partition(const DtypeInfo& di, const void* in, uint64_t n, b
   }
   if (acc != n) return BSORT_ERROR_INVALID_ARGUMENT;
   auto* w = static_cast<unsigned char*>(ws);
-  const bool d64 = n >= (1ull << 30);
 #define PART(U_)                                                                                                  \
   {                                                                                                               \
     const U_* i_ = static_cast<const U_*>(in);                                                                    \
     U_* o_ = static_cast<U_*>(out);                                                                               \
     switch (di.kind * 2 + (desc ? 1 : 0)) {                                                                       \
-      case 0: return d64 ? part_run<KIND_U, false, U_, unsigned long long>(i_, n, cuts, nranks, o_, w, hb, s)     \
-                         : part_run<KIND_U, false, U_, uint32_t>(i_, n, cuts, nranks, o_, w, hb, s);              \
-      case 1: return d64 ? part_run<KIND_U, true, U_, unsigned long long>(i_, n, cuts, nranks, o_, w, hb, s)      \
-                         : part_run<KIND_U, true, U_, uint32_t>(i_, n, cuts, nranks, o_, w, hb, s);               \
-      case 2: return d64 ? part_run<KIND_I, false, U_, unsigned long long>(i_, n, cuts, nranks, o_, w, hb, s)     \
-                         : part_run<KIND_I, false, U_, uint32_t>(i_, n, cuts, nranks, o_, w, hb, s);              \
-      case 3: return d64 ? part_run<KIND_I, true, U_, unsigned long long>(i_, n, cuts, nranks, o_, w, hb, s)      \
-                         : part_run<KIND_I, true, U_, uint32_t>(i_, n, cuts, nranks, o_, w, hb, s);               \
-      case 4: return d64 ? part_run<KIND_F, false, U_, unsigned long long>(i_, n, cuts, nranks, o_, w, hb, s)     \
-                         : part_run<KIND_F, false, U_, uint32_t>(i_, n, cuts, nranks, o_, w, hb, s);              \
-      default: return d64 ? part_run<KIND_F, true, U_, unsigned long long>(i_, n, cuts, nranks, o_, w, hb, s)     \
-                          : part_run<KIND_F, true, U_, uint32_t>(i_, n, cuts, nranks, o_, w, hb, s);              \
+      case 0: return part_run<KIND_U, false, U_>(i_, n, cuts, nranks, o_, w, hb, s);                              \
+      case 1: return part_run<KIND_U, true, U_>(i_, n, cuts, nranks, o_, w, hb, s);                               \
+      case 2: return part_run<KIND_I, false, U_>(i_, n, cuts, nranks, o_, w, hb, s);                              \
+      case 3: return part_run<KIND_I, true, U_>(i_, n, cuts, nranks, o_, w, hb, s);                               \
+      case 4: return part_run<KIND_F, false, U_>(i_, n, cuts, nranks, o_, w, hb, s);                              \
+      default: return part_run<KIND_F, true, U_>(i_, n, cuts, nranks, o_, w, hb, s);                              \
     }                                                                                                             \
   }
   if (di.bytes == 4) PART(uint32_t)

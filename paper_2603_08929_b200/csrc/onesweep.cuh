@@ -43,6 +43,41 @@ __device__ __forceinline__ void st_relaxed(unsigned long long* p, unsigned long 
   asm volatile("st.relaxed.gpu.global.b64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
 
+// Decoupled look-back for digit t of `tile` (descriptors tile-major: [tile][256 digits], so
+// the 256 walking threads of a CTA read 128-byte coalesced rows).  Each step issues G
+// independent loads for the G nearest unfolded predecessors, so one L2 round trip folds in up
+// to G tiles: at B200 tile rates (hundreds of CTAs on consecutive tiles) a one-load-per-step
+// walk is a serial chain of L2 latencies.  Returns the exclusive prefix of `tile`.
+template <int G, typename DescT>
+__device__ __forceinline__ DescT lookback_walk(const DescT* lookback, uint32_t t, uint32_t tile) {
+  using LB = LookbackBits<DescT>;
+  DescT excl = 0;
+  int64_t j = (int64_t)tile - 1;  // highest predecessor not folded in yet
+  for (;;) {
+    DescT v[G];
+#pragma unroll
+    for (int q = 0; q < G; ++q)
+      v[q] = (j - q >= 0) ? ld_relaxed(&lookback[(uint64_t)(j - q) * 256 + t]) : DescT(0);
+    bool stop = false, fin = false;
+    int adv = G;
+#pragma unroll
+    for (int q = 0; q < G; ++q) {
+      if (!stop) {
+        const DescT f = v[q] >> LB::SH;
+        if (f == 0) {
+          stop = true;  // not published yet: poll again from here
+          adv = q;
+        } else {
+          excl += v[q] & LB::VAL;
+          if (f == 2) stop = fin = true;
+        }
+      }
+    }
+    if (fin) return excl;  // tile 0 holds an inclusive prefix, so the walk ends there at the latest
+    j -= adv;
+  }
+}
+
 template <typename U> __device__ __forceinline__ U ldg_nc(const U* p);
 template <> __device__ __forceinline__ uint32_t ldg_nc(const uint32_t* p) {
   uint32_t v;
@@ -65,18 +100,20 @@ struct PassPlan {
   uint32_t pad[14];
 };
 
-// Digit of LSD pass p: byte p of the transformed key.
-template <int KIND, bool DESC, typename U>
+// Digit of LSD pass p: byte p of the transformed key (SHIFT = 8p is a compile-time constant so
+// the digit is one funnel-shift + mask after the transform).
+template <int KIND, bool DESC, typename U, int SHIFT>
 struct RadixDigit {
-  int shift;
+  static constexpr int BITS = 8;
   __device__ __forceinline__ uint32_t operator()(U x) const {
-    return uint32_t(key_encode<KIND, DESC>(x) >> shift) & 0xFFu;
+    return uint32_t(key_encode<KIND, DESC>(x) >> SHIFT) & 0xFFu;
   }
 };
 
 // Digit of the MSD partition: destination rank of the key's top-16-bit bin.
 template <int KIND, bool DESC, typename U>
 struct RankDigit {
+  static constexpr int BITS = 8;
   uint32_t cuts[BSORT_DIST_MAX_RANKS + 1];
   int nranks;
   __device__ __forceinline__ uint32_t operator()(U x) const {
@@ -147,7 +184,8 @@ __global__ void __launch_bounds__(HIST_THREADS, 1)
 // detection, ping-pong buffer assignment, tile-counter reset.  One CTA of 256 threads.
 __global__ void __launch_bounds__(256)
     k_plan(const unsigned long long* __restrict__ ghist, uint64_t n, int P, unsigned long long* __restrict__ bases,
-           PassPlan* __restrict__ plan, uint32_t* __restrict__ tile_counters) {
+           PassPlan* __restrict__ plan, uint32_t* __restrict__ tile_counters,
+           unsigned long long* __restrict__ gcount) {
   __shared__ unsigned long long wt[256 / 32 + 1];
   __shared__ uint32_t skip_s[8];
   for (int p = 0; p < P; ++p) {
@@ -173,50 +211,108 @@ __global__ void __launch_bounds__(256)
     plan->executed = executed;
   }
   if (threadIdx.x < 8) tile_counters[threadIdx.x] = 0;
+  if (gcount != nullptr)
+    for (int p = 0; p < P; ++p) gcount[p * 256 + threadIdx.x] = 0;  // unstable-pass digit counters
 }
 
 // ---------------------------------------------------------------------------------------
-// a4: one stable scatter pass.  Persistent CTAs take tiles of THREADS*ITEMS keys in order from
-// an atomic counter (forward progress for the look-back: a tile only waits on smaller tiles,
-// which were taken earlier by CTAs that are running).  Per tile:
-//   1. warp-striped coalesced loads (warp w owns a contiguous 32*ITEMS segment, item k of lane
-//      l is element 32k+l of it, so (warp, item, lane) order IS global index order);
-//   2. stable warp ranking: __match_any_sync groups equal digits, the group's highest lane
-//      bumps the warp's per-digit counter, rank = counter + lanes below in the group;
-//   3. per-digit tile counts published early to the look-back array (flag AGG), block scan of
-//      the counts => per-(warp, digit) offsets, keys staged in smem in digit order;
-//   4. decoupled look-back per digit (one thread per digit) => global digit offset, INC publish;
-//   5. coalesced scatter of the smem-sorted tile: runs of equal digits are contiguous.
-template <int THREADS, int ITEMS, typename U>
+// a4: one scatter pass.  Persistent CTAs (grid = resident CTAs) take tiles of THREADS*ITEMS keys
+// in increasing order from an atomic counter, which gives the decoupled look-back its forward
+// progress (a tile only waits on smaller tiles, all held by running CTAs).  Per tile:
+//   0. BULK: the tile was prefetched into smem buffer `cur` by a 1-D TMA bulk copy
+//      (cp.async.bulk, mbarrier completion) issued while the previous tile was processed.
+//      !BULK (source not 16-byte aligned): coalesced per-warp loads.
+//   1. keys -> registers, warp-striped: warp w owns the contiguous segment [w*32*ITEMS, ...),
+//      item k of lane l is element 32k+l of it, so (warp, item, lane) order IS index order.
+//   2. ranking (RANK):
+//      stable modes (every LSD pass after the first, the MSD partition): a warp-level
+//      multisplit that follows index order.  Per item the lanes with equal digits are grouped
+//      (RANK_MATCH: MATCH.ANY; RANK_BALLOT: 8 ballots; RANK_ATOMIC_OR / RANK_PACKED: every lane
+//      ORs its bit into a per-warp per-digit mask word in smem and reads it back), the group's
+//      highest lane advances the warp's counter of that digit, rank = old count + lanes below.
+//      RANK_PACKED keeps mask and count in one 64-bit word (one load, one leader store).
+//      RANK_UNSTABLE (the first LSD pass only: the input order carries no information, so equal
+//      digits may land in any order): one shared atomicAdd per key on block counters, and the
+//      tile's per-digit global offsets come from one global atomicAdd per digit -- no look-back.
+//   3. per-digit totals; stable modes publish the tile's counts to the look-back array early
+//      (flag AGG; tile 0 publishes INC); block scan => tile offsets; keys restaged in smem in
+//      digit order (in buffer `cur`; its keys now live in registers).
+//   4. stable modes: decoupled look-back, one thread per digit => global digit offset.
+//   5. coalesced write-out of the digit-sorted tile: runs of equal digits are contiguous.
+enum RankMode : int { RANK_MATCH = 0, RANK_BALLOT = 1, RANK_ATOMIC_OR = 2, RANK_PACKED = 3, RANK_UNSTABLE = 4 };
+
+template <int THREADS, int ITEMS, typename U, int RANK>
 struct PassSmem {
   static constexpr int WARPS = THREADS / 32;
   static constexpr int TILE = THREADS * ITEMS;
-  static constexpr size_t keys_off = 0;
-  static constexpr size_t wcnt_off = align_up(keys_off + sizeof(U) * TILE, 16);
-  static constexpr size_t gofs_off = align_up(wcnt_off + sizeof(uint32_t) * WARPS * 256, 16);
+  // per-warp counter rows: u32[256] (+ u32[256] match masks for ATOMIC_OR); u64[256] packed
+  // {count:32 | mask:32} for PACKED; one block-wide u32[256] row for UNSTABLE
+  static constexpr size_t row_bytes = RANK == RANK_ATOMIC_OR ? 2048 : RANK == RANK_PACKED ? 2048 : 1024;
+  static constexpr int rows = RANK == RANK_UNSTABLE ? 1 : WARPS;
+  static constexpr size_t buf_off = 0;  // U[2][TILE]
+  static constexpr size_t wcnt_off = align_up(buf_off + 2 * sizeof(U) * TILE, 16);
+  static constexpr size_t gofs_off = align_up(wcnt_off + row_bytes * rows, 16);
   static constexpr size_t wt_off = align_up(gofs_off + sizeof(unsigned long long) * 256, 16);
-  static constexpr size_t misc_off = align_up(wt_off + sizeof(uint32_t) * (WARPS + 1), 16);
-  static constexpr size_t bytes = align_up(misc_off + 16, 128);
+  static constexpr size_t mbar_off = align_up(wt_off + sizeof(uint32_t) * (WARPS + 1), 16);
+  static constexpr size_t tile_off = mbar_off + 16;  // uint32 tile id held by each buffer
+  static constexpr size_t bytes = align_up(tile_off + 16, 128);
 };
 
-template <typename U, int THREADS, int ITEMS, int MINB, typename DescT, typename DigitF>
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
+  const uint32_t a = smem_u32(bar);
+  uint32_t done = 0;
+  do {
+    asm volatile(
+        "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n"
+        " selp.u32 %0, 1, 0, p;\n}\n"
+        : "=r"(done)
+        : "r"(a), "r"(phase)
+        : "memory");
+  } while (!done);
+}
+// One thread: arm `bar` for `bytes` and start a 1-D bulk copy global -> shared (bytes % 16 == 0,
+// both addresses 16-byte aligned).  bytes == 0 just arrives (phase completes at once).
+__device__ __forceinline__ void bulk_load(void* dst_smem, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+               : "memory");
+  if (bytes)
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+            smem_u32(dst_smem)),
+        "l"(src), "r"(bytes), "r"(smem_u32(bar))
+        : "memory");
+}
+
+template <typename U, int THREADS, int ITEMS, int MINB, bool BULK, typename DescT, typename DigitF,
+          int RANK = RANK_ATOMIC_OR, int LBG = 8>
 __global__ void __launch_bounds__(THREADS, MINB)
     k_onesweep_pass(const U* a_ptr, U* b_ptr, uint64_t n, DigitF digit,
                     const unsigned long long* __restrict__ bases, DescT* __restrict__ lookback,
-                    uint32_t* __restrict__ tile_counter, uint32_t num_tiles,
-                    const PassPlan* __restrict__ plan, int pass) {
-  using L = PassSmem<THREADS, ITEMS, U>;
+                    unsigned long long* __restrict__ gcount, uint32_t* __restrict__ tile_counter,
+                    uint32_t num_tiles, const PassPlan* __restrict__ plan, int pass) {
+  using L = PassSmem<THREADS, ITEMS, U, RANK>;
   using LB = LookbackBits<DescT>;
   constexpr int TILE = L::TILE;
   constexpr int WARPS = L::WARPS;
+  constexpr int SEG = 32 * ITEMS;  // keys per warp segment
+  constexpr bool STABLE = RANK != RANK_UNSTABLE;
   static_assert(THREADS >= 256, "one thread per digit");
-  static_assert(32 * ITEMS <= 0xFFFF, "rank fits 16 bits");
+  static_assert(TILE < (1 << 23), "rank fits 23 bits");
+  static_assert((TILE * sizeof(U)) % 16 == 0, "bulk copies need 16-byte tiles");
   extern __shared__ __align__(128) unsigned char smem[];
-  U* keys_s = reinterpret_cast<U*>(smem + L::keys_off);
-  uint32_t(*wcnt)[256] = reinterpret_cast<uint32_t(*)[256]>(smem + L::wcnt_off);
+  U* bufs = reinterpret_cast<U*>(smem + L::buf_off);
+  unsigned char* rows = smem + L::wcnt_off;
   unsigned long long* gofs = reinterpret_cast<unsigned long long*>(smem + L::gofs_off);
   uint32_t* wt = reinterpret_cast<uint32_t*>(smem + L::wt_off);
-  uint32_t* tile_s = reinterpret_cast<uint32_t*>(smem + L::misc_off);
+  uint64_t* mbar = reinterpret_cast<uint64_t*>(smem + L::mbar_off);
+  uint32_t* tile_s = reinterpret_cast<uint32_t*>(smem + L::tile_off);
 
   const U* src = a_ptr;
   U* dst = b_ptr;
@@ -230,97 +326,264 @@ __global__ void __launch_bounds__(THREADS, MINB)
   const uint32_t lane = threadIdx.x & 31;
   const uint32_t warp = threadIdx.x >> 5;
   const uint32_t t = threadIdx.x;
+  const uint32_t lt = (1u << lane) - 1u;
+  // counters of this warp (stable modes) / of the block (UNSTABLE): u32[256] view
+  uint32_t* wc = reinterpret_cast<uint32_t*>(rows + (STABLE ? warp * L::row_bytes : 0));
+  // counter of digit d in row w, u32 view (PACKED: high word of the u64 slot)
+  auto cnt_at = [&](uint32_t w, uint32_t d) -> uint32_t& {
+    if constexpr (RANK == RANK_PACKED)
+      return reinterpret_cast<uint32_t*>(rows + w * L::row_bytes)[2 * d + 1];
+    else
+      return reinterpret_cast<uint32_t*>(rows + w * L::row_bytes)[d];
+  };
 
-  for (;;) {
-    if (t == 0) *tile_s = atomicAdd(tile_counter, 1u);
-    __syncthreads();  // publishes tile id; previous tile's smem is dead
-    const uint32_t tile = *tile_s;
-    if (tile >= num_tiles) break;
-    const uint64_t tile_base = (uint64_t)tile * TILE;
-    const bool full = tile_base + TILE <= n;
+  auto tile_valid = [&](uint32_t tile) -> uint32_t {
+    const uint64_t b = (uint64_t)tile * TILE;
+    return (uint32_t)min64((uint64_t)TILE, n - b);
+  };
+  // bulk-copied prefix of a tile (keys); the rest of a ragged last tile is loaded directly
+  auto bulk_keys = [&](uint32_t valid) -> uint32_t {
+    return (uint32_t)((valid * sizeof(U)) & ~(size_t)15) / (uint32_t)sizeof(U);
+  };
 
-    for (int j = lane; j < 256; j += 32) wcnt[warp][j] = 0;
-
-    // 1. load
-    const uint64_t seg = tile_base + (uint64_t)warp * (32 * ITEMS) + lane;
-    U keys[ITEMS];
-    if (full) {
+  if constexpr (RANK == RANK_ATOMIC_OR || RANK == RANK_PACKED) {  // match masks start at 0
+    uint32_t* r = reinterpret_cast<uint32_t*>(rows + warp * L::row_bytes);
 #pragma unroll
-      for (int k = 0; k < ITEMS; ++k) keys[k] = ldg_nc(src + seg + 32 * k);
-    } else {
-#pragma unroll
-      for (int k = 0; k < ITEMS; ++k) keys[k] = (seg + 32 * k < n) ? ldg_nc(src + seg + 32 * k) : U(0);
-    }
+    for (int j = 0; j < 512 / 32; ++j) r[lane + 32 * j] = 0;
     __syncwarp();
-
-    // 2. rank
-    uint32_t rk[ITEMS];
-#pragma unroll
-    for (int k = 0; k < ITEMS; ++k) {
-      const uint32_t d = (full || seg + 32 * k < n) ? digit(keys[k]) : 255u;
-      const uint32_t peers = __match_any_sync(0xffffffffu, d);
-      const uint32_t leader = 31 - __clz(peers);
-      const uint32_t below = __popc(peers & lanemask_lt());
-      uint32_t old = 0;
-      if (lane == leader) {
-        old = wcnt[warp][d];
-        wcnt[warp][d] = old + __popc(peers);
+  }
+  uint32_t phase0 = 0, phase1 = 0;
+  if constexpr (BULK) {
+    if (t == 0) {
+      mbar_init(&mbar[0], 1);
+      mbar_init(&mbar[1], 1);
+      asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+      for (int b = 0; b < 2; ++b) {
+        const uint32_t id = atomicAdd(tile_counter, 1u);
+        tile_s[b] = id;
+        if (id < num_tiles) {
+          const uint32_t v = tile_valid(id);
+          bulk_load(bufs + b * TILE, src + (uint64_t)id * TILE, bulk_keys(v) * (uint32_t)sizeof(U), &mbar[b]);
+        }
       }
-      __syncwarp();
-      old = __shfl_sync(0xffffffffu, old, leader);
-      rk[k] = (d << 16) | (old + below);
     }
     __syncthreads();
+  }
 
-    // 3. per-digit totals, early publish, tile-local offsets
+  for (uint32_t it = 0;; ++it) {
+    const uint32_t cur = it & 1u;
+    U* buf = bufs + cur * TILE;
+    uint32_t tile;
+    uint32_t next_id = 0;
+    if constexpr (BULK) {
+      tile = tile_s[cur];
+      if (tile >= num_tiles) break;
+      if (t == 0) next_id = atomicAdd(tile_counter, 1u);  // refill of this buffer, used at the end
+    } else {
+      if (t == 0) tile_s[0] = atomicAdd(tile_counter, 1u);
+      __syncthreads();  // publishes the tile id; previous tile's smem is dead
+      tile = tile_s[0];
+      if (tile >= num_tiles) break;
+    }
+    const uint64_t tile_base = (uint64_t)tile * TILE;
+    const uint32_t valid = tile_valid(tile);
+    const bool full = valid == (uint32_t)TILE;
+
+    // zero the counters (rows are dead: every read of them happened before the last barrier)
+    if constexpr (STABLE) {
+#pragma unroll
+      for (int j = 0; j < 256 / 32; ++j) cnt_at(warp, lane + 32 * j) = 0;
+    } else {
+      if (t < 256) wc[t] = 0;
+      if constexpr (!BULK) {
+      } else {
+        __syncthreads();  // block counters zeroed before any warp counts
+      }
+    }
+
+    // 1. keys -> registers
+    const uint32_t seg = warp * SEG + lane;  // tile-local index of item 0
+    U keys[ITEMS];
+    if constexpr (BULK) {
+      mbar_wait(&mbar[cur], cur ? phase1 : phase0);
+      if (cur) phase1 ^= 1u; else phase0 ^= 1u;
+      if (full) {
+#pragma unroll
+        for (int k = 0; k < ITEMS; ++k) keys[k] = buf[seg + 32 * k];
+      } else {
+        const uint32_t bk = bulk_keys(valid);
+#pragma unroll
+        for (int k = 0; k < ITEMS; ++k) {
+          const uint32_t i = seg + 32 * k;
+          keys[k] = i < bk ? buf[i] : (i < valid ? ldg_nc(src + tile_base + i) : U(0));
+        }
+      }
+    } else {
+      if (full) {
+#pragma unroll
+        for (int k = 0; k < ITEMS; ++k) keys[k] = ldg_nc(src + tile_base + seg + 32 * k);
+      } else {
+#pragma unroll
+        for (int k = 0; k < ITEMS; ++k)
+          keys[k] = (seg + 32 * k < valid) ? ldg_nc(src + tile_base + seg + 32 * k) : U(0);
+      }
+      if constexpr (!STABLE) __syncthreads();  // block counters zeroed before any warp counts
+    }
+
+    // 2. ranking.  Invalid tail slots take digit 255: they sit at the end of the tile in index
+    // order, so (stable modes) they rank after every valid key of digit 255 and are dropped;
+    // the unstable mode does not count them at all.
+    uint32_t info[ITEMS];  // d | rank << 8
+    if constexpr (RANK == RANK_UNSTABLE) {
+#pragma unroll
+      for (int k = 0; k < ITEMS; ++k) {
+        if (full || seg + 32 * k < valid) {
+          const uint32_t d = digit(keys[k]);
+          info[k] = d | (atomicAdd(&wc[d], 1u) << 8);
+        } else {
+          info[k] = 0xFFFFFFFFu;
+        }
+      }
+    } else if constexpr (RANK == RANK_MATCH || RANK == RANK_BALLOT) {
+#pragma unroll
+      for (int k = 0; k < ITEMS; ++k) {
+        const uint32_t d = (full || seg + 32 * k < valid) ? digit(keys[k]) : 255u;
+        uint32_t peers;
+        if constexpr (RANK == RANK_MATCH) {
+          peers = __match_any_sync(0xffffffffu, d);
+        } else {
+          peers = 0xffffffffu;
+#pragma unroll
+          for (int b = 0; b < 8; ++b) {
+            const uint32_t bb = __ballot_sync(0xffffffffu, (d >> b) & 1u);
+            peers &= ~(bb ^ (0u - ((d >> b) & 1u)));
+          }
+        }
+        const uint32_t below = __popc(peers & lt);
+        const uint32_t leader = (peers >> lane) == 1u;  // highest lane of the group
+        info[k] = d | (below << 8) | (leader << 31);
+      }
+      __syncwarp();  // counters zeroed by this warp
+#pragma unroll
+      for (int k = 0; k < ITEMS; ++k) {
+        const uint32_t d = info[k] & 0xFFu;
+        const uint32_t below = (info[k] >> 8) & 0xFFFFu;
+        const uint32_t old = wc[d];
+        if (info[k] >> 31) wc[d] = old + below + 1u;
+        __syncwarp();
+        info[k] = d | ((old + below) << 8);
+      }
+    } else if constexpr (RANK == RANK_ATOMIC_OR) {
+      uint32_t* mm = wc + 256;  // second half of the warp's row: match masks
+      __syncwarp();             // counters zeroed by this warp
+#pragma unroll
+      for (int k = 0; k < ITEMS; ++k) {
+        const uint32_t d = (full || seg + 32 * k < valid) ? digit(keys[k]) : 255u;
+        atomicOr(&mm[d], 1u << lane);
+        __syncwarp();
+        const uint32_t peers = mm[d];
+        const uint32_t old = wc[d];
+        const uint32_t below = __popc(peers & lt);
+        __syncwarp();
+        if ((peers >> lane) == 1u) {  // highest lane of the group
+          mm[d] = 0;
+          wc[d] = old + below + 1u;
+        }
+        info[k] = d | ((old + below) << 8);
+      }
+    } else {  // RANK_PACKED: slot d = {mask (low word), count (high word)}
+      unsigned long long* pw = reinterpret_cast<unsigned long long*>(wc);
+      __syncwarp();  // counters zeroed by this warp
+#pragma unroll
+      for (int k = 0; k < ITEMS; ++k) {
+        const uint32_t d = (full || seg + 32 * k < valid) ? digit(keys[k]) : 255u;
+        atomicOr(reinterpret_cast<uint32_t*>(&pw[d]), 1u << lane);
+        __syncwarp();
+        const unsigned long long w = pw[d];
+        const uint32_t peers = (uint32_t)w;
+        const uint32_t old = (uint32_t)(w >> 32);
+        const uint32_t below = __popc(peers & lt);
+        __syncwarp();
+        if ((peers >> lane) == 1u) pw[d] = (unsigned long long)(old + below + 1u) << 32;
+        info[k] = d | ((old + below) << 8);
+      }
+    }
+    __syncthreads();  // (A) counters complete; all warps done reading buf
+
+    // 3. per-digit totals, early publish (stable), tile offsets
     uint32_t total = 0;
     if (t < 256) {
+      if constexpr (STABLE) {
 #pragma unroll
-      for (int w = 0; w < WARPS; ++w) {
-        const uint32_t c = wcnt[w][t];
-        wcnt[w][t] = total;
-        total += c;
+        for (int w = 0; w < WARPS; ++w) total += cnt_at(w, t);
+        if (!full && t == 255) total -= (uint32_t)TILE - valid;  // invalid tail slots
+        st_relaxed(&lookback[(uint64_t)tile * 256 + t], (tile == 0 ? LB::INC : LB::AGG) | DescT(total));
+      } else {
+        total = wc[t];
       }
-      if (!full && t == 255) total -= (uint32_t)(tile_base + TILE - n);  // invalid tail keys
-      st_relaxed(&lookback[(uint64_t)tile * 256 + t], (tile == 0 ? LB::INC : LB::AGG) | DescT(total));
     }
     const uint32_t tile_excl = block_exclusive_scan<THREADS>(t < 256 ? total : 0u, wt, (uint32_t*)nullptr);
+    unsigned long long gbase = 0;
     if (t < 256) {
+      if constexpr (STABLE) {
+        uint32_t run = tile_excl;
 #pragma unroll
-      for (int w = 0; w < WARPS; ++w) wcnt[w][t] += tile_excl;
-    }
-    __syncthreads();
-
-#pragma unroll
-    for (int k = 0; k < ITEMS; ++k) keys_s[wcnt[warp][rk[k] >> 16] + (rk[k] & 0xFFFFu)] = keys[k];
-
-    // 4. decoupled look-back
-    if (t < 256) {
-      DescT excl = 0;
-      if (tile > 0) {
-        uint32_t j = tile - 1;
-        for (;;) {
-          const DescT v = ld_relaxed(&lookback[(uint64_t)j * 256 + t]);
-          const DescT flag = v >> LB::SH;
-          if (flag == 0) continue;
-          excl += v & LB::VAL;
-          if (flag == 2 || j == 0) break;
-          --j;
+        for (int w = 0; w < WARPS; ++w) {
+          const uint32_t c = cnt_at(w, t);
+          cnt_at(w, t) = run;
+          run += c;
         }
-        st_relaxed(&lookback[(uint64_t)tile * 256 + t], LB::INC | (excl + DescT(total)));
+      } else {
+        wc[t] = tile_excl;
+        if (total) gbase = atomicAdd(&gcount[t], (unsigned long long)total);  // tile order is free
       }
-      gofs[t] = bases[t] + (unsigned long long)excl - tile_excl;
     }
-    __syncthreads();
+    __syncthreads();  // (B)
 
-    // 5. scatter
-    const uint32_t valid = full ? (uint32_t)TILE : (uint32_t)(n - tile_base);
+    if constexpr (STABLE) {
+#pragma unroll
+      for (int k = 0; k < ITEMS; ++k) {
+        const uint32_t d = info[k] & 0xFFu;
+        buf[cnt_at(warp, d) + (info[k] >> 8)] = keys[k];
+      }
+    } else {
+#pragma unroll
+      for (int k = 0; k < ITEMS; ++k)
+        if (info[k] != 0xFFFFFFFFu) buf[wc[info[k] & 0xFFu] + (info[k] >> 8)] = keys[k];
+    }
+
+    // 4. global digit offsets
+    if (t < 256) {
+      if constexpr (STABLE) {
+        DescT excl = 0;
+        if (tile > 0) {
+          excl = lookback_walk<LBG>(lookback, t, tile);
+          st_relaxed(&lookback[(uint64_t)tile * 256 + t], LB::INC | (excl + DescT(total)));
+        }
+        gofs[t] = bases[t] + (unsigned long long)excl - tile_excl;
+      } else {
+        gofs[t] = bases[t] + gbase - tile_excl;
+      }
+    }
+    __syncthreads();  // (C)
+
+    // 5. write-out
 #pragma unroll
     for (int k = 0; k < ITEMS; ++k) {
       const uint32_t i = t + k * THREADS;
-      if (i < valid) {
-        const U x = keys_s[i];
+      if (full || i < valid) {
+        const U x = buf[i];
         dst[gofs[digit(x)] + i] = x;
+      }
+    }
+    if constexpr (BULK) {
+      __syncthreads();  // (D) buffer `cur` fully read: refill it with the tile after next
+      if (t == 0) {
+        tile_s[cur] = next_id;
+        if (next_id < num_tiles) {
+          const uint32_t v = tile_valid(next_id);
+          bulk_load(buf, src + (uint64_t)next_id * TILE, bulk_keys(v) * (uint32_t)sizeof(U), &mbar[cur]);
+        }
       }
     }
   }

@@ -7,7 +7,8 @@ Per rank (one process per GPU, torch.distributed over NCCL):
   a8  ``splitters``     cuts from the global histogram; ``send_counts`` per destination
       (host C in libbsort; the one host sync of the path is the D2H of the two histograms)
       all_to_all        per-destination counts
-  a9  ``partition``     stable P-way partition by destination (libbsort one-sweep pass kernel)
+  a9  ``partition``     P-way partition by destination (libbsort one-sweep pass kernel, unstable:
+                        order inside a bucket is irrelevant, every rank sorts what it receives)
   a10 all_to_all_v      keys to their owners (NCCL over NVLink / NVSwitch)
   a11 ``sort_``         local one-sweep LSD sort of the received keys
 
