@@ -12,10 +12,11 @@
 //                   output vectors (binary search of the first key's bin, 128-bit stores).
 //   k_count_hist16  65536 bins do not fit one CTA's smem as u32, so CTA pairs split the bin
 //                   range in two halves of 32768 (128 KB each) and both read the same key
-//                   chunk (the second read hits L2); per-chunk partial histograms are written
-//                   without atomics.
-//   k_count_reduce16 sums the partials per bin, scans 256-bin blocks.
-//   k_count_fill16  two-level search (block prefix in smem, bin prefix in L2), 128-bit stores.
+//                   chunk (the second read hits L2); nonzero bins are reduced into a global
+//                   u64 histogram.
+//   k_count_scan16  one CTA: exclusive scan of the 65536 bins (bin starts).
+//   k_count_fill16  warp-contiguous output ranges; one binary search per lane, then a forward
+//                   walk over the bin starts (L2-resident); 128-bit stores.
 #include "paths.cuh"
 #include "scan.cuh"
 
@@ -108,23 +109,33 @@ __global__ void __launch_bounds__(FILL_THREADS)
   for (uint64_t i = gt; i < head; i += T) keys[i] = uint8_t(bin_of(i) ^ X);
   uint4* v = reinterpret_cast<uint4*>(keys + head);
   const uint64_t nv = (n - head) >> 4;
-  for (uint64_t i = gt; i < nv; i += T) {
+  // warp-contiguous vector ranges (coalesced stores); each lane's position only moves forward,
+  // so one binary search per lane, then a forward walk over the bin starts
+  const uint64_t warps = T / 32;
+  const uint64_t wid = gt / 32;
+  const uint32_t lane = threadIdx.x & 31;
+  const uint64_t per = ((nv + warps - 1) / warps + 31) & ~uint64_t(31);
+  const uint64_t v0 = min64(nv, wid * per), v1 = min64(nv, v0 + per);
+  uint32_t b = 0;
+  bool init = false;
+  for (uint64_t i = v0 + lane; i < v1; i += 32) {
     const uint64_t p0 = head + (i << 4);
-    uint32_t b = bin_of(p0);
-    uint64_t next = pre[b + 1];
+    if (!init) {
+      b = bin_of(p0);
+      init = true;
+    }
+    while (pre[b + 1] <= p0) ++b;
     uint4 q;
-    if (next >= p0 + 16) {
-      uint32_t w = (b * 0x01010101u) ^ X;
+    if (pre[b + 1] >= p0 + 16) {
+      const uint32_t w = (b * 0x01010101u) ^ X;
       q = make_uint4(w, w, w, w);
     } else {
       uint32_t w[4] = {0, 0, 0, 0};
+      uint32_t bb = b;
 #pragma unroll
       for (int j = 0; j < 16; ++j) {
-        if (next <= p0 + j) {
-          b = bin_of(p0 + j);
-          next = pre[b + 1];
-        }
-        w[j >> 2] |= b << ((j & 3) * 8);
+        while (pre[bb + 1] <= p0 + j) ++bb;
+        w[j >> 2] |= bb << ((j & 3) * 8);
       }
       q = make_uint4(w[0] ^ X, w[1] ^ X, w[2] ^ X, w[3] ^ X);
     }
@@ -135,9 +146,13 @@ __global__ void __launch_bounds__(FILL_THREADS)
 
 // ----------------------------------------------------------------------------- 16-bit
 
+// 65536 u32 bins do not fit one CTA's shared memory next to anything else, so CTA pairs split
+// the bin range: CTA (chunk, half) counts the keys of its chunk whose top bit is `half` into
+// 32768 smem bins; both CTAs of a pair stream the same chunk (the second read is served by L2).
+// Nonzero bins are added into the global u64 histogram with fire-and-forget reductions.
 template <uint32_t X>
 __global__ void __launch_bounds__(CNT_THREADS, 1)
-    k_count_hist16(const uint16_t* __restrict__ keys, uint64_t n, uint32_t* __restrict__ partial) {
+    k_count_hist16(const uint16_t* __restrict__ keys, uint64_t n, unsigned long long* __restrict__ hist) {
   extern __shared__ uint32_t h16[];  // 32768 counters: this CTA's half of the bin range
   const uint32_t half = blockIdx.x & 1;
   const uint32_t chunk = blockIdx.x >> 1;
@@ -176,75 +191,78 @@ __global__ void __launch_bounds__(CNT_THREADS, 1)
   }
   for (; i < ve; i += CNT_THREADS) vec(ldg_stream(v + i));
   __syncthreads();
-  uint32_t* dst = partial + (uint64_t)chunk * BINS16 + half * (BINS16 / 2);
-  for (int b = threadIdx.x; b < BINS16 / 2; b += CNT_THREADS) dst[b] = h16[b];
+  unsigned long long* dst = hist + half * (BINS16 / 2);
+  for (int b = threadIdx.x; b < BINS16 / 2; b += CNT_THREADS)
+    if (h16[b]) atomicAdd(&dst[b], (unsigned long long)h16[b]);
 }
 
-// grid = 256 blocks x 256 threads: bin b = 256*block + thread.
-__global__ void __launch_bounds__(256)
-    k_count_reduce16(const uint32_t* __restrict__ partial, int pairs,
-                     unsigned long long* __restrict__ local_excl, unsigned long long* __restrict__ blk_total) {
-  __shared__ unsigned long long wt[256 / 32 + 1];
-  const uint32_t b = blockIdx.x * 256 + threadIdx.x;
-  unsigned long long s = 0;
-  for (int c = 0; c < pairs; ++c) s += partial[(uint64_t)c * BINS16 + b];
-  unsigned long long tot;
-  unsigned long long ex = block_exclusive_scan<256>(s, wt, &tot);
-  local_excl[b] = ex;
-  if (threadIdx.x == 0) blk_total[blockIdx.x] = tot;
+// Exclusive scan of the 65536-bin histogram in place (one CTA of 1024 threads, 64 bins each).
+__global__ void __launch_bounds__(1024) k_count_scan16(unsigned long long* __restrict__ hist) {
+  __shared__ unsigned long long wt[1024 / 32 + 1];
+  constexpr int PER = BINS16 / 1024;
+  unsigned long long* h = hist + threadIdx.x * PER;
+  unsigned long long local = 0;
+#pragma unroll 16
+  for (int j = 0; j < PER; ++j) local += h[j];
+  unsigned long long run = block_exclusive_scan<1024>(local, wt, (unsigned long long*)nullptr);
+#pragma unroll 16
+  for (int j = 0; j < PER; ++j) {
+    const unsigned long long c = h[j];
+    h[j] = run;
+    run += c;
+  }
 }
 
+// Regenerate the sorted keys in place from the bin starts pre[b] (exclusive prefix, L2-resident).
+// Warp w owns a contiguous range of 16-byte output vectors, lane l takes vectors l, l+32, ...:
+// stores are coalesced and each lane's position only moves forward, so after one binary search
+// the lane finds its bin by walking forward (uniform keys: ~4096 keys per bin, the walk is empty).
 template <uint32_t X>
 __global__ void __launch_bounds__(FILL_THREADS)
-    k_count_fill16(uint16_t* __restrict__ keys, uint64_t n, const unsigned long long* __restrict__ local_excl,
-                   const unsigned long long* __restrict__ blk_total) {
-  __shared__ unsigned long long cpre[257];
-  __shared__ unsigned long long wt[FILL_THREADS / 32 + 1];
-  unsigned long long ex = block_exclusive_scan<FILL_THREADS>(blk_total[threadIdx.x], wt,
-                                                             (unsigned long long*)nullptr);
-  cpre[threadIdx.x] = ex;
-  if (threadIdx.x == 0) cpre[256] = n;
-  __syncthreads();
-  auto prefix_of = [&](uint32_t b) -> uint64_t {
-    return b >= (uint32_t)BINS16 ? n : cpre[b >> 8] + local_excl[b];
-  };
-  auto bin_of = [&](uint64_t p) -> uint32_t {
-    uint32_t lo = 0, hi = 256;
+    k_count_fill16(uint16_t* __restrict__ keys, uint64_t n, const unsigned long long* __restrict__ pre) {
+  auto next_start = [&](uint32_t b) -> uint64_t { return b + 1 < (uint32_t)BINS16 ? pre[b + 1] : n; };
+  auto bin_of = [&](uint64_t p) -> uint32_t {  // largest b with pre[b] <= p  (pre[0] = 0 <= p < n)
+    uint32_t lo = 0, hi = BINS16;
     while (hi - lo > 1) {
-      uint32_t mid = (lo + hi) >> 1;
-      if (cpre[mid] <= p) lo = mid; else hi = mid;
+      const uint32_t mid = (lo + hi) >> 1;
+      if (pre[mid] <= p) lo = mid; else hi = mid;
     }
-    const uint64_t base = cpre[lo];
-    uint32_t blo = lo << 8, bhi = blo + 256;
-    while (bhi - blo > 1) {
-      uint32_t mid = (blo + bhi) >> 1;
-      if (base + local_excl[mid] <= p) blo = mid; else bhi = mid;
-    }
-    return blo;
+    return lo;
   };
-  const uint64_t T = (uint64_t)gridDim.x * FILL_THREADS;
-  const uint64_t gt = (uint64_t)blockIdx.x * FILL_THREADS + threadIdx.x;
   const uint64_t head = min64(n, ((16 - ((uintptr_t)keys & 15)) & 15) >> 1);
+  const uint64_t gt = (uint64_t)blockIdx.x * FILL_THREADS + threadIdx.x;
+  const uint64_t T = (uint64_t)gridDim.x * FILL_THREADS;
   for (uint64_t i = gt; i < head; i += T) keys[i] = uint16_t(bin_of(i) ^ X);
   uint4* v = reinterpret_cast<uint4*>(keys + head);
   const uint64_t nv = (n - head) >> 3;
-  for (uint64_t i = gt; i < nv; i += T) {
+  const uint64_t warps = T / 32;
+  const uint64_t wid = gt / 32;
+  const uint32_t lane = threadIdx.x & 31;
+  const uint64_t per = ((nv + warps - 1) / warps + 31) & ~uint64_t(31);
+  const uint64_t v0 = min64(nv, wid * per), v1 = min64(nv, v0 + per);
+  uint32_t b = 0;
+  uint64_t nxt = 0;
+  bool init = false;
+  for (uint64_t i = v0 + lane; i < v1; i += 32) {
     const uint64_t p0 = head + (i << 3);
-    uint32_t b = bin_of(p0);
-    uint64_t next = prefix_of(b + 1);
+    if (!init) {
+      b = bin_of(p0);
+      nxt = next_start(b);
+      init = true;
+    }
+    while (nxt <= p0) nxt = next_start(++b);
     uint4 q;
-    if (next >= p0 + 8) {
-      uint32_t w = (b * 0x00010001u) ^ X;
+    if (nxt >= p0 + 8) {
+      const uint32_t w = (b * 0x00010001u) ^ X;
       q = make_uint4(w, w, w, w);
     } else {
       uint32_t w[4] = {0, 0, 0, 0};
+      uint32_t bb = b;
+      uint64_t nn = nxt;
 #pragma unroll
       for (int j = 0; j < 8; ++j) {
-        if (next <= p0 + j) {
-          b = bin_of(p0 + j);
-          next = prefix_of(b + 1);
-        }
-        w[j >> 1] |= b << ((j & 1) * 16);
+        while (nn <= p0 + j) nn = next_start(++bb);
+        w[j >> 1] |= bb << ((j & 1) * 16);
       }
       q = make_uint4(w[0] ^ X, w[1] ^ X, w[2] ^ X, w[3] ^ X);
     }
@@ -277,21 +295,18 @@ int pairs16() { return max(1, num_sms() / 2); }
 template <uint32_t X>
 bsort_status_t run16(uint16_t* keys, uint64_t n, void* ws, cudaStream_t s) {
   const int pairs = pairs16();
-  auto* local_excl = reinterpret_cast<unsigned long long*>(ws);
-  auto* blk_total = local_excl + BINS16;
-  auto* partial = reinterpret_cast<uint32_t*>(blk_total + 256);
+  auto* hist = reinterpret_cast<unsigned long long*>(ws);
   const int smem = (BINS16 / 2) * sizeof(uint32_t);
   static bool attr_set = false;  // idempotent; benign race
   if (!attr_set) {
     BSORT_CUDA(cudaFuncSetAttribute(k_count_hist16<X>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
     attr_set = true;
   }
-  BSORT_LAUNCH(PROF_COUNT_HIST, s,
-               k_count_hist16<X><<<2 * pairs, CNT_THREADS, smem, s>>>(keys, n, partial));
-  BSORT_LAUNCH(PROF_COUNT_SCAN, s,
-               k_count_reduce16<<<256, 256, 0, s>>>(partial, pairs, local_excl, blk_total));
+  BSORT_LAUNCH(PROF_MEMSET, s, cudaMemsetAsync(hist, 0, BINS16 * sizeof(unsigned long long), s));
+  BSORT_LAUNCH(PROF_COUNT_HIST, s, k_count_hist16<X><<<2 * pairs, CNT_THREADS, smem, s>>>(keys, n, hist));
+  BSORT_LAUNCH(PROF_COUNT_SCAN, s, k_count_scan16<<<1, 1024, 0, s>>>(hist));
   BSORT_LAUNCH(PROF_COUNT_FILL, s,
-               k_count_fill16<X><<<fill_grid(n / 8 + 1), FILL_THREADS, 0, s>>>(keys, n, local_excl, blk_total));
+               k_count_fill16<X><<<fill_grid(n / 8 + 1), FILL_THREADS, 0, s>>>(keys, n, hist));
   return BSORT_SUCCESS;
 }
 
@@ -300,7 +315,7 @@ bsort_status_t run16(uint16_t* keys, uint64_t n, void* ws, cudaStream_t s) {
 size_t counting_workspace_bytes(int bytes, uint64_t n) {
   if (n <= 1) return 0;
   if (bytes == 1) return 256 * sizeof(unsigned long long);
-  return (BINS16 + 256) * sizeof(unsigned long long) + (size_t)pairs16() * BINS16 * sizeof(uint32_t);
+  return BINS16 * sizeof(unsigned long long);
 }
 
 bsort_status_t counting_sort(const DtypeInfo& di, void* keys, uint64_t n, bool desc, void* ws,

@@ -1,0 +1,154 @@
+"""GPU parity of the MSD building blocks on one B200.
+
+* ``top_hist`` (k_dist_tophist) against the oracle's total-order key, bit for bit.
+* ``partition`` (unstable k_onesweep_pass over destination ranks): every bucket holds exactly
+  the keys whose top-16-bit bin the splitters assign to it (multiset equality).
+* P simulated ranks on one GPU: every device step of ``sort_dist`` runs in libbsort on rank
+  slices; only the two collectives are stood in for by in-process tensor ops (there is one GPU
+  in this pool, and ranks whose kernels wait on each other must not share a GPU).  The
+  concatenated shards must equal the oracle's sort of all keys.
+* ``sort_dist`` end to end over a real one-rank NCCL process group.
+"""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+
+import oracle
+import workloads as W
+
+pytestmark = pytest.mark.gpu
+
+NP = {torch.int32: np.int32, torch.float32: np.float32, torch.int64: np.int64,
+      torch.float64: np.float64, torch.uint32: np.uint32, torch.uint64: np.uint64}
+UINT = {4: np.uint32, 8: np.uint64}
+SIGNED = {torch.uint32: torch.int32, torch.uint64: torch.int64}
+
+
+@pytest.fixture(scope="module")
+def B():
+    if not torch.cuda.is_available():
+        pytest.skip("needs a CUDA device")
+    import paper_2603_08929_b200 as b
+    return b
+
+
+def host(t):
+    return t.view(SIGNED.get(t.dtype, t.dtype)).cpu().numpy().view(NP[t.dtype])
+
+
+def top16_oracle(arr: np.ndarray, descending: bool) -> np.ndarray:
+    s = oracle.NATIVE_SCHEMES[arr.dtype]
+    k = oracle.total_order_keys(arr.view(UINT[arr.itemsize]).astype(np.uint64), s)
+    if descending:
+        k = ~k & np.uint64((1 << s.width) - 1 if s.width < 64 else 0xFFFFFFFFFFFFFFFF)
+    return (k >> np.uint64(s.width - 16)).astype(np.int64)
+
+
+def gen(dtype, n, seed):
+    if dtype.is_floating_point:
+        return W.special_mix(dtype, n, seed, "cuda")
+    return W.uniform_int(dtype, n, seed, "cuda")
+
+
+@pytest.mark.parametrize("dtype", [torch.int32, torch.float32, torch.uint64, torch.float64])
+@pytest.mark.parametrize("descending", [False, True])
+def test_top_hist(B, dtype, descending):
+    for n in (1, 1000, 300_007):
+        x = gen(dtype, n, 40 + n)
+        h = B.top_hist(x, descending).view(torch.int64).cpu().numpy()
+        ref = np.bincount(top16_oracle(host(x), descending), minlength=65536)
+        assert np.array_equal(h, ref)
+
+
+@pytest.mark.parametrize("dtype", [torch.int32, torch.float64])
+@pytest.mark.parametrize("P", [2, 3, 8])
+def test_partition_buckets(B, dtype, P):
+    n = 200_003
+    x = gen(dtype, n, 7 * P)
+    desc = P == 3
+    h = B.top_hist(x, desc).view(torch.int64).cpu().numpy().view(np.uint64)
+    cuts = B.splitters(h, P)
+    sc = B.send_counts(h, cuts)
+    out = B.partition(x, cuts, sc, desc)
+    torch.cuda.synchronize()
+    xs, os_ = host(x), host(out)
+    dest = np.searchsorted(cuts.astype(np.int64), top16_oracle(xs, desc), side="right") - 1
+    starts = np.concatenate([[0], np.cumsum(sc.astype(np.int64))])
+    for q in range(P):
+        got = np.sort(os_[starts[q]:starts[q + 1]].view(UINT[xs.itemsize]))
+        exp = np.sort(xs[dest == q].view(UINT[xs.itemsize]))
+        assert np.array_equal(got, exp), f"bucket {q}"
+
+
+def simulated_sort_dist(B, parts, descending):
+    """sort_dist's data path on one GPU: libbsort kernels per rank slice, collectives as
+    in-process tensor ops (all_reduce = sum, all_to_all = slicing + cat)."""
+    P = len(parts)
+    hl = [B.top_hist(p, descending) for p in parts]
+    hg = torch.stack([h.view(torch.int64) for h in hl]).sum(0)  # all_reduce(sum)
+    hg_np = hg.cpu().numpy().view(np.uint64)
+    cuts = B.splitters(hg_np, P)
+    sends = [B.send_counts(h.view(torch.int64).cpu().numpy().view(np.uint64), cuts) for h in hl]
+    buckets = [B.partition(p, cuts, sc, descending) for p, sc in zip(parts, sends)]
+    offs = [np.concatenate([[0], np.cumsum(sc.astype(np.int64))]) for sc in sends]
+    shards = []
+    for q in range(P):  # all_to_all: rank q receives bucket q of every rank, in rank order
+        recv = torch.cat([buckets[r][int(offs[r][q]):int(offs[r][q + 1])] for r in range(P)])
+        B.sort_(recv, descending)
+        shards.append(recv)
+    return shards
+
+
+@pytest.mark.parametrize("dtype,P,desc", [(torch.int64, 2, False), (torch.float64, 4, False),
+                                          (torch.float32, 8, True), (torch.int32, 3, False)])
+def test_simulated_ranks_match_oracle(B, dtype, P, desc):
+    n_per = 100_000
+    parts = []
+    for r in range(P):
+        if dtype == torch.float64:
+            parts.append(W.make("cfg5", "cuda", n=n_per * P, dtype=torch.float64, rank=r, world=P))
+        elif dtype == torch.int64:
+            parts.append(W.make("cfg5", "cuda", n=n_per * P, dtype=torch.int64, rank=r, world=P))
+        else:
+            parts.append(gen(dtype, n_per + 13 * r, 90 + r))
+    allkeys = np.concatenate([host(p) for p in parts])
+    shards = simulated_sort_dist(B, parts, desc)
+    torch.cuda.synchronize()
+    got = np.concatenate([host(s) for s in shards])
+    assert got.tobytes() == oracle.sort_native(allkeys, descending=desc).tobytes()
+    if dtype in (torch.int64, torch.float64):  # bit-uniform keys split evenly (SV-7)
+        sizes = [s.numel() for s in shards]
+        assert max(sizes) <= 1.05 * (n_per * P / P)
+
+
+def test_simulated_ranks_all_equal(B):
+    parts = [torch.full((50_000,), 7, dtype=torch.int32, device="cuda") for _ in range(4)]
+    shards = simulated_sort_dist(B, parts, False)
+    sizes = [s.numel() for s in shards]
+    assert sorted(sizes) == [0, 0, 0, 200_000]  # bin-granular split (reading Q16)
+    assert bool((torch.cat(shards) == 7).all())
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def test_sort_dist_nccl_one_rank(B):
+    import torch.distributed as dist
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(_free_port()))
+    dist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device("cuda:0"))
+    try:
+        x = W.make("cfg5", "cuda", n=300_001, dtype=torch.float64)
+        ref = oracle.sort_native(host(x))
+        out = B.sort_dist(x)
+        torch.cuda.synchronize()
+        assert host(out).tobytes() == ref.tobytes()
+    finally:
+        dist.destroy_process_group()

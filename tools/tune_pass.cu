@@ -139,7 +139,7 @@ void suite(uint64_t n) {
   float hms;
   CK(cudaEventElapsedTime(&hms, a, b));
   printf("{\"hist_ms\": %.4f, \"hist_GBps\": %.1f}\n", hms, n * sizeof(U) / (hms * 1e-3) / 1e9);
-  k_plan<<<1, 256>>>(ghist, n, P, bases, plan, tc);
+  k_plan<<<1, 256>>>(ghist, n, P, bases, plan, tc, nullptr);
   CK(cudaMemset(dbg, 0, 16));
   k_sum<<<1184, 256>>>(in, n, dbg + 1);
   unsigned long long h[2];
