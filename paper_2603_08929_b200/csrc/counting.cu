@@ -10,13 +10,12 @@
 //                   atomics), one read of the keys with 128-bit loads, flush to 256 global u64.
 //   k_count_fill8   every CTA scans the 256 counts in smem; each thread regenerates 16-byte
 //                   output vectors (binary search of the first key's bin, 128-bit stores).
-//   k_count_hist16  65536 bins do not fit one CTA's smem as u32, so CTA pairs split the bin
-//                   range in two halves of 32768 (128 KB each) and both read the same key
-//                   chunk (the second read hits L2); nonzero bins are reduced into a global
-//                   u64 histogram.
-//   k_count_scan16  one CTA: exclusive scan of the 65536 bins (bin starts).
-//   k_count_fill16  warp-contiguous output ranges; one binary search per lane, then a forward
-//                   walk over the bin starts (L2-resident); 128-bit stores.
+//   k_count_hist16  one CTA per SM, all 65536 bins as u16 halves in 128 KB of smem (drained
+//                   to a global overflow counter at 0x8000), one read of the keys; per-CTA
+//                   rows of residual counts.
+//   k_count_scan16  64 CTAs: bin totals over the rows + overflow, block-local exclusive scan.
+//   k_count_fill16  warp-contiguous output ranges; one two-level binary search per lane, then a
+//                   forward walk over the bin starts (L2-resident); 128-bit stores.
 #include "paths.cuh"
 #include "scan.cuh"
 
@@ -146,21 +145,29 @@ __global__ void __launch_bounds__(FILL_THREADS)
 
 // ----------------------------------------------------------------------------- 16-bit
 
-// 65536 u32 bins do not fit one CTA's shared memory next to anything else, so CTA pairs split
-// the bin range: CTA (chunk, half) counts the keys of its chunk whose top bit is `half` into
-// 32768 smem bins; both CTAs of a pair stream the same chunk (the second read is served by L2).
-// Nonzero bins are added into the global u64 histogram with fire-and-forget reductions.
+constexpr int SCAN16_BLOCK = 1024;
+constexpr int SCAN16_BLOCKS = BINS16 / SCAN16_BLOCK;  // 64
+
+// One CTA per SM counts its contiguous chunk into all 65536 bins held as u16 halves of 32768 u32
+// words (128 KB of smem; each key is read once, every lane of a warp is busy).  A half that
+// reaches 0x8000 is drained: the one thread whose atomicAdd returned 0x7FFF subtracts 0x8000
+// from the half and adds 0x8000 to the bin's global overflow counter.  At most CNT_THREADS
+// increments are in flight, so a half never wraps.  The CTA's residual u16 counts are written
+// as a row of `partial` (no atomics).
 template <uint32_t X>
 __global__ void __launch_bounds__(CNT_THREADS, 1)
-    k_count_hist16(const uint16_t* __restrict__ keys, uint64_t n, unsigned long long* __restrict__ hist) {
-  extern __shared__ uint32_t h16[];  // 32768 counters: this CTA's half of the bin range
-  const uint32_t half = blockIdx.x & 1;
-  const uint32_t chunk = blockIdx.x >> 1;
-  const uint32_t pairs = gridDim.x >> 1;
+    k_count_hist16(const uint16_t* __restrict__ keys, uint64_t n, uint16_t* __restrict__ partial,
+                   unsigned long long* __restrict__ ovf) {
+  extern __shared__ uint32_t h16[];  // 32768 words: bin 2w in the low half, 2w+1 in the high half
   for (int i = threadIdx.x; i < BINS16 / 2; i += CNT_THREADS) h16[i] = 0;
   __syncthreads();
   auto add = [&](uint32_t k) {
-    if ((k >> 15) == half) atomicAdd(&h16[k & 0x7FFF], 1u);
+    const uint32_t sh = (k & 1u) << 4;
+    const uint32_t old = atomicAdd(&h16[k >> 1], 1u << sh);
+    if (((old >> sh) & 0xFFFFu) == 0x7FFFu) {
+      atomicAdd(&h16[k >> 1], 0u - (0x8000u << sh));
+      atomicAdd(&ovf[k], 0x8000ull);
+    }
   };
   auto vec = [&](uint4 q) {
     uint32_t w[4] = {q.x ^ X, q.y ^ X, q.z ^ X, q.w ^ X};
@@ -173,12 +180,12 @@ __global__ void __launch_bounds__(CNT_THREADS, 1)
   const uint64_t head = min64(n, ((16 - ((uintptr_t)keys & 15)) & 15) >> 1);
   const uint4* v = reinterpret_cast<const uint4*>(keys + head);
   const uint64_t nv = (n - head) >> 3;
-  const uint64_t per = (nv + pairs - 1) / pairs;
-  const uint64_t vs = min64(nv, (uint64_t)chunk * per);
+  const uint64_t per = (nv + gridDim.x - 1) / gridDim.x;
+  const uint64_t vs = min64(nv, (uint64_t)blockIdx.x * per);
   const uint64_t ve = min64(nv, vs + per);
-  if (chunk == 0)
+  if (blockIdx.x == 0)
     for (uint64_t i = threadIdx.x; i < head; i += CNT_THREADS) add((keys[i] ^ X) & 0xFFFF);
-  if (chunk == pairs - 1)
+  if (blockIdx.x == gridDim.x - 1)
     for (uint64_t i = head + (nv << 3) + threadIdx.x; i < n; i += CNT_THREADS) add((keys[i] ^ X) & 0xFFFF);
   uint64_t i = vs + threadIdx.x;
   for (; i + 3 * CNT_THREADS < ve; i += 4 * CNT_THREADS) {
@@ -191,43 +198,58 @@ __global__ void __launch_bounds__(CNT_THREADS, 1)
   }
   for (; i < ve; i += CNT_THREADS) vec(ldg_stream(v + i));
   __syncthreads();
-  unsigned long long* dst = hist + half * (BINS16 / 2);
-  for (int b = threadIdx.x; b < BINS16 / 2; b += CNT_THREADS)
-    if (h16[b]) atomicAdd(&dst[b], (unsigned long long)h16[b]);
+  uint32_t* row = reinterpret_cast<uint32_t*>(partial + (uint64_t)blockIdx.x * BINS16);  // same packing
+  for (int w = threadIdx.x; w < BINS16 / 2; w += CNT_THREADS) row[w] = h16[w];
 }
 
-// Exclusive scan of the 65536-bin histogram in place (one CTA of 1024 threads, 64 bins each).
-__global__ void __launch_bounds__(1024) k_count_scan16(unsigned long long* __restrict__ hist) {
-  __shared__ unsigned long long wt[1024 / 32 + 1];
-  constexpr int PER = BINS16 / 1024;
-  unsigned long long* h = hist + threadIdx.x * PER;
-  unsigned long long local = 0;
-#pragma unroll 16
-  for (int j = 0; j < PER; ++j) local += h[j];
-  unsigned long long run = block_exclusive_scan<1024>(local, wt, (unsigned long long*)nullptr);
-#pragma unroll 16
-  for (int j = 0; j < PER; ++j) {
-    const unsigned long long c = h[j];
-    h[j] = run;
-    run += c;
-  }
+// Bin totals (sum of the per-CTA rows + overflow) and exclusive scan, 64 CTAs x 1024 bins:
+// local[b] = prefix of b inside its 1024-bin block; tot[blk] = the block's total.
+__global__ void __launch_bounds__(SCAN16_BLOCK)
+    k_count_scan16(const uint16_t* __restrict__ partial, int rows, const unsigned long long* __restrict__ ovf,
+                   unsigned long long* __restrict__ local, unsigned long long* __restrict__ tot) {
+  __shared__ unsigned long long wt[SCAN16_BLOCK / 32 + 1];
+  const uint32_t b = blockIdx.x * SCAN16_BLOCK + threadIdx.x;
+  unsigned long long c = ovf[b];
+#pragma unroll 8
+  for (int r = 0; r < rows; ++r) c += partial[(uint64_t)r * BINS16 + b];
+  unsigned long long t;
+  local[b] = block_exclusive_scan<SCAN16_BLOCK>(c, wt, &t);
+  if (threadIdx.x == 0) tot[blockIdx.x] = t;
 }
 
-// Regenerate the sorted keys in place from the bin starts pre[b] (exclusive prefix, L2-resident).
-// Warp w owns a contiguous range of 16-byte output vectors, lane l takes vectors l, l+32, ...:
-// stores are coalesced and each lane's position only moves forward, so after one binary search
-// the lane finds its bin by walking forward (uniform keys: ~4096 keys per bin, the walk is empty).
+// Regenerate the sorted keys in place.  Bin starts: pre(b) = ctot[b >> 10] + local[b] (ctot in
+// smem, local L2-resident).  Warp w owns a contiguous range of 16-byte output vectors, lane l
+// takes vectors l, l+32, ...: stores are coalesced and each lane's position only moves forward,
+// so after one two-level binary search the lane finds its bin by walking forward.
 template <uint32_t X>
 __global__ void __launch_bounds__(FILL_THREADS)
-    k_count_fill16(uint16_t* __restrict__ keys, uint64_t n, const unsigned long long* __restrict__ pre) {
-  auto next_start = [&](uint32_t b) -> uint64_t { return b + 1 < (uint32_t)BINS16 ? pre[b + 1] : n; };
-  auto bin_of = [&](uint64_t p) -> uint32_t {  // largest b with pre[b] <= p  (pre[0] = 0 <= p < n)
-    uint32_t lo = 0, hi = BINS16;
+    k_count_fill16(uint16_t* __restrict__ keys, uint64_t n, const unsigned long long* __restrict__ local,
+                   const unsigned long long* __restrict__ tot) {
+  __shared__ unsigned long long ctot[SCAN16_BLOCKS + 1];
+  if (threadIdx.x < 32) {  // exclusive scan of the 64 block totals
+    unsigned long long a = tot[threadIdx.x], b2 = tot[threadIdx.x + 32];
+    const unsigned long long ia = warp_inclusive_scan(a);
+    const unsigned long long sa = __shfl_sync(0xffffffffu, ia, 31);
+    const unsigned long long ib = warp_inclusive_scan(b2) + sa;
+    ctot[threadIdx.x] = ia - a;
+    ctot[threadIdx.x + 32] = ib - b2;
+    if (threadIdx.x == 31) ctot[SCAN16_BLOCKS] = ib;
+  }
+  __syncthreads();
+  auto pre = [&](uint32_t b) -> uint64_t { return b < (uint32_t)BINS16 ? ctot[b >> 10] + local[b] : n; };
+  auto bin_of = [&](uint64_t p) -> uint32_t {  // largest b with pre(b) <= p  (pre(0) = 0 <= p < n)
+    uint32_t lo = 0, hi = SCAN16_BLOCKS;
     while (hi - lo > 1) {
       const uint32_t mid = (lo + hi) >> 1;
-      if (pre[mid] <= p) lo = mid; else hi = mid;
+      if (ctot[mid] <= p) lo = mid; else hi = mid;
     }
-    return lo;
+    const uint64_t base = ctot[lo];
+    uint32_t blo = lo * SCAN16_BLOCK, bhi = blo + SCAN16_BLOCK;
+    while (bhi - blo > 1) {
+      const uint32_t mid = (blo + bhi) >> 1;
+      if (base + local[mid] <= p) blo = mid; else bhi = mid;
+    }
+    return blo;
   };
   const uint64_t head = min64(n, ((16 - ((uintptr_t)keys & 15)) & 15) >> 1);
   const uint64_t gt = (uint64_t)blockIdx.x * FILL_THREADS + threadIdx.x;
@@ -247,10 +269,10 @@ __global__ void __launch_bounds__(FILL_THREADS)
     const uint64_t p0 = head + (i << 3);
     if (!init) {
       b = bin_of(p0);
-      nxt = next_start(b);
+      nxt = pre(b + 1);
       init = true;
     }
-    while (nxt <= p0) nxt = next_start(++b);
+    while (nxt <= p0) nxt = pre(++b + 1);
     uint4 q;
     if (nxt >= p0 + 8) {
       const uint32_t w = (b * 0x00010001u) ^ X;
@@ -261,7 +283,7 @@ __global__ void __launch_bounds__(FILL_THREADS)
       uint64_t nn = nxt;
 #pragma unroll
       for (int j = 0; j < 8; ++j) {
-        while (nn <= p0 + j) nn = next_start(++bb);
+        while (nn <= p0 + j) nn = pre(++bb + 1);
         w[j >> 1] |= bb << ((j & 1) * 16);
       }
       q = make_uint4(w[0] ^ X, w[1] ^ X, w[2] ^ X, w[3] ^ X);
@@ -290,23 +312,41 @@ bsort_status_t run8(uint8_t* keys, uint64_t n, void* ws, cudaStream_t s) {
   return BSORT_SUCCESS;
 }
 
-int pairs16() { return max(1, num_sms() / 2); }
+struct Count16Layout {
+  size_t ovf, local, tot, partial, total;
+};
+Count16Layout count16_layout() {
+  Count16Layout l;
+  size_t off = 0;
+  l.ovf = off;     off = align_up(off + BINS16 * 8, 256);
+  l.local = off;   off = align_up(off + BINS16 * 8, 256);
+  l.tot = off;     off = align_up(off + SCAN16_BLOCKS * 8, 256);
+  l.partial = off; off = align_up(off + (size_t)num_sms() * BINS16 * sizeof(uint16_t), 256);
+  l.total = off;
+  return l;
+}
 
 template <uint32_t X>
 bsort_status_t run16(uint16_t* keys, uint64_t n, void* ws, cudaStream_t s) {
-  const int pairs = pairs16();
-  auto* hist = reinterpret_cast<unsigned long long*>(ws);
+  const Count16Layout l = count16_layout();
+  auto* w = static_cast<unsigned char*>(ws);
+  auto* ovf = reinterpret_cast<unsigned long long*>(w + l.ovf);
+  auto* local = reinterpret_cast<unsigned long long*>(w + l.local);
+  auto* tot = reinterpret_cast<unsigned long long*>(w + l.tot);
+  auto* partial = reinterpret_cast<uint16_t*>(w + l.partial);
   const int smem = (BINS16 / 2) * sizeof(uint32_t);
   static bool attr_set = false;  // idempotent; benign race
   if (!attr_set) {
     BSORT_CUDA(cudaFuncSetAttribute(k_count_hist16<X>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
     attr_set = true;
   }
-  BSORT_LAUNCH(PROF_MEMSET, s, cudaMemsetAsync(hist, 0, BINS16 * sizeof(unsigned long long), s));
-  BSORT_LAUNCH(PROF_COUNT_HIST, s, k_count_hist16<X><<<2 * pairs, CNT_THREADS, smem, s>>>(keys, n, hist));
-  BSORT_LAUNCH(PROF_COUNT_SCAN, s, k_count_scan16<<<1, 1024, 0, s>>>(hist));
+  const int rows = num_sms();
+  BSORT_LAUNCH(PROF_MEMSET, s, cudaMemsetAsync(ovf, 0, BINS16 * sizeof(unsigned long long), s));
+  BSORT_LAUNCH(PROF_COUNT_HIST, s, k_count_hist16<X><<<rows, CNT_THREADS, smem, s>>>(keys, n, partial, ovf));
+  BSORT_LAUNCH(PROF_COUNT_SCAN, s,
+               k_count_scan16<<<SCAN16_BLOCKS, SCAN16_BLOCK, 0, s>>>(partial, rows, ovf, local, tot));
   BSORT_LAUNCH(PROF_COUNT_FILL, s,
-               k_count_fill16<X><<<fill_grid(n / 8 + 1), FILL_THREADS, 0, s>>>(keys, n, hist));
+               k_count_fill16<X><<<fill_grid(n / 8 + 1), FILL_THREADS, 0, s>>>(keys, n, local, tot));
   return BSORT_SUCCESS;
 }
 
@@ -315,7 +355,7 @@ bsort_status_t run16(uint16_t* keys, uint64_t n, void* ws, cudaStream_t s) {
 size_t counting_workspace_bytes(int bytes, uint64_t n) {
   if (n <= 1) return 0;
   if (bytes == 1) return 256 * sizeof(unsigned long long);
-  return BINS16 * sizeof(unsigned long long);
+  return count16_layout().total;
 }
 
 bsort_status_t counting_sort(const DtypeInfo& di, void* keys, uint64_t n, bool desc, void* ws,

@@ -178,3 +178,16 @@ def test_launch_counter_moves(B):
     B.sort_(x)
     torch.cuda.synchronize()
     assert B.launch_count() - c0 >= 6  # hist + plan + 4 passes (+ memsets, copy)
+
+
+@pytest.mark.parametrize("dtype", [torch.int16, torch.uint16])
+def test_count16_drain_path(B, dtype):
+    """16-bit histogram: a bin receiving more than 0x8000 keys inside one CTA drains to the
+    global overflow counter (all-equal and 3-valued inputs large enough to drain several times)."""
+    n = (1 << 23) + 5
+    x = sview(gen(dtype, 1, 31)).repeat(n).view(dtype)
+    check_equal(B, x.clone(), False, "all equal")
+    check_equal(B, x.clone(), True, "all equal desc")
+    table = sview(gen(dtype, 3, 32))
+    y = table[(W.bits(n, 33, "cuda") >> 62) % 3].view(dtype)
+    check_equal(B, y, True, "3 distinct")
