@@ -127,7 +127,7 @@ bsort_status_t lsd_run(U* keys, uint64_t n, unsigned char* ws, cudaStream_t s) {
       st = launch_pass<U, RANK_UNSTABLE, DescT>(keys, scratch, n, RadixDigit<KIND, DESC, U, SH>{}, bases, lookback,
                                                 gcount, counters, plan, p, s);
     else
-      st = launch_pass<U, RANK_ATOMIC_OR, DescT>(keys, scratch, n, RadixDigit<KIND, DESC, U, SH>{},
+      st = launch_pass<U, RANK_RUN2, DescT>(keys, scratch, n, RadixDigit<KIND, DESC, U, SH>{},
                                                  bases + p * 256, lookback, gcount + p * 256, counters + p,
                                                  plan, p, s);
   };

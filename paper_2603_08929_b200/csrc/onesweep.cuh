@@ -43,21 +43,23 @@ __device__ __forceinline__ void st_relaxed(unsigned long long* p, unsigned long 
   asm volatile("st.relaxed.gpu.global.b64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
 
-// Decoupled look-back for digit t of `tile` (descriptors tile-major: [tile][256 digits], so
+// Decoupled look-back, one thread per digit t (descriptors tile-major: [tile][256 digits], so
 // the 256 walking threads of a CTA read 128-byte coalesced rows).  Each step issues G
 // independent loads for the G nearest unfolded predecessors, so one L2 round trip folds in up
 // to G tiles: at B200 tile rates (hundreds of CTAs on consecutive tiles) a one-load-per-step
-// walk is a serial chain of L2 latencies.  Returns the exclusive prefix of `tile`.
+// walk is a serial chain of L2 latencies.
 template <int G, typename DescT>
-__device__ __forceinline__ DescT lookback_walk(const DescT* lookback, uint32_t t, uint32_t tile) {
+__device__ __forceinline__ void lookback_issue(const DescT* lookback, uint32_t t, int64_t j, DescT (&v)[G]) {
+#pragma unroll
+  for (int q = 0; q < G; ++q) v[q] = (j - q >= 0) ? ld_relaxed(&lookback[(uint64_t)(j - q) * 256 + t]) : DescT(0);
+}
+// Folds the window v (predecessors j, j-1, ..., j-G+1, loaded by lookback_issue) and walks on
+// until an inclusive prefix is found.  Returns the exclusive prefix of the tile.
+template <int G, typename DescT>
+__device__ __forceinline__ DescT lookback_finish(const DescT* lookback, uint32_t t, int64_t j, DescT (&v)[G]) {
   using LB = LookbackBits<DescT>;
   DescT excl = 0;
-  int64_t j = (int64_t)tile - 1;  // highest predecessor not folded in yet
   for (;;) {
-    DescT v[G];
-#pragma unroll
-    for (int q = 0; q < G; ++q)
-      v[q] = (j - q >= 0) ? ld_relaxed(&lookback[(uint64_t)(j - q) * 256 + t]) : DescT(0);
     bool stop = false, fin = false;
     int adv = G;
 #pragma unroll
@@ -75,7 +77,14 @@ __device__ __forceinline__ DescT lookback_walk(const DescT* lookback, uint32_t t
     }
     if (fin) return excl;  // tile 0 holds an inclusive prefix, so the walk ends there at the latest
     j -= adv;
+    lookback_issue<G>(lookback, t, j, v);
   }
+}
+template <int G, typename DescT>
+__device__ __forceinline__ DescT lookback_walk(const DescT* lookback, uint32_t t, uint32_t tile) {
+  DescT v[G];
+  lookback_issue<G>(lookback, t, (int64_t)tile - 1, v);
+  return lookback_finish<G>(lookback, t, (int64_t)tile - 1, v);
 }
 
 template <typename U> __device__ __forceinline__ U ldg_nc(const U* p);
@@ -104,16 +113,23 @@ struct PassPlan {
 // the digit is one funnel-shift + mask after the transform).
 template <int KIND, bool DESC, typename U, int SHIFT>
 struct RadixDigit {
-  static constexpr int BITS = 8;
   __device__ __forceinline__ uint32_t operator()(U x) const {
     return uint32_t(key_encode<KIND, DESC>(x) >> SHIFT) & 0xFFu;
+  }
+  // digit and the bits below it (the digits the earlier LSD passes sorted by), one encode
+  __device__ __forceinline__ uint32_t digit_low(U x, U* low) const {
+    const U e = key_encode<KIND, DESC>(x);
+    if constexpr (SHIFT == 0)
+      *low = U(0);
+    else
+      *low = U(e & U((U(1) << SHIFT) - 1));
+    return uint32_t(e >> SHIFT) & 0xFFu;
   }
 };
 
 // Digit of the MSD partition: destination rank of the key's top-16-bit bin.
 template <int KIND, bool DESC, typename U>
 struct RankDigit {
-  static constexpr int BITS = 8;
   uint32_t cuts[BSORT_DIST_MAX_RANKS + 1];
   int nranks;
   __device__ __forceinline__ uint32_t operator()(U x) const {
@@ -124,6 +140,10 @@ struct RankDigit {
       if (cuts[mid] <= b) lo = mid; else hi = mid;
     }
     return lo;
+  }
+  __device__ __forceinline__ uint32_t digit_low(U x, U* low) const {
+    *low = U(0);
+    return (*this)(x);
   }
 };
 
@@ -224,34 +244,38 @@ __global__ void __launch_bounds__(256)
 //      !BULK (source not 16-byte aligned): coalesced per-warp loads.
 //   1. keys -> registers, warp-striped: warp w owns the contiguous segment [w*32*ITEMS, ...),
 //      item k of lane l is element 32k+l of it, so (warp, item, lane) order IS index order.
-//   2. ranking (RANK):
-//      stable modes (every LSD pass after the first, the MSD partition): a warp-level
-//      multisplit that follows index order.  Per item the lanes with equal digits are grouped
-//      (RANK_MATCH: MATCH.ANY; RANK_BALLOT: 8 ballots; RANK_ATOMIC_OR / RANK_PACKED: every lane
-//      ORs its bit into a per-warp per-digit mask word in smem and reads it back), the group's
-//      highest lane advances the warp's counter of that digit, rank = old count + lanes below.
-//      RANK_PACKED keeps mask and count in one 64-bit word (one load, one leader store).
-//      RANK_UNSTABLE (the first LSD pass only: the input order carries no information, so equal
-//      digits may land in any order): one shared atomicAdd per key on block counters, and the
-//      tile's per-digit global offsets come from one global atomicAdd per digit -- no look-back.
-//   3. per-digit totals; stable modes publish the tile's counts to the look-back array early
-//      (flag AGG; tile 0 publishes INC); block scan => tile offsets; keys restaged in smem in
-//      digit order (in buffer `cur`; its keys now live in registers).
-//   4. stable modes: decoupled look-back, one thread per digit => global digit offset.
+//   2. ranking (MODE):
+//      RANK_STABLE: warp-level multisplit in index order.  Per item, every lane ORs its bit into
+//        a per-warp per-digit mask word in smem and reads it back (its group of equal digits);
+//        the group's highest lane advances the warp's counter of that digit and clears the
+//        mask; rank = old count + lanes below in the group.  (MATCH.ANY, 8-ballot and
+//        leader-election grouping were measured slower on sm_100: DESIGN.md §6.)
+//      RANK_UNSTABLE (first LSD pass, MSD partition: the input order carries no information):
+//        one shared atomicAdd per key on block counters; the tile's per-digit global offsets
+//        come from one global atomicAdd per digit -- no look-back.
+//      RANK_RUN2 (LSD passes p >= 1): the array is sorted by the low 8p bits L (the digits of
+//        the earlier passes), so a tile holds runs of equal L in increasing order.  If the tile
+//        has at most two distinct L (those of its first and last key), keys are ranked unstably
+//        by (run, digit) over 512 block counters -- keys with equal (run, digit) have equal low
+//        8(p+1) bits, so their order is irrelevant, and run 0 precedes run 1 within a digit:
+//        exactly the stable order.  Otherwise the tile falls back to RANK_STABLE.
+//   3. per-digit totals; look-back modes publish the tile's counts early (flag AGG; tile 0
+//      publishes INC); block scan => tile offsets; keys restaged in smem in digit order (in
+//      buffer `cur`; its keys now live in registers).
+//   4. look-back modes: decoupled look-back => global digit offsets.
 //   5. coalesced write-out of the digit-sorted tile: runs of equal digits are contiguous.
-enum RankMode : int { RANK_MATCH = 0, RANK_BALLOT = 1, RANK_ATOMIC_OR = 2, RANK_PACKED = 3, RANK_UNSTABLE = 4 };
+enum RankMode : int { RANK_STABLE = 0, RANK_UNSTABLE = 1, RANK_RUN2 = 2 };
 
-template <int THREADS, int ITEMS, typename U, int RANK>
+template <int THREADS, int ITEMS, typename U, int MODE>
 struct PassSmem {
   static constexpr int WARPS = THREADS / 32;
   static constexpr int TILE = THREADS * ITEMS;
-  // per-warp counter rows: u32[256] (+ u32[256] match masks for ATOMIC_OR); u64[256] packed
-  // {count:32 | mask:32} for PACKED; one block-wide u32[256] row for UNSTABLE
-  static constexpr size_t row_bytes = RANK == RANK_ATOMIC_OR ? 2048 : RANK == RANK_PACKED ? 2048 : 1024;
-  static constexpr int rows = RANK == RANK_UNSTABLE ? 1 : WARPS;
+  // per-warp rows {u32 count[256], u32 mask[256]} for the multisplit; 512 block counters
+  static constexpr int rows = MODE == RANK_UNSTABLE ? 0 : WARPS;
   static constexpr size_t buf_off = 0;  // U[2][TILE]
-  static constexpr size_t wcnt_off = align_up(buf_off + 2 * sizeof(U) * TILE, 16);
-  static constexpr size_t gofs_off = align_up(wcnt_off + row_bytes * rows, 16);
+  static constexpr size_t rows_off = align_up(buf_off + 2 * sizeof(U) * TILE, 16);
+  static constexpr size_t bcnt_off = align_up(rows_off + 2048 * rows, 16);
+  static constexpr size_t gofs_off = align_up(bcnt_off + sizeof(uint32_t) * 512, 16);
   static constexpr size_t wt_off = align_up(gofs_off + sizeof(unsigned long long) * 256, 16);
   static constexpr size_t mbar_off = align_up(wt_off + sizeof(uint32_t) * (WARPS + 1), 16);
   static constexpr size_t tile_off = mbar_off + 16;  // uint32 tile id held by each buffer
@@ -290,25 +314,26 @@ __device__ __forceinline__ void bulk_load(void* dst_smem, const void* src, uint3
         : "memory");
 }
 
-template <typename U, int THREADS, int ITEMS, int MINB, bool BULK, typename DescT, typename DigitF,
-          int RANK = RANK_ATOMIC_OR, int LBG = 8>
+template <typename U, int THREADS, int ITEMS, int MINB, bool BULK, typename DescT, typename DigitF, int MODE,
+          int LBG = 8>
 __global__ void __launch_bounds__(THREADS, MINB)
     k_onesweep_pass(const U* a_ptr, U* b_ptr, uint64_t n, DigitF digit,
                     const unsigned long long* __restrict__ bases, DescT* __restrict__ lookback,
                     unsigned long long* __restrict__ gcount, uint32_t* __restrict__ tile_counter,
                     uint32_t num_tiles, const PassPlan* __restrict__ plan, int pass) {
-  using L = PassSmem<THREADS, ITEMS, U, RANK>;
+  using L = PassSmem<THREADS, ITEMS, U, MODE>;
   using LB = LookbackBits<DescT>;
   constexpr int TILE = L::TILE;
   constexpr int WARPS = L::WARPS;
   constexpr int SEG = 32 * ITEMS;  // keys per warp segment
-  constexpr bool STABLE = RANK != RANK_UNSTABLE;
-  static_assert(THREADS >= 256, "one thread per digit");
-  static_assert(TILE < (1 << 23), "rank fits 23 bits");
+  constexpr bool LOOKBACK = MODE != RANK_UNSTABLE;
+  static_assert(THREADS >= 256 && THREADS % 32 == 0, "one thread per digit");
+  static_assert(TILE < (1 << 22), "rank fits 22 bits");
   static_assert((TILE * sizeof(U)) % 16 == 0, "bulk copies need 16-byte tiles");
   extern __shared__ __align__(128) unsigned char smem[];
   U* bufs = reinterpret_cast<U*>(smem + L::buf_off);
-  unsigned char* rows = smem + L::wcnt_off;
+  uint32_t* rows = reinterpret_cast<uint32_t*>(smem + L::rows_off);  // [warp][count 256 | mask 256]
+  uint32_t* bcnt = reinterpret_cast<uint32_t*>(smem + L::bcnt_off);  // [512]
   unsigned long long* gofs = reinterpret_cast<unsigned long long*>(smem + L::gofs_off);
   uint32_t* wt = reinterpret_cast<uint32_t*>(smem + L::wt_off);
   uint64_t* mbar = reinterpret_cast<uint64_t*>(smem + L::mbar_off);
@@ -327,15 +352,7 @@ __global__ void __launch_bounds__(THREADS, MINB)
   const uint32_t warp = threadIdx.x >> 5;
   const uint32_t t = threadIdx.x;
   const uint32_t lt = (1u << lane) - 1u;
-  // counters of this warp (stable modes) / of the block (UNSTABLE): u32[256] view
-  uint32_t* wc = reinterpret_cast<uint32_t*>(rows + (STABLE ? warp * L::row_bytes : 0));
-  // counter of digit d in row w, u32 view (PACKED: high word of the u64 slot)
-  auto cnt_at = [&](uint32_t w, uint32_t d) -> uint32_t& {
-    if constexpr (RANK == RANK_PACKED)
-      return reinterpret_cast<uint32_t*>(rows + w * L::row_bytes)[2 * d + 1];
-    else
-      return reinterpret_cast<uint32_t*>(rows + w * L::row_bytes)[d];
-  };
+  uint32_t* wc = rows + warp * 512;  // this warp's counters; wc + 256: its match masks
 
   auto tile_valid = [&](uint32_t tile) -> uint32_t {
     const uint64_t b = (uint64_t)tile * TILE;
@@ -346,11 +363,9 @@ __global__ void __launch_bounds__(THREADS, MINB)
     return (uint32_t)((valid * sizeof(U)) & ~(size_t)15) / (uint32_t)sizeof(U);
   };
 
-  if constexpr (RANK == RANK_ATOMIC_OR || RANK == RANK_PACKED) {  // match masks start at 0
-    uint32_t* r = reinterpret_cast<uint32_t*>(rows + warp * L::row_bytes);
+  if constexpr (MODE != RANK_UNSTABLE) {  // match masks start (and stay) at 0
 #pragma unroll
-    for (int j = 0; j < 512 / 32; ++j) r[lane + 32 * j] = 0;
-    __syncwarp();
+    for (int j = 0; j < 8; ++j) wc[256 + lane + 32 * j] = 0;
   }
   uint32_t phase0 = 0, phase1 = 0;
   if constexpr (BULK) {
@@ -389,33 +404,39 @@ __global__ void __launch_bounds__(THREADS, MINB)
     const uint32_t valid = tile_valid(tile);
     const bool full = valid == (uint32_t)TILE;
 
-    // zero the counters (rows are dead: every read of them happened before the last barrier)
-    if constexpr (STABLE) {
+    // zero the counters (every read of them happened before the previous tile's last barrier)
+    if constexpr (MODE != RANK_UNSTABLE) {
 #pragma unroll
-      for (int j = 0; j < 256 / 32; ++j) cnt_at(warp, lane + 32 * j) = 0;
-    } else {
-      if (t < 256) wc[t] = 0;
-      if constexpr (!BULK) {
-      } else {
-        __syncthreads();  // block counters zeroed before any warp counts
-      }
+      for (int j = 0; j < 8; ++j) wc[lane + 32 * j] = 0;
+    }
+    if constexpr (MODE != RANK_STABLE) {
+      for (int j = t; j < 512; j += THREADS) bcnt[j] = 0;
     }
 
     // 1. keys -> registers
     const uint32_t seg = warp * SEG + lane;  // tile-local index of item 0
     U keys[ITEMS];
+    U first_key = U(0), last_key = U(0);
     if constexpr (BULK) {
       mbar_wait(&mbar[cur], cur ? phase1 : phase0);
       if (cur) phase1 ^= 1u; else phase0 ^= 1u;
       if (full) {
 #pragma unroll
         for (int k = 0; k < ITEMS; ++k) keys[k] = buf[seg + 32 * k];
+        if constexpr (MODE == RANK_RUN2) {
+          first_key = buf[0];
+          last_key = buf[TILE - 1];
+        }
       } else {
         const uint32_t bk = bulk_keys(valid);
 #pragma unroll
         for (int k = 0; k < ITEMS; ++k) {
           const uint32_t i = seg + 32 * k;
           keys[k] = i < bk ? buf[i] : (i < valid ? ldg_nc(src + tile_base + i) : U(0));
+        }
+        if constexpr (MODE == RANK_RUN2) {
+          first_key = bk > 0 ? buf[0] : ldg_nc(src + tile_base);
+          last_key = valid - 1 < bk ? buf[valid - 1] : ldg_nc(src + tile_base + valid - 1);
         }
       }
     } else {
@@ -427,55 +448,51 @@ __global__ void __launch_bounds__(THREADS, MINB)
         for (int k = 0; k < ITEMS; ++k)
           keys[k] = (seg + 32 * k < valid) ? ldg_nc(src + tile_base + seg + 32 * k) : U(0);
       }
-      if constexpr (!STABLE) __syncthreads();  // block counters zeroed before any warp counts
+      if constexpr (MODE == RANK_RUN2) {
+        first_key = ldg_nc(src + tile_base);
+        last_key = ldg_nc(src + tile_base + valid - 1);
+      }
     }
 
-    // 2. ranking.  Invalid tail slots take digit 255: they sit at the end of the tile in index
-    // order, so (stable modes) they rank after every valid key of digit 255 and are dropped;
-    // the unstable mode does not count them at all.
-    uint32_t info[ITEMS];  // d | rank << 8
-    if constexpr (RANK == RANK_UNSTABLE) {
+    // Ranking strategy of this tile (block-uniform); the barrier also orders the zeroing of
+    // the block counters before their first atomic.
+    bool unstable_rank = MODE == RANK_UNSTABLE;
+    U low_first = U(0);
+    if constexpr (MODE == RANK_RUN2) {
+      U low_last, lo;
+      digit.digit_low(first_key, &low_first);
+      digit.digit_low(last_key, &low_last);
+      bool bad = false;
+#pragma unroll
+      for (int k = 0; k < ITEMS; ++k) {
+        digit.digit_low(keys[k], &lo);
+        bad |= (full || seg + 32 * k < valid) && lo != low_first && lo != low_last;
+      }
+      unstable_rank = !__syncthreads_or(bad);
+    } else if constexpr (MODE == RANK_UNSTABLE) {
+      __syncthreads();
+    }
+
+    // 2. ranking.  info = bin | rank << 9 (bin = digit, + 256 for run 1 in RUN2).
+    uint32_t info[ITEMS];
+    if (unstable_rank) {
+      // invalid tail slots are not counted at all
 #pragma unroll
       for (int k = 0; k < ITEMS; ++k) {
         if (full || seg + 32 * k < valid) {
-          const uint32_t d = digit(keys[k]);
-          info[k] = d | (atomicAdd(&wc[d], 1u) << 8);
+          U lo;
+          uint32_t bin = digit.digit_low(keys[k], &lo);
+          if constexpr (MODE == RANK_RUN2) bin |= (lo != low_first) ? 256u : 0u;
+          info[k] = bin | (atomicAdd(&bcnt[bin], 1u) << 9);
         } else {
           info[k] = 0xFFFFFFFFu;
         }
       }
-    } else if constexpr (RANK == RANK_MATCH || RANK == RANK_BALLOT) {
-#pragma unroll
-      for (int k = 0; k < ITEMS; ++k) {
-        const uint32_t d = (full || seg + 32 * k < valid) ? digit(keys[k]) : 255u;
-        uint32_t peers;
-        if constexpr (RANK == RANK_MATCH) {
-          peers = __match_any_sync(0xffffffffu, d);
-        } else {
-          peers = 0xffffffffu;
-#pragma unroll
-          for (int b = 0; b < 8; ++b) {
-            const uint32_t bb = __ballot_sync(0xffffffffu, (d >> b) & 1u);
-            peers &= ~(bb ^ (0u - ((d >> b) & 1u)));
-          }
-        }
-        const uint32_t below = __popc(peers & lt);
-        const uint32_t leader = (peers >> lane) == 1u;  // highest lane of the group
-        info[k] = d | (below << 8) | (leader << 31);
-      }
+    } else if constexpr (MODE != RANK_UNSTABLE) {
+      // Invalid tail slots take digit 255: they sit at the end of the tile in index order, so
+      // they rank after every valid key of digit 255 and are dropped at write-out.
+      uint32_t* mm = wc + 256;
       __syncwarp();  // counters zeroed by this warp
-#pragma unroll
-      for (int k = 0; k < ITEMS; ++k) {
-        const uint32_t d = info[k] & 0xFFu;
-        const uint32_t below = (info[k] >> 8) & 0xFFFFu;
-        const uint32_t old = wc[d];
-        if (info[k] >> 31) wc[d] = old + below + 1u;
-        __syncwarp();
-        info[k] = d | ((old + below) << 8);
-      }
-    } else if constexpr (RANK == RANK_ATOMIC_OR) {
-      uint32_t* mm = wc + 256;  // second half of the warp's row: match masks
-      __syncwarp();             // counters zeroed by this warp
 #pragma unroll
       for (int k = 0; k < ITEMS; ++k) {
         const uint32_t d = (full || seg + 32 * k < valid) ? digit(keys[k]) : 255u;
@@ -489,72 +506,58 @@ __global__ void __launch_bounds__(THREADS, MINB)
           mm[d] = 0;
           wc[d] = old + below + 1u;
         }
-        info[k] = d | ((old + below) << 8);
-      }
-    } else {  // RANK_PACKED: slot d = {mask (low word), count (high word)}
-      unsigned long long* pw = reinterpret_cast<unsigned long long*>(wc);
-      __syncwarp();  // counters zeroed by this warp
-#pragma unroll
-      for (int k = 0; k < ITEMS; ++k) {
-        const uint32_t d = (full || seg + 32 * k < valid) ? digit(keys[k]) : 255u;
-        atomicOr(reinterpret_cast<uint32_t*>(&pw[d]), 1u << lane);
-        __syncwarp();
-        const unsigned long long w = pw[d];
-        const uint32_t peers = (uint32_t)w;
-        const uint32_t old = (uint32_t)(w >> 32);
-        const uint32_t below = __popc(peers & lt);
-        __syncwarp();
-        if ((peers >> lane) == 1u) pw[d] = (unsigned long long)(old + below + 1u) << 32;
-        info[k] = d | ((old + below) << 8);
+        info[k] = d | ((old + below) << 9);
       }
     }
     __syncthreads();  // (A) counters complete; all warps done reading buf
 
-    // 3. per-digit totals, early publish (stable), tile offsets
-    uint32_t total = 0;
+    // 3. per-digit totals, early publish, tile offsets
+    uint32_t total = 0, c0 = 0;
     if (t < 256) {
-      if constexpr (STABLE) {
-#pragma unroll
-        for (int w = 0; w < WARPS; ++w) total += cnt_at(w, t);
-        if (!full && t == 255) total -= (uint32_t)TILE - valid;  // invalid tail slots
-        st_relaxed(&lookback[(uint64_t)tile * 256 + t], (tile == 0 ? LB::INC : LB::AGG) | DescT(total));
+      if (unstable_rank) {
+        c0 = bcnt[t];
+        total = c0 + (MODE == RANK_RUN2 ? bcnt[256 + t] : 0u);
       } else {
-        total = wc[t];
+#pragma unroll
+        for (int w = 0; w < WARPS; ++w) total += rows[w * 512 + t];
+        if (!full && t == 255) total -= (uint32_t)TILE - valid;  // invalid tail slots
+      }
+      if constexpr (LOOKBACK) {
+        st_relaxed(&lookback[(uint64_t)tile * 256 + t], (tile == 0 ? LB::INC : LB::AGG) | DescT(total));
       }
     }
     const uint32_t tile_excl = block_exclusive_scan<THREADS>(t < 256 ? total : 0u, wt, (uint32_t*)nullptr);
     unsigned long long gbase = 0;
     if (t < 256) {
-      if constexpr (STABLE) {
+      if (unstable_rank) {
+        bcnt[t] = tile_excl;
+        if constexpr (MODE == RANK_RUN2) bcnt[256 + t] = tile_excl + c0;
+        if constexpr (MODE == RANK_UNSTABLE)
+          if (total) gbase = atomicAdd(&gcount[t], (unsigned long long)total);  // tile order is free
+      } else {
         uint32_t run = tile_excl;
 #pragma unroll
         for (int w = 0; w < WARPS; ++w) {
-          const uint32_t c = cnt_at(w, t);
-          cnt_at(w, t) = run;
+          const uint32_t c = rows[w * 512 + t];
+          rows[w * 512 + t] = run;
           run += c;
         }
-      } else {
-        wc[t] = tile_excl;
-        if (total) gbase = atomicAdd(&gcount[t], (unsigned long long)total);  // tile order is free
       }
     }
     __syncthreads();  // (B)
 
-    if constexpr (STABLE) {
-#pragma unroll
-      for (int k = 0; k < ITEMS; ++k) {
-        const uint32_t d = info[k] & 0xFFu;
-        buf[cnt_at(warp, d) + (info[k] >> 8)] = keys[k];
-      }
-    } else {
+    if (unstable_rank) {
 #pragma unroll
       for (int k = 0; k < ITEMS; ++k)
-        if (info[k] != 0xFFFFFFFFu) buf[wc[info[k] & 0xFFu] + (info[k] >> 8)] = keys[k];
+        if (info[k] != 0xFFFFFFFFu) buf[bcnt[info[k] & 0x1FFu] + (info[k] >> 9)] = keys[k];
+    } else {
+#pragma unroll
+      for (int k = 0; k < ITEMS; ++k) buf[wc[info[k] & 0xFFu] + (info[k] >> 9)] = keys[k];
     }
 
     // 4. global digit offsets
     if (t < 256) {
-      if constexpr (STABLE) {
+      if constexpr (LOOKBACK) {
         DescT excl = 0;
         if (tile > 0) {
           excl = lookback_walk<LBG>(lookback, t, tile);
