@@ -266,6 +266,11 @@ __global__ void __launch_bounds__(256)
 //   5. coalesced write-out of the digit-sorted tile: runs of equal digits are contiguous.
 enum RankMode : int { RANK_STABLE = 0, RANK_UNSTABLE = 1, RANK_RUN2 = 2 };
 
+// Block counters of the unstable ranking are replicated BREP ways (replica = lane % BREP): lanes
+// of one warp instruction that share a digit hit BREP different words, so same-address atomic
+// serialization is at most 32/BREP-way (skewed digits, runs of equal keys).
+constexpr int BREP = 4;  // the offset code below reads one uint4 per bin
+
 template <int THREADS, int ITEMS, typename U, int MODE>
 struct PassSmem {
   static constexpr int WARPS = THREADS / 32;
@@ -275,7 +280,7 @@ struct PassSmem {
   static constexpr size_t buf_off = 0;  // U[2][TILE]
   static constexpr size_t rows_off = align_up(buf_off + 2 * sizeof(U) * TILE, 16);
   static constexpr size_t bcnt_off = align_up(rows_off + 2048 * rows, 16);
-  static constexpr size_t gofs_off = align_up(bcnt_off + sizeof(uint32_t) * 512, 16);
+  static constexpr size_t gofs_off = align_up(bcnt_off + sizeof(uint32_t) * 512 * BREP, 16);
   static constexpr size_t wt_off = align_up(gofs_off + sizeof(unsigned long long) * 256, 16);
   static constexpr size_t mbar_off = align_up(wt_off + sizeof(uint32_t) * (WARPS + 1), 16);
   static constexpr size_t tile_off = mbar_off + 16;  // uint32 tile id held by each buffer
@@ -333,7 +338,7 @@ __global__ void __launch_bounds__(THREADS, MINB)
   extern __shared__ __align__(128) unsigned char smem[];
   U* bufs = reinterpret_cast<U*>(smem + L::buf_off);
   uint32_t* rows = reinterpret_cast<uint32_t*>(smem + L::rows_off);  // [warp][count 256 | mask 256]
-  uint32_t* bcnt = reinterpret_cast<uint32_t*>(smem + L::bcnt_off);  // [512]
+  uint32_t* bcnt = reinterpret_cast<uint32_t*>(smem + L::bcnt_off);  // [512 bins][BREP]
   unsigned long long* gofs = reinterpret_cast<unsigned long long*>(smem + L::gofs_off);
   uint32_t* wt = reinterpret_cast<uint32_t*>(smem + L::wt_off);
   uint64_t* mbar = reinterpret_cast<uint64_t*>(smem + L::mbar_off);
@@ -410,7 +415,7 @@ __global__ void __launch_bounds__(THREADS, MINB)
       for (int j = 0; j < 8; ++j) wc[lane + 32 * j] = 0;
     }
     if constexpr (MODE != RANK_STABLE) {
-      for (int j = t; j < 512; j += THREADS) bcnt[j] = 0;
+      for (int j = t; j < 512 * BREP / 4; j += THREADS) reinterpret_cast<uint4*>(bcnt)[j] = make_uint4(0, 0, 0, 0);
     }
 
     // 1. keys -> registers
@@ -483,7 +488,7 @@ __global__ void __launch_bounds__(THREADS, MINB)
           U lo;
           uint32_t bin = digit.digit_low(keys[k], &lo);
           if constexpr (MODE == RANK_RUN2) bin |= (lo != low_first) ? 256u : 0u;
-          info[k] = bin | (atomicAdd(&bcnt[bin], 1u) << 9);
+          info[k] = bin | (atomicAdd(&bcnt[bin * BREP + (lane & (BREP - 1))], 1u) << 9);
         } else {
           info[k] = 0xFFFFFFFFu;
         }
@@ -513,10 +518,16 @@ __global__ void __launch_bounds__(THREADS, MINB)
 
     // 3. per-digit totals, early publish, tile offsets
     uint32_t total = 0, c0 = 0;
+    (void)c0;
     if (t < 256) {
       if (unstable_rank) {
-        c0 = bcnt[t];
-        total = c0 + (MODE == RANK_RUN2 ? bcnt[256 + t] : 0u);
+        const uint4 r0 = reinterpret_cast<const uint4*>(bcnt)[t];
+        c0 = r0.x + r0.y + r0.z + r0.w;
+        total = c0;
+        if constexpr (MODE == RANK_RUN2) {
+          const uint4 r1 = reinterpret_cast<const uint4*>(bcnt)[256 + t];
+          total += r1.x + r1.y + r1.z + r1.w;
+        }
       } else {
 #pragma unroll
         for (int w = 0; w < WARPS; ++w) total += rows[w * 512 + t];
@@ -530,8 +541,24 @@ __global__ void __launch_bounds__(THREADS, MINB)
     unsigned long long gbase = 0;
     if (t < 256) {
       if (unstable_rank) {
-        bcnt[t] = tile_excl;
-        if constexpr (MODE == RANK_RUN2) bcnt[256 + t] = tile_excl + c0;
+        // replica start offsets: run 0 replicas 0..3, then run 1 replicas 0..3
+        uint4 r0 = reinterpret_cast<const uint4*>(bcnt)[t];
+        uint32_t run = tile_excl;
+        uint4 o0;
+        o0.x = run; run += r0.x;
+        o0.y = run; run += r0.y;
+        o0.z = run; run += r0.z;
+        o0.w = run; run += r0.w;
+        reinterpret_cast<uint4*>(bcnt)[t] = o0;
+        if constexpr (MODE == RANK_RUN2) {
+          uint4 r1 = reinterpret_cast<const uint4*>(bcnt)[256 + t];
+          uint4 o1;
+          o1.x = run; run += r1.x;
+          o1.y = run; run += r1.y;
+          o1.z = run; run += r1.z;
+          o1.w = run;
+          reinterpret_cast<uint4*>(bcnt)[256 + t] = o1;
+        }
         if constexpr (MODE == RANK_UNSTABLE)
           if (total) gbase = atomicAdd(&gcount[t], (unsigned long long)total);  // tile order is free
       } else {
@@ -549,7 +576,7 @@ __global__ void __launch_bounds__(THREADS, MINB)
     if (unstable_rank) {
 #pragma unroll
       for (int k = 0; k < ITEMS; ++k)
-        if (info[k] != 0xFFFFFFFFu) buf[bcnt[info[k] & 0x1FFu] + (info[k] >> 9)] = keys[k];
+        if (info[k] != 0xFFFFFFFFu) buf[bcnt[(info[k] & 0x1FFu) * BREP + (lane & (BREP - 1))] + (info[k] >> 9)] = keys[k];
     } else {
 #pragma unroll
       for (int k = 0; k < ITEMS; ++k) buf[wc[info[k] & 0xFFu] + (info[k] >> 9)] = keys[k];
