@@ -11,12 +11,16 @@
 namespace bsort {
 namespace {
 
-// Tile configuration per key width (tuned on B200).
-template <typename U> struct PassCfg;
-template <> struct PassCfg<uint32_t> {
+// Tile configuration per key width and ranking mode (tuned on B200 with tools/tune_pass.cu;
+// profiles/r1/tune_*.jsonl).  Two CTAs per SM of 512 (384) threads, 8192 (4608) keys per tile.
+// One 1024-thread CTA per SM shortens the look-back chains of a pure RUN2 pass (3.64 -> 3.38 ms)
+// but its 16384-key tiles break RUN2's two-run condition in pass 2 (runs of ~16K keys at
+// n = 2^30) and 8 keys per thread lose too much ILP (profiles/r1: cfg3 16.1 vs 16.6 / 19.7 ms).
+template <typename U, int MODE> struct PassCfg;
+template <int MODE> struct PassCfg<uint32_t, MODE> {
   static constexpr int THREADS = 512, ITEMS = 16, MINB = 2, LBG = 8;
 };
-template <> struct PassCfg<unsigned long long> {
+template <int MODE> struct PassCfg<unsigned long long, MODE> {
   static constexpr int THREADS = 384, ITEMS = 12, MINB = 2, LBG = 8;
 };
 
@@ -28,7 +32,7 @@ struct LsdLayout {
 
 template <typename U>
 LsdLayout lsd_layout(uint64_t n) {
-  using C = PassCfg<U>;
+  using C = PassCfg<U, RANK_RUN2>;  // the look-back passes size the descriptor array
   constexpr uint64_t TILE = (uint64_t)C::THREADS * C::ITEMS;
   constexpr int P = sizeof(U);
   const uint64_t tiles = (n + TILE - 1) / TILE;
@@ -50,7 +54,7 @@ template <typename U, bool BULK, int RANK, typename DescT, typename DigitF>
 bsort_status_t launch_pass_t(const U* a, U* b, uint64_t n, DigitF digit, const unsigned long long* bases,
                              DescT* lookback, unsigned long long* gcount, uint32_t* counter, const PassPlan* plan,
                              int pass, cudaStream_t s) {
-  using C = PassCfg<U>;
+  using C = PassCfg<U, RANK>;
   using L = PassSmem<C::THREADS, C::ITEMS, U, RANK>;
   auto kern = k_onesweep_pass<U, C::THREADS, C::ITEMS, C::MINB, BULK, DescT, DigitF, RANK, C::LBG>;
   static int occ = 0;  // per instantiation; benign race (idempotent)
@@ -88,7 +92,7 @@ bsort_status_t memset_async(void* p, size_t bytes, cudaStream_t s) {
 
 template <int KIND, bool DESC, typename U, typename DescT>
 bsort_status_t lsd_run(U* keys, uint64_t n, unsigned char* ws, cudaStream_t s) {
-  using C = PassCfg<U>;
+  using C = PassCfg<U, RANK_RUN2>;
   constexpr int P = sizeof(U);
   constexpr int LANES = hist_lanes<U>();
   constexpr uint64_t TILE = (uint64_t)C::THREADS * C::ITEMS;
