@@ -3,6 +3,7 @@
 //   memset(hist) -> k_onesweep_hist -> k_plan -> P x { memset(look-back) ; k_onesweep_pass }
 //   -> k_copy_back (no-op unless an odd number of passes executed)
 // Everything is stream-ordered on the caller's stream; no host synchronisation.
+#include <cstdlib>
 #include <type_traits>
 
 #include "onesweep.cuh"
@@ -27,8 +28,13 @@ template <int MODE> struct PassCfg<unsigned long long, MODE> {
 template <typename U> constexpr int hist_lanes() { return sizeof(U) == 4 ? 32 : 16; }
 
 struct LsdLayout {
-  size_t scratch, ghist, bases, gcount, plan, counters, lookback, total;
+  size_t scratch, ghist, bases, gcount, joint, seg, plan, counters, lookback, total;
 };
+
+// Pass 1 may run look-back-free (RANK_J01) from the joint histogram of digits 0 and 1; below
+// this size the digit-0 buckets are shorter than a tile anyway and the joint histogram's fixed
+// cost (65536 bins) is not worth it.
+constexpr uint64_t JOINT_MIN_N = 1ull << 24;
 
 template <typename U>
 LsdLayout lsd_layout(uint64_t n) {
@@ -43,8 +49,11 @@ LsdLayout lsd_layout(uint64_t n) {
   l.ghist = off;    off = align_up(off + P * 256 * 8, 256);
   l.bases = off;    off = align_up(off + P * 256 * 8, 256);
   l.gcount = off;   off = align_up(off + P * 256 * 8, 256);
+  const size_t jbytes = n >= JOINT_MIN_N ? 65536 * 8 : 0;  // joint histogram + segment starts
+  l.joint = off;    off = align_up(off + jbytes, 256);
+  l.seg = off;      off = align_up(off + jbytes, 256);
   l.plan = off;     off = align_up(off + sizeof(PassPlan), 256);
-  l.counters = off; off = align_up(off + 8 * 4, 256);
+  l.counters = off; off = align_up(off + 16 * 4, 256);
   l.lookback = off; off = align_up(off + tiles * 256 * desc, 256);
   l.total = off;
   return l;
@@ -101,21 +110,41 @@ bsort_status_t lsd_run(U* keys, uint64_t n, unsigned char* ws, cudaStream_t s) {
   auto* ghist = reinterpret_cast<unsigned long long*>(ws + l.ghist);
   auto* bases = reinterpret_cast<unsigned long long*>(ws + l.bases);
   auto* gcount = reinterpret_cast<unsigned long long*>(ws + l.gcount);
+  auto* joint = reinterpret_cast<unsigned long long*>(ws + l.joint);
+  auto* seg = reinterpret_cast<unsigned long long*>(ws + l.seg);
   auto* plan = reinterpret_cast<PassPlan*>(ws + l.plan);
   auto* counters = reinterpret_cast<uint32_t*>(ws + l.counters);
   auto* lookback = reinterpret_cast<DescT*>(ws + l.lookback);
   const uint64_t tiles = (n + TILE - 1) / TILE;
 
+  static const bool joint_off = getenv("BSORT_NO_JOINT") != nullptr;  // A/B and debugging
+  const bool use_joint = n >= JOINT_MIN_N && !joint_off;
   BSORT_LAUNCH(PROF_MEMSET, s, cudaMemsetAsync(ghist, 0, P * 256 * 8, s));
-  auto hk = k_onesweep_hist<KIND, DESC, U, LANES>;
-  constexpr int hsmem = P * 256 * LANES * 4;
-  static bool hattr = false;
-  if (!hattr) {
-    BSORT_CUDA(cudaFuncSetAttribute(hk, cudaFuncAttributeMaxDynamicSharedMemorySize, hsmem));
-    hattr = true;
+  if (use_joint) {
+    constexpr int JL = sizeof(U) == 4 ? 32 : 8;  // lanes of the digit >= 2 counters
+    auto hk = k_onesweep_hist_joint<KIND, DESC, U, JL>;
+    constexpr int hsmem = (32768 + (P - 2) * 256 * JL) * 4;
+    static bool hattr = false;
+    if (!hattr) {
+      BSORT_CUDA(cudaFuncSetAttribute(hk, cudaFuncAttributeMaxDynamicSharedMemorySize, hsmem));
+      hattr = true;
+    }
+    BSORT_LAUNCH(PROF_MEMSET, s, cudaMemsetAsync(joint, 0, 65536 * 8, s));
+    BSORT_LAUNCH(PROF_HIST, s, hk<<<num_sms(), HIST_THREADS, hsmem, s>>>(keys, n, ghist, joint));
+  } else {
+    auto hk = k_onesweep_hist<KIND, DESC, U, LANES>;
+    constexpr int hsmem = P * 256 * LANES * 4;
+    static bool hattr = false;
+    if (!hattr) {
+      BSORT_CUDA(cudaFuncSetAttribute(hk, cudaFuncAttributeMaxDynamicSharedMemorySize, hsmem));
+      hattr = true;
+    }
+    BSORT_LAUNCH(PROF_HIST, s, hk<<<num_sms(), HIST_THREADS, hsmem, s>>>(keys, n, ghist));
   }
-  BSORT_LAUNCH(PROF_HIST, s, hk<<<num_sms(), HIST_THREADS, hsmem, s>>>(keys, n, ghist));
-  BSORT_LAUNCH(PROF_SCAN, s, k_plan<<<1, 256, 0, s>>>(ghist, n, P, bases, plan, counters, gcount));
+  BSORT_LAUNCH(PROF_SCAN, s,
+               k_plan<<<1, 256, 0, s>>>(ghist, n, P, bases, plan, counters, gcount, use_joint ? joint : nullptr));
+  if (use_joint)
+    BSORT_LAUNCH(PROF_SCAN, s, k_plan_joint<<<1, 256, 0, s>>>(joint, ghist, bases + 256, TILE, plan, seg));
   bsort_status_t st = BSORT_SUCCESS;
   auto one_pass = [&](auto shift_c) {
     constexpr int SH = decltype(shift_c)::value;
@@ -134,6 +163,12 @@ bsort_status_t lsd_run(U* keys, uint64_t n, unsigned char* ws, cudaStream_t s) {
       st = launch_pass<U, RANK_RUN2, DescT>(keys, scratch, n, RadixDigit<KIND, DESC, U, SH>{},
                                                  bases + p * 256, lookback, gcount + p * 256, counters + p,
                                                  plan, p, s);
+    // pass 1 without look-back when the joint plan allows it (each launch checks plan->j01
+    // and exactly one of the two does the work)
+    if constexpr (p == 1)
+      if (st == BSORT_SUCCESS && use_joint)
+        st = launch_pass<U, RANK_J01, DescT>(keys, scratch, n, RadixDigit<KIND, DESC, U, SH>{}, bases + 256,
+                                             lookback, seg, counters + 8, plan, p, s);
   };
   one_pass(std::integral_constant<int, 0>{});
   one_pass(std::integral_constant<int, 8>{});

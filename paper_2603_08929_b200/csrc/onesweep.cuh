@@ -106,7 +106,8 @@ struct PassPlan {
   uint32_t src_alt[8];  // executed pass p reads the scratch buffer (and writes the user buffer)
   uint32_t final_copy;  // odd number of executed passes: result is in scratch, copy back
   uint32_t executed;    // number of executed passes
-  uint32_t pad[14];
+  uint32_t j01;         // pass 1 runs as RANK_J01 (every nonzero digit-0 bucket >= one tile)
+  uint32_t pad[13];
 };
 
 // Digit of LSD pass p: byte p of the transformed key (SHIFT = 8p is a compile-time constant so
@@ -200,14 +201,164 @@ __global__ void __launch_bounds__(HIST_THREADS, 1)
   }
 }
 
+// a3 with the joint histogram of the two lowest digits (pass 1 without look-back, RANK_J01):
+// J[d1 * 256 + d0] counted in 65536 u16 halves of 32768 smem words (a half that reaches 0x8000
+// is drained to the global count), the digits >= 2 lane-banked as above.  d0 is the fast index
+// so that nearly sorted keys spread over banks; a warp whose 32 keys share one joint bin (runs
+// of equal keys) adds once.  The marginals of digits 0 and 1 are derived from J by k_plan.  One
+// read of the keys.
+template <int KIND, bool DESC, typename U, int LANES>
+__global__ void __launch_bounds__(HIST_THREADS, 1)
+    k_onesweep_hist_joint(const U* __restrict__ keys, uint64_t n, unsigned long long* __restrict__ ghist,
+                          unsigned long long* __restrict__ gjoint) {
+  constexpr int P = sizeof(U);
+  extern __shared__ uint32_t hs[];  // [32768 joint words][P-2][256][LANES]
+  uint32_t* hj = hs;
+  uint32_t* hd = hs + 32768;
+  for (int i = threadIdx.x; i < 32768 + (P - 2) * 256 * LANES; i += HIST_THREADS) hs[i] = 0;
+  __syncthreads();
+  const uint32_t lane = threadIdx.x & (LANES - 1);
+  auto add_joint = [&](uint32_t jb, uint32_t inc) {  // jb = d1 * 256 + d0
+    const uint32_t sh = (jb & 1u) << 4;
+    const uint32_t old = atomicAdd(&hj[jb >> 1], inc << sh);
+    const uint32_t h = (old >> sh) & 0xFFFFu;
+    if (h < 0x8000u && h + inc >= 0x8000u) {  // this add took the half to >= 0x8000: drain
+      atomicAdd(&hj[jb >> 1], 0u - (0x8000u << sh));
+      atomicAdd(&gjoint[jb], 0x8000ull);
+    }
+  };
+  auto add_high = [&](U k) {
+#pragma unroll
+    for (int p = 2; p < P; ++p) {
+      const uint32_t d = uint32_t(k >> (8 * p)) & 0xFFu;
+      atomicAdd(&hd[((p - 2) * 256 + d) * LANES + lane], 1u);
+    }
+  };
+  // scalar keys (ragged head/tail, divergent): no warp collectives
+  auto add = [&](U x) {
+    const U k = key_encode<KIND, DESC>(x);
+    add_joint(uint32_t(k) & 0xFFFFu, 1u);
+    add_high(k);
+  };
+  constexpr int PER_VEC = 16 / sizeof(U);
+  // a full vector of PER_VEC consecutive keys, called by whole warps: equal joint bins within
+  // the thread, and within the warp, are added once (runs of equal keys do not serialize)
+  auto add_vec = [&](const U (&kv)[PER_VEC]) {
+    U k[PER_VEC];
+    uint32_t jb[PER_VEC];
+    bool same = true;
+#pragma unroll
+    for (int j = 0; j < PER_VEC; ++j) {
+      k[j] = key_encode<KIND, DESC>(kv[j]);
+      jb[j] = uint32_t(k[j]) & 0xFFFFu;
+      same &= jb[j] == jb[0];
+    }
+    const uint32_t j0 = __shfl_sync(0xffffffffu, jb[0], 0);  // every lane (no short-circuit)
+    const bool uniform = __all_sync(0xffffffffu, same & (jb[0] == j0));
+    if (uniform) {
+      if ((threadIdx.x & 31) == 0) add_joint(jb[0], 32u * PER_VEC);
+    } else if (same) {
+      add_joint(jb[0], PER_VEC);
+    } else {
+#pragma unroll
+      for (int j = 0; j < PER_VEC; ++j) add_joint(jb[j], 1u);
+    }
+#pragma unroll
+    for (int j = 0; j < PER_VEC; ++j) add_high(k[j]);
+  };
+  const uint64_t T = (uint64_t)gridDim.x * HIST_THREADS;
+  const uint64_t gt = (uint64_t)blockIdx.x * HIST_THREADS + threadIdx.x;
+  const uint64_t head = min64(n, ((16 - ((uintptr_t)keys & 15)) & 15) / sizeof(U));
+  for (uint64_t i = gt; i < head; i += T) add(keys[i]);
+  const uint4* v = reinterpret_cast<const uint4*>(keys + head);
+  const uint64_t nv = (n - head) / PER_VEC;
+  auto vec = [&](uint4 q) {
+    if constexpr (sizeof(U) == 4) {
+      const U kv[4] = {U(q.x), U(q.y), U(q.z), U(q.w)};
+      add_vec(kv);
+    } else {
+      const U kv[2] = {U(q.x) | (U(q.y) << 32), U(q.z) | (U(q.w) << 32)};
+      add_vec(kv);
+    }
+  };
+  // whole warps iterate together (collectives inside): the loop bound is warp-uniform
+  const uint64_t wbase = gt & ~uint64_t(31);
+  uint64_t i = gt;
+  for (; wbase + (i - gt) + 3 * T + 31 < nv; i += 4 * T) {
+    uint4 q0 = __ldcs(v + i), q1 = __ldcs(v + i + T), q2 = __ldcs(v + i + 2 * T), q3 = __ldcs(v + i + 3 * T);
+    vec(q0); vec(q1); vec(q2); vec(q3);
+  }
+  for (; i < nv; i += T) {  // remaining vectors: per key (a warp may be partial here)
+    const uint4 q = __ldcs(v + i);
+    if constexpr (sizeof(U) == 4) {
+      add(U(q.x)); add(U(q.y)); add(U(q.z)); add(U(q.w));
+    } else {
+      add(U(q.x) | (U(q.y) << 32));
+      add(U(q.z) | (U(q.w) << 32));
+    }
+  }
+  for (uint64_t j = head + nv * PER_VEC + gt; j < n; j += T) add(keys[j]);
+  __syncthreads();
+  for (int w = threadIdx.x; w < 32768; w += HIST_THREADS) {
+    const uint32_t c = hj[w];
+    if (c & 0xFFFFu) atomicAdd(&gjoint[2 * w], (unsigned long long)(c & 0xFFFFu));
+    if (c >> 16) atomicAdd(&gjoint[2 * w + 1], (unsigned long long)(c >> 16));
+  }
+  for (int b = threadIdx.x; b < (P - 2) * 256; b += HIST_THREADS) {
+    uint32_t s = 0;
+#pragma unroll 8
+    for (int l = 0; l < LANES; ++l) s += hd[b * LANES + ((l + b) & (LANES - 1))];
+    if (s) atomicAdd(&ghist[512 + b], (unsigned long long)s);
+  }
+}
+
+// Joint plan for RANK_J01 (one CTA of 256 threads, after k_plan): pass 1 may skip the look-back
+// when every nonzero digit-0 bucket holds at least `tile` keys -- then any tile-sized window of
+// the pass-0 output meets at most two digit-0 runs.  Segment (d1 = a, d0 = b) of the pass-1
+// output starts at bases1[a] + sum_{b' < b} J[a][b']; those starts seed the allocation counters
+// (seg[b * 256 + a], the layout RANK_J01 indexes by (run's d0, digit)).
+__global__ void __launch_bounds__(256)
+    k_plan_joint(const unsigned long long* __restrict__ gjoint, const unsigned long long* __restrict__ ghist,
+                 const unsigned long long* __restrict__ bases1, uint64_t tile, PassPlan* __restrict__ plan,
+                 unsigned long long* __restrict__ seg) {
+  const uint32_t t = threadIdx.x;
+  const unsigned long long c0 = ghist[t];  // digit-0 marginal
+  const int eligible = __syncthreads_and(c0 == 0 || c0 >= tile);
+  if (t == 0) plan->j01 = (uint32_t)eligible && !plan->skip[1];
+  if (!eligible) return;
+  unsigned long long run = bases1[t];
+  const ulonglong2* row = reinterpret_cast<const ulonglong2*>(gjoint + t * 256);  // row a = t
+  for (int b = 0; b < 128; ++b) {
+    const ulonglong2 q = row[b];
+    seg[(2 * b) * 256 + t] = run;
+    run += q.x;
+    seg[(2 * b + 1) * 256 + t] = run;
+    run += q.y;
+  }
+}
+
 // Plan: exclusive scan of every digit histogram into global digit bases, trivial-digit
 // detection, ping-pong buffer assignment, tile-counter reset.  One CTA of 256 threads.
 __global__ void __launch_bounds__(256)
-    k_plan(const unsigned long long* __restrict__ ghist, uint64_t n, int P, unsigned long long* __restrict__ bases,
+    k_plan(unsigned long long* __restrict__ ghist, uint64_t n, int P, unsigned long long* __restrict__ bases,
            PassPlan* __restrict__ plan, uint32_t* __restrict__ tile_counters,
-           unsigned long long* __restrict__ gcount) {
+           unsigned long long* __restrict__ gcount, const unsigned long long* __restrict__ gjoint) {
   __shared__ unsigned long long wt[256 / 32 + 1];
   __shared__ uint32_t skip_s[8];
+  if (gjoint != nullptr) {  // marginals of digits 1 (row sums) and 0 (column sums) of J[d1][d0]
+    unsigned long long r = 0, c = 0;
+    const ulonglong2* row = reinterpret_cast<const ulonglong2*>(gjoint + threadIdx.x * 256);
+#pragma unroll 8
+    for (int a = 0; a < 128; ++a) {
+      const ulonglong2 q = row[a];
+      r += q.x + q.y;
+    }
+#pragma unroll 8
+    for (int b = 0; b < 256; ++b) c += gjoint[b * 256 + threadIdx.x];
+    ghist[threadIdx.x] = c;
+    ghist[256 + threadIdx.x] = r;
+    __syncthreads();
+  }
   for (int p = 0; p < P; ++p) {
     const unsigned long long c = ghist[p * 256 + threadIdx.x];
     const unsigned long long ex = block_exclusive_scan<256>(c, wt, (unsigned long long*)nullptr);
@@ -229,8 +380,9 @@ __global__ void __launch_bounds__(256)
     }
     plan->final_copy = alt;
     plan->executed = executed;
+    plan->j01 = 0;  // k_plan_joint (if launched) may enable the look-back-free pass 1
   }
-  if (threadIdx.x < 8) tile_counters[threadIdx.x] = 0;
+  if (threadIdx.x < 16) tile_counters[threadIdx.x] = 0;  // 8 passes + the J01 pass
   if (gcount != nullptr)
     for (int p = 0; p < P; ++p) gcount[p * 256 + threadIdx.x] = 0;  // unstable-pass digit counters
 }
@@ -259,12 +411,17 @@ __global__ void __launch_bounds__(256)
 //        by (run, digit) over 512 block counters -- keys with equal (run, digit) have equal low
 //        8(p+1) bits, so their order is irrelevant, and run 0 precedes run 1 within a digit:
 //        exactly the stable order.  Otherwise the tile falls back to RANK_STABLE.
+//      RANK_J01 (LSD pass 1 when k_plan_joint found every nonzero digit-0 bucket at least one
+//        tile long): as RUN2's unstable path, but the (digit-1, digit-0) segment of every key is
+//        known from the joint histogram, so each (run, digit) bin of the tile takes its global
+//        offset with one atomicAdd on its segment counter -- no look-back (order inside a
+//        segment is irrelevant: equal low 16 bits).
 //   3. per-digit totals; look-back modes publish the tile's counts early (flag AGG; tile 0
 //      publishes INC); block scan => tile offsets; keys restaged in smem in digit order (in
 //      buffer `cur`; its keys now live in registers).
 //   4. look-back modes: decoupled look-back => global digit offsets.
 //   5. coalesced write-out of the digit-sorted tile: runs of equal digits are contiguous.
-enum RankMode : int { RANK_STABLE = 0, RANK_UNSTABLE = 1, RANK_RUN2 = 2 };
+enum RankMode : int { RANK_STABLE = 0, RANK_UNSTABLE = 1, RANK_RUN2 = 2, RANK_J01 = 3 };
 
 // Block counters of the unstable ranking are replicated BREP ways (replica = lane % BREP): lanes
 // of one warp instruction that share a digit hit BREP different words, so same-address atomic
@@ -281,7 +438,7 @@ struct PassSmem {
   static constexpr size_t rows_off = align_up(buf_off + 2 * sizeof(U) * TILE, 16);
   static constexpr size_t bcnt_off = align_up(rows_off + 2048 * rows, 16);
   static constexpr size_t gofs_off = align_up(bcnt_off + sizeof(uint32_t) * 512 * BREP, 16);
-  static constexpr size_t wt_off = align_up(gofs_off + sizeof(unsigned long long) * 256, 16);
+  static constexpr size_t wt_off = align_up(gofs_off + sizeof(unsigned long long) * 512, 16);
   static constexpr size_t mbar_off = align_up(wt_off + sizeof(uint32_t) * (WARPS + 1), 16);
   static constexpr size_t tile_off = mbar_off + 16;  // uint32 tile id held by each buffer
   static constexpr size_t bytes = align_up(tile_off + 16, 128);
@@ -331,7 +488,8 @@ __global__ void __launch_bounds__(THREADS, MINB)
   constexpr int TILE = L::TILE;
   constexpr int WARPS = L::WARPS;
   constexpr int SEG = 32 * ITEMS;  // keys per warp segment
-  constexpr bool LOOKBACK = MODE != RANK_UNSTABLE;
+  constexpr bool LOOKBACK = MODE == RANK_STABLE || MODE == RANK_RUN2;
+  constexpr bool RUNS = MODE == RANK_RUN2 || MODE == RANK_J01;  // bins carry the digit-0 run
   static_assert(THREADS >= 256 && THREADS % 32 == 0, "one thread per digit");
   static_assert(TILE < (1 << 22), "rank fits 22 bits");
   static_assert((TILE * sizeof(U)) % 16 == 0, "bulk copies need 16-byte tiles");
@@ -348,6 +506,11 @@ __global__ void __launch_bounds__(THREADS, MINB)
   U* dst = b_ptr;
   if (plan != nullptr) {
     if (plan->skip[pass]) return;
+    if constexpr (MODE == RANK_J01) {
+      if (!plan->j01) return;  // the RUN2 launch of this pass runs instead
+    } else if constexpr (MODE == RANK_RUN2) {
+      if (pass == 1 && plan->j01) return;  // the J01 launch of this pass runs instead
+    }
     if (plan->src_alt[pass]) {
       src = b_ptr;
       dst = const_cast<U*>(a_ptr);
@@ -428,7 +591,7 @@ __global__ void __launch_bounds__(THREADS, MINB)
       if (full) {
 #pragma unroll
         for (int k = 0; k < ITEMS; ++k) keys[k] = buf[seg + 32 * k];
-        if constexpr (MODE == RANK_RUN2) {
+        if constexpr (RUNS) {
           first_key = buf[0];
           last_key = buf[TILE - 1];
         }
@@ -439,7 +602,7 @@ __global__ void __launch_bounds__(THREADS, MINB)
           const uint32_t i = seg + 32 * k;
           keys[k] = i < bk ? buf[i] : (i < valid ? ldg_nc(src + tile_base + i) : U(0));
         }
-        if constexpr (MODE == RANK_RUN2) {
+        if constexpr (RUNS) {
           first_key = bk > 0 ? buf[0] : ldg_nc(src + tile_base);
           last_key = valid - 1 < bk ? buf[valid - 1] : ldg_nc(src + tile_base + valid - 1);
         }
@@ -453,7 +616,7 @@ __global__ void __launch_bounds__(THREADS, MINB)
         for (int k = 0; k < ITEMS; ++k)
           keys[k] = (seg + 32 * k < valid) ? ldg_nc(src + tile_base + seg + 32 * k) : U(0);
       }
-      if constexpr (MODE == RANK_RUN2) {
+      if constexpr (RUNS) {
         first_key = ldg_nc(src + tile_base);
         last_key = ldg_nc(src + tile_base + valid - 1);
       }
@@ -461,10 +624,14 @@ __global__ void __launch_bounds__(THREADS, MINB)
 
     // Ranking strategy of this tile (block-uniform); the barrier also orders the zeroing of
     // the block counters before their first atomic.
-    bool unstable_rank = MODE == RANK_UNSTABLE;
-    U low_first = U(0);
-    if constexpr (MODE == RANK_RUN2) {
-      U low_last, lo;
+    bool unstable_rank = MODE == RANK_UNSTABLE || MODE == RANK_J01;
+    U low_first = U(0), low_last = U(0);
+    if constexpr (MODE == RANK_J01) {
+      digit.digit_low(first_key, &low_first);
+      digit.digit_low(last_key, &low_last);
+      __syncthreads();  // counters zeroed before the atomics
+    } else if constexpr (MODE == RANK_RUN2) {
+      U lo;
       digit.digit_low(first_key, &low_first);
       digit.digit_low(last_key, &low_last);
       bool bad = false;
@@ -487,7 +654,7 @@ __global__ void __launch_bounds__(THREADS, MINB)
         if (full || seg + 32 * k < valid) {
           U lo;
           uint32_t bin = digit.digit_low(keys[k], &lo);
-          if constexpr (MODE == RANK_RUN2) bin |= (lo != low_first) ? 256u : 0u;
+          if constexpr (RUNS) bin |= (lo != low_first) ? 256u : 0u;
           info[k] = bin | (atomicAdd(&bcnt[bin * BREP + (lane & (BREP - 1))], 1u) << 9);
         } else {
           info[k] = 0xFFFFFFFFu;
@@ -518,13 +685,16 @@ __global__ void __launch_bounds__(THREADS, MINB)
 
     // 3. per-digit totals, early publish, tile offsets
     uint32_t total = 0, c0 = 0;
+    unsigned long long jg0 = 0, jg1 = 0;
     (void)c0;
+    (void)jg0;
+    (void)jg1;
     if (t < 256) {
       if (unstable_rank) {
         const uint4 r0 = reinterpret_cast<const uint4*>(bcnt)[t];
         c0 = r0.x + r0.y + r0.z + r0.w;
         total = c0;
-        if constexpr (MODE == RANK_RUN2) {
+        if constexpr (RUNS) {
           const uint4 r1 = reinterpret_cast<const uint4*>(bcnt)[256 + t];
           total += r1.x + r1.y + r1.z + r1.w;
         }
@@ -535,6 +705,11 @@ __global__ void __launch_bounds__(THREADS, MINB)
       }
       if constexpr (LOOKBACK) {
         st_relaxed(&lookback[(uint64_t)tile * 256 + t], (tile == 0 ? LB::INC : LB::AGG) | DescT(total));
+      }
+      if constexpr (MODE == RANK_J01) {  // allocate in the (digit, run) segments, tile order free
+        const uint32_t c1 = total - c0;
+        if (c0) jg0 = atomicAdd(&gcount[(uint32_t)low_first * 256 + t], (unsigned long long)c0);
+        if (c1) jg1 = atomicAdd(&gcount[(uint32_t)low_last * 256 + t], (unsigned long long)c1);
       }
     }
     const uint32_t tile_excl = block_exclusive_scan<THREADS>(t < 256 ? total : 0u, wt, (uint32_t*)nullptr);
@@ -550,7 +725,7 @@ __global__ void __launch_bounds__(THREADS, MINB)
         o0.z = run; run += r0.z;
         o0.w = run; run += r0.w;
         reinterpret_cast<uint4*>(bcnt)[t] = o0;
-        if constexpr (MODE == RANK_RUN2) {
+        if constexpr (RUNS) {
           uint4 r1 = reinterpret_cast<const uint4*>(bcnt)[256 + t];
           uint4 o1;
           o1.x = run; run += r1.x;
@@ -591,6 +766,9 @@ __global__ void __launch_bounds__(THREADS, MINB)
           st_relaxed(&lookback[(uint64_t)tile * 256 + t], LB::INC | (excl + DescT(total)));
         }
         gofs[t] = bases[t] + (unsigned long long)excl - tile_excl;
+      } else if constexpr (MODE == RANK_J01) {
+        gofs[t] = jg0 - tile_excl;
+        gofs[256 + t] = jg1 - (tile_excl + c0);
       } else {
         gofs[t] = bases[t] + gbase - tile_excl;
       }
@@ -603,7 +781,13 @@ __global__ void __launch_bounds__(THREADS, MINB)
       const uint32_t i = t + k * THREADS;
       if (full || i < valid) {
         const U x = buf[i];
-        dst[gofs[digit(x)] + i] = x;
+        if constexpr (MODE == RANK_J01) {
+          U lo;
+          const uint32_t d = digit.digit_low(x, &lo);
+          dst[gofs[d + (lo != low_first ? 256u : 0u)] + i] = x;
+        } else {
+          dst[gofs[digit(x)] + i] = x;
+        }
       }
     }
     if constexpr (BULK) {

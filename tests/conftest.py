@@ -36,3 +36,31 @@ def parse_golden(name):
             key, *vals = line.split()
             out[key] = vals
     return out
+
+
+# A kernel that never finishes would block pytest inside a CUDA call, where pytest-timeout's
+# signal cannot interrupt it.  For GPU tests a watchdog thread ends the process instead, so a
+# hang shows up as a failed run rather than a stalled one.
+_WATCHDOG_S = float(os.environ.get("BSORT_TEST_WATCHDOG_S", "900"))
+
+
+@pytest.fixture(autouse=True)
+def _gpu_watchdog(request):
+    if request.node.get_closest_marker("gpu") is None:
+        yield
+        return
+    import threading
+    done = threading.Event()
+
+    def watch():
+        if not done.wait(_WATCHDOG_S):
+            sys.stderr.write(f"\nwatchdog: {request.node.nodeid} exceeded {_WATCHDOG_S}s, aborting\n")
+            sys.stderr.flush()
+            os._exit(3)
+
+    t = threading.Thread(target=watch, daemon=True)
+    t.start()
+    try:
+        yield
+    finally:
+        done.set()

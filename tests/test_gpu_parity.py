@@ -191,3 +191,20 @@ def test_count16_drain_path(B, dtype):
     table = sview(gen(dtype, 3, 32))
     y = table[(W.bits(n, 33, "cuda") >> 62) % 3].view(dtype)
     check_equal(B, y, True, "3 distinct")
+
+
+@pytest.mark.parametrize("dtype", [torch.float32, torch.int32, torch.uint64, torch.float64])
+def test_joint_pass1_paths(B, dtype):
+    """n >= 2^24 switches the histogram to the joint (digit 0, digit 1) form.  Pass 1 then runs
+    look-back-free when every nonzero digit-0 bucket is at least one tile long (random keys), and
+    falls back to the look-back pass when one bucket is tiny (second case)."""
+    n = (1 << 24) + 12345
+    x = gen(dtype, n, 123)
+    check_equal(B, x.clone(), dtype == torch.float32, "joint-eligible")
+    es = x.element_size()
+    ib = {4: torch.int32, 8: torch.int64}[es]
+    b = x.view(ib).clone()
+    low = b & 0xFF
+    b = torch.where(low == 0x42, b + 1, b)       # empty digit-0 bucket 0x42 ...
+    b[:100] = (b[:100] & ~0xFF) | 0x42           # ... except for 100 keys
+    check_equal(B, b.view(dtype), False, "joint-ineligible")

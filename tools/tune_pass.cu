@@ -139,7 +139,7 @@ void suite(uint64_t n) {
   float hms;
   CK(cudaEventElapsedTime(&hms, a, b));
   printf("{\"hist_ms\": %.4f, \"hist_GBps\": %.1f}\n", hms, n * sizeof(U) / (hms * 1e-3) / 1e9);
-  k_plan<<<1, 256>>>(ghist, n, P, bases, plan, tc, nullptr);
+  k_plan<<<1, 256>>>(ghist, n, P, bases, plan, tc, nullptr, nullptr);
   CK(cudaMemset(dbg, 0, 16));
   k_sum<<<1184, 256>>>(in, n, dbg + 1);
   unsigned long long h[2];
@@ -149,10 +149,17 @@ void suite(uint64_t n) {
   if constexpr (sizeof(U) == 4) {
     run<U, 512, 16, 2, true, RANK_STABLE, 8>(in, out, n, bases, lookback, counter, gcount, ref, dbg);
     run<U, 512, 16, 2, true, RANK_RUN2, 8>(in, out, n, bases, lookback, counter, gcount, ref, dbg);
+    run<U, 512, 16, 2, true, RANK_RUN2, 16>(in, out, n, bases, lookback, counter, gcount, ref, dbg);
+    run<U, 512, 16, 2, true, RANK_RUN2, 32>(in, out, n, bases, lookback, counter, gcount, ref, dbg);
+    run<U, 1024, 16, 1, true, RANK_RUN2, 8>(in, out, n, bases, lookback, counter, gcount, ref, dbg);
+    run<U, 1024, 16, 1, true, RANK_RUN2, 16>(in, out, n, bases, lookback, counter, gcount, ref, dbg);
+    run<U, 1024, 16, 1, true, RANK_STABLE, 16>(in, out, n, bases, lookback, counter, gcount, ref, dbg);
     run<U, 512, 16, 2, true, RANK_UNSTABLE, 8>(in, out, n, bases, lookback, counter, gcount, ref, dbg);
   } else {
     run<U, 384, 12, 2, true, RANK_STABLE, 8>(in, out, n, bases, lookback, counter, gcount, ref, dbg);
     run<U, 384, 12, 2, true, RANK_RUN2, 8>(in, out, n, bases, lookback, counter, gcount, ref, dbg);
+    run<U, 384, 12, 2, true, RANK_RUN2, 16>(in, out, n, bases, lookback, counter, gcount, ref, dbg);
+    run<U, 768, 12, 1, true, RANK_RUN2, 16>(in, out, n, bases, lookback, counter, gcount, ref, dbg);
     run<U, 384, 12, 2, true, RANK_UNSTABLE, 8>(in, out, n, bases, lookback, counter, gcount, ref, dbg);
   }
   cudaFree(in);
