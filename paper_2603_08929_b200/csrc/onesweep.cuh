@@ -394,14 +394,17 @@ __global__ void __launch_bounds__(256)
 //   0. BULK: the tile was prefetched into smem buffer `cur` by a 1-D TMA bulk copy
 //      (cp.async.bulk, mbarrier completion) issued while the previous tile was processed.
 //      !BULK (source not 16-byte aligned): coalesced per-warp loads.
-//   1. keys -> registers, warp-striped: warp w owns the contiguous segment [w*32*ITEMS, ...),
-//      item k of lane l is element 32k+l of it, so (warp, item, lane) order IS index order.
+//   1. keys -> registers: half-warp h of warp w owns the contiguous keys
+//      [w*32*ITEMS + h*16*ITEMS, +16*ITEMS), item k of its lane l is element 16k+l of them, so
+//      (warp, half, item, lane) order IS index order (order-free modes read warp-striped).
 //   2. ranking (MODE):
-//      RANK_STABLE: warp-level multisplit in index order.  Per item, every lane ORs its bit into
-//        a per-warp per-digit mask word in smem and reads it back (its group of equal digits);
-//        the group's highest lane advances the warp's counter of that digit and clears the
-//        mask; rank = old count + lanes below in the group.  (MATCH.ANY, 8-ballot and
-//        leader-election grouping were measured slower on sm_100: DESIGN.md §6.)
+//      RANK_STABLE: half-warp multisplit in index order.  Each half-warp keeps one smem word per
+//        digit, {count so far : 16 | match mask : 16}.  Per item every lane ORs its bit into
+//        its digit's word and reads the word back (its group of equal digits and the count
+//        before this item, in one load); the group's highest lane stores the new count with
+//        a cleared mask; rank = old count + lanes below in the group.  (MATCH.ANY, 8-ballot and
+//        leader-election grouping, and separate mask/count words per warp, were measured
+//        slower on sm_100: DESIGN.md §6.)
 //      RANK_UNSTABLE (first LSD pass, MSD partition: the input order carries no information):
 //        one shared atomicAdd per key on block counters; the tile's per-digit global offsets
 //        come from one global atomicAdd per digit -- no look-back.
@@ -432,11 +435,13 @@ template <int THREADS, int ITEMS, typename U, int MODE>
 struct PassSmem {
   static constexpr int WARPS = THREADS / 32;
   static constexpr int TILE = THREADS * ITEMS;
-  // per-warp rows {u32 count[256], u32 mask[256]} for the multisplit; 512 block counters
+  // multisplit tables: per half-warp 256 words {count:16 | mask:16} (+16 words of padding so the
+  // two halves of a warp start 16 banks apart); 512 x BREP block counters
+  static constexpr int HALF_WORDS = 272;
   static constexpr int rows = MODE == RANK_UNSTABLE ? 0 : WARPS;
   static constexpr size_t buf_off = 0;  // U[2][TILE]
   static constexpr size_t rows_off = align_up(buf_off + 2 * sizeof(U) * TILE, 16);
-  static constexpr size_t bcnt_off = align_up(rows_off + 2048 * rows, 16);
+  static constexpr size_t bcnt_off = align_up(rows_off + 2 * HALF_WORDS * 4 * rows, 16);
   static constexpr size_t gofs_off = align_up(bcnt_off + sizeof(uint32_t) * 512 * BREP, 16);
   static constexpr size_t wt_off = align_up(gofs_off + sizeof(unsigned long long) * 512, 16);
   static constexpr size_t mbar_off = align_up(wt_off + sizeof(uint32_t) * (WARPS + 1), 16);
@@ -495,7 +500,7 @@ __global__ void __launch_bounds__(THREADS, MINB)
   static_assert((TILE * sizeof(U)) % 16 == 0, "bulk copies need 16-byte tiles");
   extern __shared__ __align__(128) unsigned char smem[];
   U* bufs = reinterpret_cast<U*>(smem + L::buf_off);
-  uint32_t* rows = reinterpret_cast<uint32_t*>(smem + L::rows_off);  // [warp][count 256 | mask 256]
+  uint32_t* rows = reinterpret_cast<uint32_t*>(smem + L::rows_off);  // [warp][half][HALF_WORDS]
   uint32_t* bcnt = reinterpret_cast<uint32_t*>(smem + L::bcnt_off);  // [512 bins][BREP]
   unsigned long long* gofs = reinterpret_cast<unsigned long long*>(smem + L::gofs_off);
   uint32_t* wt = reinterpret_cast<uint32_t*>(smem + L::wt_off);
@@ -520,7 +525,13 @@ __global__ void __launch_bounds__(THREADS, MINB)
   const uint32_t warp = threadIdx.x >> 5;
   const uint32_t t = threadIdx.x;
   const uint32_t lt = (1u << lane) - 1u;
-  uint32_t* wc = rows + warp * 512;  // this warp's counters; wc + 256: its match masks
+  constexpr int HW = L::HALF_WORDS;
+  const uint32_t half = lane >> 4;
+  const uint32_t l16 = lane & 15;
+  const uint32_t lt16 = (1u << l16) - 1u;
+  // this half-warp's table: word d = {count of digit d so far : 16 | match mask : 16}
+  uint32_t* wc = rows + (2 * warp + half) * HW;
+  (void)lt;
 
   auto tile_valid = [&](uint32_t tile) -> uint32_t {
     const uint64_t b = (uint64_t)tile * TILE;
@@ -531,10 +542,6 @@ __global__ void __launch_bounds__(THREADS, MINB)
     return (uint32_t)((valid * sizeof(U)) & ~(size_t)15) / (uint32_t)sizeof(U);
   };
 
-  if constexpr (MODE != RANK_UNSTABLE) {  // match masks start (and stay) at 0
-#pragma unroll
-    for (int j = 0; j < 8; ++j) wc[256 + lane + 32 * j] = 0;
-  }
   uint32_t phase0 = 0, phase1 = 0;
   if constexpr (BULK) {
     if (t == 0) {
@@ -573,16 +580,21 @@ __global__ void __launch_bounds__(THREADS, MINB)
     const bool full = valid == (uint32_t)TILE;
 
     // zero the counters (every read of them happened before the previous tile's last barrier)
-    if constexpr (MODE != RANK_UNSTABLE) {
+    if constexpr (MODE != RANK_UNSTABLE) {  // both half tables of this warp
 #pragma unroll
-      for (int j = 0; j < 8; ++j) wc[lane + 32 * j] = 0;
+      for (int j = 0; j < 16; ++j) wc[l16 + 16 * j] = 0;
     }
     if constexpr (MODE != RANK_STABLE) {
       for (int j = t; j < 512 * BREP / 4; j += THREADS) reinterpret_cast<uint4*>(bcnt)[j] = make_uint4(0, 0, 0, 0);
     }
 
     // 1. keys -> registers
-    const uint32_t seg = warp * SEG + lane;  // tile-local index of item 0
+    // tile-local index of item 0.  Stable-capable modes: half-warp h of warp w owns the
+    // contiguous keys [w*SEG + h*16*ITEMS, +16*ITEMS), item k of its lane l16 is element
+    // 16k + l16 of them.  Order-free modes: warp-striped (conflict-free loads from the buffer).
+    constexpr bool HALF_MAP = MODE == RANK_STABLE || MODE == RANK_RUN2;
+    constexpr uint32_t IS = HALF_MAP ? 16u : 32u;  // index stride between items
+    const uint32_t seg = HALF_MAP ? warp * SEG + half * (16 * ITEMS) + l16 : warp * SEG + lane;
     U keys[ITEMS];
     U first_key = U(0), last_key = U(0);
     if constexpr (BULK) {
@@ -590,7 +602,7 @@ __global__ void __launch_bounds__(THREADS, MINB)
       if (cur) phase1 ^= 1u; else phase0 ^= 1u;
       if (full) {
 #pragma unroll
-        for (int k = 0; k < ITEMS; ++k) keys[k] = buf[seg + 32 * k];
+        for (int k = 0; k < ITEMS; ++k) keys[k] = buf[seg + IS * k];
         if constexpr (RUNS) {
           first_key = buf[0];
           last_key = buf[TILE - 1];
@@ -599,7 +611,7 @@ __global__ void __launch_bounds__(THREADS, MINB)
         const uint32_t bk = bulk_keys(valid);
 #pragma unroll
         for (int k = 0; k < ITEMS; ++k) {
-          const uint32_t i = seg + 32 * k;
+          const uint32_t i = seg + IS * k;
           keys[k] = i < bk ? buf[i] : (i < valid ? ldg_nc(src + tile_base + i) : U(0));
         }
         if constexpr (RUNS) {
@@ -610,11 +622,11 @@ __global__ void __launch_bounds__(THREADS, MINB)
     } else {
       if (full) {
 #pragma unroll
-        for (int k = 0; k < ITEMS; ++k) keys[k] = ldg_nc(src + tile_base + seg + 32 * k);
+        for (int k = 0; k < ITEMS; ++k) keys[k] = ldg_nc(src + tile_base + seg + IS * k);
       } else {
 #pragma unroll
         for (int k = 0; k < ITEMS; ++k)
-          keys[k] = (seg + 32 * k < valid) ? ldg_nc(src + tile_base + seg + 32 * k) : U(0);
+          keys[k] = (seg + IS * k < valid) ? ldg_nc(src + tile_base + seg + IS * k) : U(0);
       }
       if constexpr (RUNS) {
         first_key = ldg_nc(src + tile_base);
@@ -638,7 +650,7 @@ __global__ void __launch_bounds__(THREADS, MINB)
 #pragma unroll
       for (int k = 0; k < ITEMS; ++k) {
         digit.digit_low(keys[k], &lo);
-        bad |= (full || seg + 32 * k < valid) && lo != low_first && lo != low_last;
+        bad |= (full || seg + IS * k < valid) && lo != low_first && lo != low_last;
       }
       unstable_rank = !__syncthreads_or(bad);
     } else if constexpr (MODE == RANK_UNSTABLE) {
@@ -651,7 +663,7 @@ __global__ void __launch_bounds__(THREADS, MINB)
       // invalid tail slots are not counted at all
 #pragma unroll
       for (int k = 0; k < ITEMS; ++k) {
-        if (full || seg + 32 * k < valid) {
+        if (full || seg + IS * k < valid) {
           U lo;
           uint32_t bin = digit.digit_low(keys[k], &lo);
           if constexpr (RUNS) bin |= (lo != low_first) ? 256u : 0u;
@@ -663,21 +675,18 @@ __global__ void __launch_bounds__(THREADS, MINB)
     } else if constexpr (MODE != RANK_UNSTABLE) {
       // Invalid tail slots take digit 255: they sit at the end of the tile in index order, so
       // they rank after every valid key of digit 255 and are dropped at write-out.
-      uint32_t* mm = wc + 256;
-      __syncwarp();  // counters zeroed by this warp
+      __syncwarp();  // tables zeroed by this warp
 #pragma unroll
       for (int k = 0; k < ITEMS; ++k) {
-        const uint32_t d = (full || seg + 32 * k < valid) ? digit(keys[k]) : 255u;
-        atomicOr(&mm[d], 1u << lane);
+        const uint32_t d = (full || seg + IS * k < valid) ? digit(keys[k]) : 255u;
+        atomicOr(&wc[d], 1u << l16);
         __syncwarp();
-        const uint32_t peers = mm[d];
-        const uint32_t old = wc[d];
-        const uint32_t below = __popc(peers & lt);
+        const uint32_t w = wc[d];  // {count before this item | this item's group}
+        const uint32_t peers = w & 0xFFFFu;
+        const uint32_t below = __popc(peers & lt16);
+        const uint32_t old = w >> 16;
         __syncwarp();
-        if ((peers >> lane) == 1u) {  // highest lane of the group
-          mm[d] = 0;
-          wc[d] = old + below + 1u;
-        }
+        if ((peers >> l16) == 1u) wc[d] = (old + below + 1u) << 16;  // highest lane: count, clear mask
         info[k] = d | ((old + below) << 9);
       }
     }
@@ -700,7 +709,7 @@ __global__ void __launch_bounds__(THREADS, MINB)
         }
       } else {
 #pragma unroll
-        for (int w = 0; w < WARPS; ++w) total += rows[w * 512 + t];
+        for (int h = 0; h < 2 * WARPS; ++h) total += rows[h * HW + t] >> 16;
         if (!full && t == 255) total -= (uint32_t)TILE - valid;  // invalid tail slots
       }
       if constexpr (LOOKBACK) {
@@ -739,9 +748,9 @@ __global__ void __launch_bounds__(THREADS, MINB)
       } else {
         uint32_t run = tile_excl;
 #pragma unroll
-        for (int w = 0; w < WARPS; ++w) {
-          const uint32_t c = rows[w * 512 + t];
-          rows[w * 512 + t] = run;
+        for (int h = 0; h < 2 * WARPS; ++h) {
+          const uint32_t c = rows[h * HW + t] >> 16;
+          rows[h * HW + t] = run;
           run += c;
         }
       }
