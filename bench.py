@@ -172,8 +172,13 @@ def bench_single(args, B):
 
     # roofline of the dominant kernel (onesweep pass): algorithmic bytes = read + write of
     # every key once per pass: 2 * n * 4 B per launch.
+    # One sort runs 4 LSD passes (8-bit digits of 32-bit keys; none of cfg3's digits is trivial)
+    # plus, at n >= 2^24, one extra pass-1 launch that exits at once (libbsort launches both
+    # pass-1 variants and the device plan picks one).  The per-pass time is therefore the total
+    # pass time / 4 (the idle launch's ~4 us is included: conservative).
     pk = prof.get("onesweep_pass", {"ms": float("nan"), "launches": 1})
-    pass_ms = pk["ms"] / pk["launches"]
+    passes = 4 * len(times)
+    pass_ms = pk["ms"] / passes
     pass_bytes = 2 * n * 4
     achieved = pass_bytes / (pass_ms / 1e3) / 1e9
     # whole-sort fraction against the fixed 36 B/key model
@@ -228,7 +233,8 @@ def bench_single(args, B):
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
                      "frac": achieved / hbm_peak, "traffic": load_traffic("onesweep_pass"),
                      "kernel": "k_onesweep_pass", "algorithmic_bytes_per_launch": pass_bytes,
-                     "avg_launch_ms": pass_ms, "peak_source": peak_src,
+                     "avg_launch_ms": pass_ms, "working_launches_per_step": 4,
+                     "launches_per_step": pk["launches"] / len(times), "peak_source": peak_src,
                      "whole_sort_36B_per_key_GBps": sort_gbs, "whole_sort_frac": sort_gbs / hbm_peak,
                      "kernel_share_of_step": kernel_share},
         "cpu_baseline": cpu,
@@ -283,7 +289,13 @@ def bench_extra(B, dev, stream, args):
 
 # ------------------------------------------------------------------------ multi-GPU (N>1)
 
+def nvlink_peak():
+    """Measured NVLink reference of this pool (B200_PROFILING.md): peer copy per direction."""
+    return 770.0, "B200_PROFILING.md measured peer copy 770 GB/s per direction (900 nominal)"
+
+
 def bench_multi(args, B):
+    """N > 1: one step = sort_dist of 2^30 cfg3-distributed f32 keys per rank (weak scaling)."""
     import torch.distributed as dist
     rank, world = dist.get_rank(), dist.get_world_size()
     local = int(os.environ.get("LOCAL_RANK", rank))
@@ -294,45 +306,84 @@ def bench_multi(args, B):
     pristine = cfg3_input(n, dev, rank)
     work = torch.empty_like(pristine)
     restore = lambda: work.copy_(pristine)  # noqa: E731
-    run = lambda: B.sort_dist(work)  # noqa: E731
     for _ in range(args.warmup):
         restore()
-        run()
+        B.sort_dist(work)
     torch.cuda.synchronize()
     dist.barrier()
     launches0 = B.launch_count()
-    times = []
+    a2a = []
     with ClockSampler(local) as clk:
-        for _ in range(args.steps):
-            restore()
-            torch.cuda.synchronize()
-            dist.barrier()
-            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            a.record(stream)
-            run()
-            b.record(stream)
-            torch.cuda.synchronize()
-            times.append(a.elapsed_time(b))
+        restore()
+        torch.cuda.synchronize()
+        dist.barrier()
+        a = torch.cuda.Event(enable_timing=True)
+        b = torch.cuda.Event(enable_timing=True)
+        step_ev = []
+        a.record(stream)
+        for i in range(args.steps):
+            # the restore copy is outside the step events but inside the bracket (input >> L2)
+            if i:
+                restore()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            B.sort_dist(work, a2a_events=a2a)
+            e1.record(stream)
+            step_ev.append((e0, e1))
+        b.record(stream)
+        torch.cuda.synchronize()
+        dist.barrier()
     launches = B.launch_count() - launches0
-    t = torch.tensor([sum(times)], dtype=torch.float64, device=dev)
+    step_ms = sum(e0.elapsed_time(e1) for e0, e1 in step_ev)
+    a2a_ms = sum(ev[0].elapsed_time(ev[1]) for ev, _ in a2a)
+    a2a_bytes = sum(nb for _, nb in a2a)
+    t = torch.tensor([step_ms, a2a_ms], dtype=torch.float64, device=dev)
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    ms = t.item() / args.steps
+    ms = t[0].item() / args.steps
+    a2a_max_ms = t[1].item() / args.steps
+
+    # end to end through the public API: pinned host keys -> H2D -> sort_dist -> D2H of the shard
+    host = pristine.cpu().pin_memory()
+    e_times, out_bytes = [], 0
+    for i in range(2):
+        dist.barrier()
+        torch.cuda.synchronize()
+        ea, eb = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        ea.record(stream)
+        work.copy_(host, non_blocking=True)
+        shard = B.sort_dist(work)
+        res = shard.cpu()
+        eb.record(stream)
+        torch.cuda.synchronize()
+        out_bytes = res.numel() * res.element_size()
+        if i:
+            e_times.append(ea.elapsed_time(eb))
+    te = torch.tensor([max(e_times)], dtype=torch.float64, device=dev)
+    dist.all_reduce(te, op=dist.ReduceOp.MAX)
     total = n * world
     if rank == 0:
-        hbm_peak, src = load_peaks()
+        nv_peak, nv_src = nvlink_peak()
+        per_rank_bytes = a2a_bytes / max(1, args.steps)
+        achieved = per_rank_bytes / (a2a_max_ms / 1e3) / 1e9 if a2a_max_ms > 0 else None
         line = {
             "metric": METRIC, "value": total / (ms / 1e3), "unit": UNIT, "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "u32", "data": "synthetic",
-            "config": {"workload": f"cfg3 distribution, 2^30 f32 keys per rank x {world} ranks, "
+            "config": {"workload": f"cfg3 distribution, {n} f32 keys per rank x {world} ranks, "
                                    "globally sorted shards (MSD top-16-bit split + NCCL all-to-all "
                                    "+ local one-sweep LSD)", "n_per_rank": n,
-                       "parallelism": f"msd-a2a x{world}"},
-            "roofline": {"bound": "hbm", "achieved": None, "peak": hbm_peak, "unit": "GB/s",
-                         "frac": None, "traffic": None, "peak_source": src,
-                         "note": "per-kernel roofline is reported by the N=1 run"},
+                       "parallelism": f"msd-a2a x{world}",
+                       "l2": "inputs of n*4 B per rank (4 GiB at the default n) >> L2; restored by D2D copy between steps"},
+            "roofline": {"bound": "nvlink", "achieved": achieved, "peak": nv_peak, "unit": "GB/s",
+                         "frac": (achieved / nv_peak) if achieved else None, "traffic": None,
+                         "kernel": "keys all-to-all (NCCL, rank 0's egress bytes / max-over-ranks time)",
+                         "a2a_ms_per_step": a2a_max_ms, "a2a_bytes_per_step_rank0": per_rank_bytes,
+                         "peak_source": nv_src},
             "cpu_baseline": None,
-            "e2e": None,
+            "e2e": {"value": total / (te.item() / 1e3), "unit": UNIT,
+                    "h2d_bytes_per_step": n * 4, "d2h_bytes_per_step": out_bytes,
+                    "ms_per_step": te.item(),
+                    "note": "per rank: pinned host keys -> H2D -> sort_dist -> D2H of the shard; max over ranks"},
             "gpu_launches": launches,
             "clocks": clk.summary(),
         }
@@ -380,6 +431,8 @@ def main():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--cpu-sample", type=int, default=1 << 25)
     ap.add_argument("--ref-sample", type=int, default=1 << 22)
+    ap.add_argument("--force-dist", action="store_true",
+                    help="run the multi-GPU code path even at world size 1 (testing)")
     args = ap.parse_args()
     if args.warmup < 3 and args.impl == "ours":
         args.warmup = 3
@@ -390,9 +443,11 @@ def main():
 
     import paper_2603_08929_b200 as B
     world = int(os.environ.get("WORLD_SIZE", "1"))
-    if world > 1:
+    if world > 1 or args.force_dist:
         import torch.distributed as dist
-        dist.init_process_group("nccl")
+        local = int(os.environ.get("LOCAL_RANK", "0"))
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
         try:
             bench_multi(args, B)
         finally:

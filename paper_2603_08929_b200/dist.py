@@ -53,11 +53,14 @@ class DistStats:
 
 
 def sort_dist(t: torch.Tensor, group=None, descending: bool = False,
-              ops: Optional[DistOps] = None, return_stats: bool = False):
+              ops: Optional[DistOps] = None, return_stats: bool = False,
+              a2a_events: Optional[list] = None):
     """Globally sort the keys held by all ranks of ``group``; returns this rank's shard.
 
     ``t`` (1-D, contiguous) may be clobbered.  The concatenation of the returned shards over
-    ranks 0..P-1 is the sorted sequence of all keys, in the requested direction."""
+    ranks 0..P-1 is the sorted sequence of all keys, in the requested direction.
+    ``a2a_events``: if a list is given (CUDA tensors only), a pair of timing events recorded
+    around the keys all-to-all on the current stream is appended to it."""
     ops = ops or cuda_ops()
     P = dist.get_world_size(group)
     hl = ops.top_hist(t, descending)
@@ -74,9 +77,16 @@ def sort_dist(t: torch.Tensor, group=None, descending: bool = False,
     bucketed = ops.partition(t, cuts, sc, descending)
     es = t.element_size()
     out = torch.empty(int(rc.sum()), dtype=t.dtype, device=t.device)
+    ev = None
+    if a2a_events is not None and t.is_cuda:
+        ev = (torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+        ev[0].record()
     dist.all_to_all_single(out.view(torch.uint8), bucketed.view(torch.uint8),
                            output_split_sizes=[int(c) * es for c in rc],
                            input_split_sizes=[int(c) * es for c in sc], group=group)
+    if ev is not None:
+        ev[1].record()
+        a2a_events.append((ev, int(sc.sum() - sc[dist.get_rank(group)]) * es))
     ops.local_sort(out, descending)
     if return_stats:
         return out, DistStats(cuts=cuts, send_counts=sc, recv_counts=rc.astype(np.uint64))
