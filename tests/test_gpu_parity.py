@@ -208,3 +208,18 @@ def test_joint_pass1_paths(B, dtype):
     b = torch.where(low == 0x42, b + 1, b)       # empty digit-0 bucket 0x42 ...
     b[:100] = (b[:100] & ~0xFF) | 0x42           # ... except for 100 keys
     check_equal(B, b.view(dtype), False, "joint-ineligible")
+
+
+@pytest.mark.parametrize("dtype", [torch.float64, torch.int64, torch.float32])
+def test_large_descending_misaligned_and_trivial(B, dtype):
+    """n >= 2^24 (joint histogram, J01/RUN2 passes) combined with: descending order, a caller
+    pointer that is not 16-byte aligned (per-warp loads instead of TMA, ragged head and tail in
+    the histogram), and keys confined to the low 24 bits (trivial high digits are skipped)."""
+    n = (1 << 24) + 777
+    base = gen(dtype, n + 3, 321)
+    view = base[1:n + 1]  # element-aligned, not 16-byte aligned
+    assert view.data_ptr() % 16 != 0
+    check_equal(B, view, True, "misaligned desc")
+    ib = {4: torch.int32, 8: torch.int64}[view.element_size()]
+    low = (W.bits(n, 654, "cuda") & 0xFFFFFF).to(ib)
+    check_equal(B, low.view(dtype), dtype == torch.int64, "low 24 bits")
