@@ -36,7 +36,9 @@
 extern "C" {
 #endif
 
-/* Key types: Table II word sizes plus the unsigned variants. Values are ABI. */
+/* Key types: Table II word sizes plus the unsigned variants, and the half-width
+ * floats f16/bf16 (the paper's method applies to any float layout sign | exponent | mantissa,
+ * P:498).  Values are ABI. */
 typedef enum {
   BSORT_U8 = 0,
   BSORT_I8 = 1,
@@ -47,7 +49,9 @@ typedef enum {
   BSORT_F32 = 6,
   BSORT_U64 = 7,
   BSORT_I64 = 8,
-  BSORT_F64 = 9
+  BSORT_F64 = 9,
+  BSORT_F16 = 10,  /* IEEE binary16 (1 | 5 | 10), same order rules as f32/f64 */
+  BSORT_BF16 = 11  /* bfloat16 (1 | 8 | 7) */
 } bsort_dtype_t;
 
 /* Sort direction: Algorithm 1's boolean `asc`. */

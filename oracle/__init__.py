@@ -71,7 +71,9 @@ NATIVE_SCHEMES = {
     np.dtype(np.float32): F(32, 8, 23),
     np.dtype(np.uint64): U(64), np.dtype(np.int64): I(64),
     np.dtype(np.float64): F(64, 11, 52),
+    np.dtype(np.float16): F(16, 5, 10),   # IEEE binary16
 }
+BF16 = F(16, 8, 7)  # bfloat16 (numpy has no dtype for it: sort its uint16 bit patterns)
 _UINT_OF_SIZE = {1: np.uint8, 2: np.uint16, 4: np.uint32, 8: np.uint64}
 
 _lib = None

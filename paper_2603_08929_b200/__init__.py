@@ -31,6 +31,7 @@ _TORCH_CODES = {
     torch.uint8: _lib.U8, torch.int8: _lib.I8, torch.uint16: _lib.U16, torch.int16: _lib.I16,
     torch.uint32: _lib.U32, torch.int32: _lib.I32, torch.float32: _lib.F32,
     torch.uint64: _lib.U64, torch.int64: _lib.I64, torch.float64: _lib.F64,
+    torch.float16: _lib.F16, torch.bfloat16: _lib.BF16,
 }
 
 

@@ -12,9 +12,9 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "libbsort.so")
 
 # bsort_dtype_t
-U8, I8, U16, I16, U32, I32, F32, U64, I64, F64 = range(10)
-DTYPE_NAMES = ["u8", "i8", "u16", "i16", "u32", "i32", "f32", "u64", "i64", "f64"]
-DTYPE_BYTES = [1, 1, 2, 2, 4, 4, 4, 8, 8, 8]
+U8, I8, U16, I16, U32, I32, F32, U64, I64, F64, F16, BF16 = range(12)
+DTYPE_NAMES = ["u8", "i8", "u16", "i16", "u32", "i32", "f32", "u64", "i64", "f64", "f16", "bf16"]
+DTYPE_BYTES = [1, 1, 2, 2, 4, 4, 4, 8, 8, 8, 2, 2]
 ASCENDING, DESCENDING = 0, 1
 DIST_BINS = 65536
 DIST_MAX_RANKS = 64

@@ -38,6 +38,8 @@ bool dtype_info(bsort_dtype_t dt, DtypeInfo* o) {
     case BSORT_U64: *o = {8, KIND_U}; return true;
     case BSORT_I64: *o = {8, KIND_I}; return true;
     case BSORT_F64: *o = {8, KIND_F}; return true;
+    case BSORT_F16: *o = {2, KIND_F}; return true;
+    case BSORT_BF16: *o = {2, KIND_F}; return true;
     default: return false;
   }
 }

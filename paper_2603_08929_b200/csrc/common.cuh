@@ -64,7 +64,7 @@ __host__ __device__ __forceinline__ U key_decode(U k) {
 // one LOP.  Returns the XOR constant replicated over the word.
 template <int KIND, bool DESC, int BYTES>
 __host__ __device__ constexpr uint32_t packed_xor() {
-  static_assert(KIND != KIND_F, "no 8/16-bit float keys");
+  static_assert(KIND != KIND_F, "half floats use Float16 in counting.cu, not an XOR constant");
   uint32_t lane = (KIND == KIND_I) ? (1u << (BYTES * 8 - 1)) : 0u;
   if (DESC) lane ^= (BYTES == 1) ? 0xFFu : 0xFFFFu;
   return BYTES == 1 ? lane * 0x01010101u : lane * 0x00010001u;

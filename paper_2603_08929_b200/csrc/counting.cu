@@ -145,6 +145,29 @@ __global__ void __launch_bounds__(FILL_THREADS)
 
 // ----------------------------------------------------------------------------- 16-bit
 
+// Transforms of two 16-bit keys packed in a u32 (enc2: key -> order key; dec2: inverse).
+// Integers: an XOR with a constant (sign flip and/or complement).  Half floats (f16, bf16):
+// per half, negative ? ~h : h | 0x8000 (the paper's sign -> exponent -> mantissa order with
+// negatives inverted), complemented for descending.
+template <uint32_t X>
+struct Xor16 {
+  __device__ __forceinline__ static uint32_t enc2(uint32_t w) { return w ^ X; }
+  __device__ __forceinline__ static uint32_t dec2(uint32_t e) { return e ^ X; }
+};
+template <bool DESC>
+struct Float16 {
+  static constexpr uint32_t D = DESC ? 0xFFFFFFFFu : 0u;
+  __device__ __forceinline__ static uint32_t enc2(uint32_t w) {
+    const uint32_t neg = ((w >> 15) & 0x00010001u) * 0xFFFFu;  // 0xFFFF in negative halves
+    return (w ^ (neg | 0x80008000u)) ^ D;
+  }
+  __device__ __forceinline__ static uint32_t dec2(uint32_t e) {
+    e ^= D;
+    const uint32_t pos = (e >> 15) & 0x00010001u;  // encoded top bit set <=> non-negative key
+    return e ^ (((pos ^ 0x00010001u) * 0xFFFFu) | (pos * 0x8000u));
+  }
+};
+
 constexpr int SCAN16_BLOCK = 1024;
 constexpr int SCAN16_BLOCKS = BINS16 / SCAN16_BLOCK;  // 64
 
@@ -154,7 +177,7 @@ constexpr int SCAN16_BLOCKS = BINS16 / SCAN16_BLOCK;  // 64
 // from the half and adds 0x8000 to the bin's global overflow counter.  At most CNT_THREADS
 // increments are in flight, so a half never wraps.  The CTA's residual u16 counts are written
 // as a row of `partial` (no atomics).
-template <uint32_t X>
+template <typename TR>
 __global__ void __launch_bounds__(CNT_THREADS, 1)
     k_count_hist16(const uint16_t* __restrict__ keys, uint64_t n, uint16_t* __restrict__ partial,
                    unsigned long long* __restrict__ ovf) {
@@ -170,7 +193,7 @@ __global__ void __launch_bounds__(CNT_THREADS, 1)
     }
   };
   auto vec = [&](uint4 q) {
-    uint32_t w[4] = {q.x ^ X, q.y ^ X, q.z ^ X, q.w ^ X};
+    uint32_t w[4] = {TR::enc2(q.x), TR::enc2(q.y), TR::enc2(q.z), TR::enc2(q.w)};
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
       add(w[j] & 0xFFFF);
@@ -184,9 +207,9 @@ __global__ void __launch_bounds__(CNT_THREADS, 1)
   const uint64_t vs = min64(nv, (uint64_t)blockIdx.x * per);
   const uint64_t ve = min64(nv, vs + per);
   if (blockIdx.x == 0)
-    for (uint64_t i = threadIdx.x; i < head; i += CNT_THREADS) add((keys[i] ^ X) & 0xFFFF);
+    for (uint64_t i = threadIdx.x; i < head; i += CNT_THREADS) add(TR::enc2(keys[i]) & 0xFFFF);
   if (blockIdx.x == gridDim.x - 1)
-    for (uint64_t i = head + (nv << 3) + threadIdx.x; i < n; i += CNT_THREADS) add((keys[i] ^ X) & 0xFFFF);
+    for (uint64_t i = head + (nv << 3) + threadIdx.x; i < n; i += CNT_THREADS) add(TR::enc2(keys[i]) & 0xFFFF);
   uint64_t i = vs + threadIdx.x;
   for (; i + 3 * CNT_THREADS < ve; i += 4 * CNT_THREADS) {
     uint4 q0 = ldg_stream(v + i), q1 = ldg_stream(v + i + CNT_THREADS);
@@ -221,7 +244,7 @@ __global__ void __launch_bounds__(SCAN16_BLOCK)
 // smem, local L2-resident).  Warp w owns a contiguous range of 16-byte output vectors, lane l
 // takes vectors l, l+32, ...: stores are coalesced and each lane's position only moves forward,
 // so after one two-level binary search the lane finds its bin by walking forward.
-template <uint32_t X>
+template <typename TR>
 __global__ void __launch_bounds__(FILL_THREADS)
     k_count_fill16(uint16_t* __restrict__ keys, uint64_t n, const unsigned long long* __restrict__ local,
                    const unsigned long long* __restrict__ tot) {
@@ -254,7 +277,7 @@ __global__ void __launch_bounds__(FILL_THREADS)
   const uint64_t head = min64(n, ((16 - ((uintptr_t)keys & 15)) & 15) >> 1);
   const uint64_t gt = (uint64_t)blockIdx.x * FILL_THREADS + threadIdx.x;
   const uint64_t T = (uint64_t)gridDim.x * FILL_THREADS;
-  for (uint64_t i = gt; i < head; i += T) keys[i] = uint16_t(bin_of(i) ^ X);
+  for (uint64_t i = gt; i < head; i += T) keys[i] = uint16_t(TR::dec2(bin_of(i)));
   uint4* v = reinterpret_cast<uint4*>(keys + head);
   const uint64_t nv = (n - head) >> 3;
   const uint64_t warps = T / 32;
@@ -275,7 +298,7 @@ __global__ void __launch_bounds__(FILL_THREADS)
     while (nxt <= p0) nxt = pre(++b + 1);
     uint4 q;
     if (nxt >= p0 + 8) {
-      const uint32_t w = (b * 0x00010001u) ^ X;
+      const uint32_t w = TR::dec2(b * 0x00010001u);
       q = make_uint4(w, w, w, w);
     } else {
       uint32_t w[4] = {0, 0, 0, 0};
@@ -286,11 +309,11 @@ __global__ void __launch_bounds__(FILL_THREADS)
         while (nn <= p0 + j) nn = pre(++bb + 1);
         w[j >> 1] |= bb << ((j & 1) * 16);
       }
-      q = make_uint4(w[0] ^ X, w[1] ^ X, w[2] ^ X, w[3] ^ X);
+      q = make_uint4(TR::dec2(w[0]), TR::dec2(w[1]), TR::dec2(w[2]), TR::dec2(w[3]));
     }
     v[i] = q;
   }
-  for (uint64_t j = head + (nv << 3) + gt; j < n; j += T) keys[j] = uint16_t(bin_of(j) ^ X);
+  for (uint64_t j = head + (nv << 3) + gt; j < n; j += T) keys[j] = uint16_t(TR::dec2(bin_of(j)));
 }
 
 // ------------------------------------------------------------------------ host launch
@@ -326,7 +349,7 @@ Count16Layout count16_layout() {
   return l;
 }
 
-template <uint32_t X>
+template <typename TR>
 bsort_status_t run16(uint16_t* keys, uint64_t n, void* ws, cudaStream_t s) {
   const Count16Layout l = count16_layout();
   auto* w = static_cast<unsigned char*>(ws);
@@ -337,16 +360,16 @@ bsort_status_t run16(uint16_t* keys, uint64_t n, void* ws, cudaStream_t s) {
   const int smem = (BINS16 / 2) * sizeof(uint32_t);
   static bool attr_set = false;  // idempotent; benign race
   if (!attr_set) {
-    BSORT_CUDA(cudaFuncSetAttribute(k_count_hist16<X>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    BSORT_CUDA(cudaFuncSetAttribute(k_count_hist16<TR>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
     attr_set = true;
   }
   const int rows = num_sms();
   BSORT_LAUNCH(PROF_MEMSET, s, cudaMemsetAsync(ovf, 0, BINS16 * sizeof(unsigned long long), s));
-  BSORT_LAUNCH(PROF_COUNT_HIST, s, k_count_hist16<X><<<rows, CNT_THREADS, smem, s>>>(keys, n, partial, ovf));
+  BSORT_LAUNCH(PROF_COUNT_HIST, s, k_count_hist16<TR><<<rows, CNT_THREADS, smem, s>>>(keys, n, partial, ovf));
   BSORT_LAUNCH(PROF_COUNT_SCAN, s,
                k_count_scan16<<<SCAN16_BLOCKS, SCAN16_BLOCK, 0, s>>>(partial, rows, ovf, local, tot));
   BSORT_LAUNCH(PROF_COUNT_FILL, s,
-               k_count_fill16<X><<<fill_grid(n / 8 + 1), FILL_THREADS, 0, s>>>(keys, n, local, tot));
+               k_count_fill16<TR><<<fill_grid(n / 8 + 1), FILL_THREADS, 0, s>>>(keys, n, local, tot));
   return BSORT_SUCCESS;
 }
 
@@ -371,10 +394,12 @@ bsort_status_t counting_sort(const DtypeInfo& di, void* keys, uint64_t n, bool d
                 : run8<packed_xor<KIND_I, false, 1>()>(k8, n, ws, s);
   }
   if (di.kind == KIND_U)
-    return desc ? run16<packed_xor<KIND_U, true, 2>()>(k16, n, ws, s)
-                : run16<packed_xor<KIND_U, false, 2>()>(k16, n, ws, s);
-  return desc ? run16<packed_xor<KIND_I, true, 2>()>(k16, n, ws, s)
-              : run16<packed_xor<KIND_I, false, 2>()>(k16, n, ws, s);
+    return desc ? run16<Xor16<packed_xor<KIND_U, true, 2>()>>(k16, n, ws, s)
+                : run16<Xor16<packed_xor<KIND_U, false, 2>()>>(k16, n, ws, s);
+  if (di.kind == KIND_I)
+    return desc ? run16<Xor16<packed_xor<KIND_I, true, 2>()>>(k16, n, ws, s)
+                : run16<Xor16<packed_xor<KIND_I, false, 2>()>>(k16, n, ws, s);
+  return desc ? run16<Float16<true>>(k16, n, ws, s) : run16<Float16<false>>(k16, n, ws, s);
 }
 
 }  // namespace bsort

@@ -60,7 +60,7 @@ def test_library_exports_every_declared_symbol(B):
 def test_enum_values_match_binding(B):
     from paper_2603_08929_b200 import _lib
     e = header_enums()
-    names = ["U8", "I8", "U16", "I16", "U32", "I32", "F32", "U64", "I64", "F64"]
+    names = ["U8", "I8", "U16", "I16", "U32", "I32", "F32", "U64", "I64", "F64", "F16", "BF16"]
     for i, nm in enumerate(names):
         assert e[f"BSORT_{nm}"] == i == getattr(_lib, nm)
     assert e["BSORT_ASCENDING"] == _lib.ASCENDING and e["BSORT_DESCENDING"] == _lib.DESCENDING

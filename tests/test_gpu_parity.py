@@ -163,7 +163,7 @@ def test_sort_host_roundtrip(B):
 
 
 def test_errors_raise(B):
-    t = torch.zeros(10, dtype=torch.float16, device="cuda")
+    t = torch.zeros(10, dtype=torch.complex64, device="cuda")
     with pytest.raises(TypeError):
         B.sort_(t)
     with pytest.raises(TypeError):
@@ -223,3 +223,22 @@ def test_large_descending_misaligned_and_trivial(B, dtype):
     ib = {4: torch.int32, 8: torch.int64}[view.element_size()]
     low = (W.bits(n, 654, "cuda") & 0xFFFFFF).to(ib)
     check_equal(B, low.view(dtype), dtype == torch.int64, "low 24 bits")
+
+
+@pytest.mark.parametrize("dtype", [torch.float16, torch.bfloat16])
+@pytest.mark.parametrize("descending", [False, True], ids=["asc", "desc"])
+def test_half_floats(B, dtype, descending):
+    """f16 / bf16 (N4 widening): every bit pattern incl. NaNs of both signs, +-0, +-inf and
+    subnormals, against the oracle's Float(16,5,10) / Float(16,8,7) schemes."""
+    scheme = oracle.F(16, 5, 10) if dtype == torch.float16 else oracle.BF16
+    for n in (0, 1, 2, 31, 1000, 65537, (1 << 20) + 13, 65536 * 3):
+        bits16 = W.uniform_int(torch.int16, n, 500 + n, "cuda")
+        if n == 65536 * 3:  # every pattern three times
+            bits16 = (torch.arange(n, device="cuda", dtype=torch.int64) % 65536).to(torch.int32).to(torch.int16)
+        x = bits16.view(dtype).clone()
+        words = x.view(torch.int16).cpu().numpy().view(np.uint16).astype(np.uint64)
+        ref = oracle.bsort(words, scheme, asc=not descending).astype(np.uint16)
+        B.sort_(x, descending=descending)
+        torch.cuda.synchronize()
+        got = x.view(torch.int16).cpu().numpy().view(np.uint16)
+        assert got.tobytes() == ref.tobytes(), f"{dtype} n={n}"

@@ -282,3 +282,28 @@ def test_all_permutations_small():
     exp = sorted(base)
     for perm in itertools.permutations(base):
         assert list(oracle.bsort(list(perm), oracle.U(3), True)) == exp
+
+
+def test_float16_matches_numpy_sort():
+    """binary16 (Float(16,5,10)): bsort order is numeric order with -0 before +0 (np.sort on f16)."""
+    rng = np.random.default_rng(16)
+    a = np.concatenate([rng.standard_normal(3000) * 100, rng.uniform(-6e4, 6e4, 3000),
+                        np.array([0.0, -0.0, np.inf, -np.inf, 6e-8, -6e-8, 65504, -65504] * 5)]).astype(np.float16)
+    rng.shuffle(a)
+    out = oracle.sort_native(a)
+    _float_bits_equal_numeric(out, np.sort(a))
+    assert oracle.sort_native(a, descending=True).tobytes() == out[::-1].tobytes()
+
+
+def test_bfloat16_matches_float32_order():
+    """bfloat16 words are the top halves of f32 words: sorting them as Float(16,8,7) must give the
+    same order as sorting the widened f32 values (the exact numeric order of the bf16 values)."""
+    rng = np.random.default_rng(17)
+    f = np.concatenate([rng.standard_normal(2000) * 1e3, np.array([0.0, -0.0, np.inf, -np.inf] * 4)])
+    w = (f.astype(np.float32).view(np.uint32) >> 16).astype(np.uint64)  # bf16 bit patterns
+    w = np.concatenate([w, np.array([0x7FC1, 0xFFC1, 0x0001, 0x8001], np.uint64)])  # NaNs, subnormals
+    rng.shuffle(w)
+    got = oracle.bsort(w, oracle.BF16, True)
+    widened = (got.astype(np.uint32) << 16).view(np.float32)
+    ref = oracle.sort_native((w.astype(np.uint32) << 16).view(np.float32))
+    assert np.array_equal(widened.view(np.uint32), ref.view(np.uint32))
