@@ -136,6 +136,23 @@ bsort_status_t bsort_dist_partition(bsort_dtype_t dtype, const void* dev_in, uin
                                     const uint64_t* host_send_counts, int nranks, void* dev_out,
                                     void* workspace, size_t workspace_bytes, void* stream);
 
+/* Fused partition + exchange.  As bsort_dist_partition, but every key of
+ * destination rank q is stored directly at a slot in the device byte range
+ * [dst_addrs[q], dst_addrs[q] + host_send_counts[q] * sizeof(key)) -- normally rank q's
+ * receive buffer mapped into this process (torch symmetric memory / CUDA IPC peer mapping over
+ * NVLink), at the offset where this rank's keys for q begin (the exclusive prefix, over source
+ * ranks, of what q receives).  No local bucketed copy and no separate keys all-to-all: the
+ * partition's coalesced write-out is the exchange.  Exactly host_send_counts[q] keys land in
+ * range q, in unspecified order.  dst_addrs (host, nranks entries) must be element-aligned and
+ * non-null where host_send_counts[q] > 0.  The caller synchronises the ranks (e.g. a barrier
+ * after this stream's work completes) before any rank reads its receive buffer.  Workspace as
+ * bsort_dist_partition_workspace_bytes(). */
+bsort_status_t bsort_dist_partition_remote(bsort_dtype_t dtype, const void* dev_in, uint64_t n,
+                                           bsort_direction_t direction, const uint32_t* host_cuts,
+                                           const uint64_t* host_send_counts, int nranks,
+                                           const uint64_t* host_dst_addrs, void* workspace,
+                                           size_t workspace_bytes, void* stream);
+
 /* ----------------------------------------------------------------------- diagnostics */
 
 const char* bsort_status_string(bsort_status_t status);

@@ -24,7 +24,8 @@ from . import _lib
 from ._lib import BsortError, check, lib
 
 __all__ = ["sort_", "sort", "Sorter", "sort_host", "sort_dist", "dtype_code", "workspace_bytes",
-           "top_hist", "splitters", "send_counts", "partition", "profile", "launch_count",
+           "top_hist", "splitters", "send_counts", "partition", "partition_remote", "profile",
+           "launch_count",
            "BsortError", "version"]
 
 _TORCH_CODES = {
@@ -188,6 +189,25 @@ def partition(t: torch.Tensor, cuts: np.ndarray, counts: np.ndarray,
                                    ctypes.c_void_p(out.data_ptr()), ctypes.c_void_p(ws.data_ptr()),
                                    wsb, _stream_ptr(t.device)), "bsort_dist_partition")
     return out
+
+
+def partition_remote(t: torch.Tensor, cuts: np.ndarray, counts: np.ndarray, dst_addrs,
+                     descending: bool = False) -> None:
+    """Fused partition + exchange (§8 N1): every key of destination q is written straight to
+    the device byte range starting at dst_addrs[q] (e.g. a peer rank's symmetric-memory receive
+    buffer at this rank's offset); exactly counts[q] keys land there."""
+    _check_tensor(t)
+    code = dtype_code(t.dtype)
+    c = np.ascontiguousarray(cuts, dtype=np.uint32)
+    sc = np.ascontiguousarray(counts, dtype=np.uint64)
+    da = np.ascontiguousarray(np.asarray(dst_addrs, dtype=np.uint64))
+    nranks = c.size - 1
+    wsb = int(lib.bsort_dist_partition_workspace_bytes(code, t.numel(), nranks))
+    ws = _workspace(wsb, t.device)
+    check(lib.bsort_dist_partition_remote(code, ctypes.c_void_p(t.data_ptr()), t.numel(),
+                                          int(bool(descending)), _u32p(c), _u64p(sc), nranks,
+                                          _u64p(da), ctypes.c_void_p(ws.data_ptr()), wsb,
+                                          _stream_ptr(t.device)), "bsort_dist_partition_remote")
 
 
 from .dist import sort_dist  # noqa: E402  (needs the helpers above)

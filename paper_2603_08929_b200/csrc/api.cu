@@ -241,7 +241,29 @@ bsort_status_t bsort_dist_partition(bsort_dtype_t dtype, const void* dev_in, uin
   if (!dev_out || !aligned_to(dev_out, di.bytes) || dev_out == dev_in) return BSORT_ERROR_INVALID_ARGUMENT;
   if (!workspace || !aligned_to(workspace, 256)) return BSORT_ERROR_INVALID_ARGUMENT;
   return dist_partition(di, dev_in, n, direction == BSORT_DESCENDING, cuts, send_counts, nranks, dev_out,
-                        workspace, workspace_bytes_, (cudaStream_t)stream);
+                        nullptr, workspace, workspace_bytes_, (cudaStream_t)stream);
+}
+
+bsort_status_t bsort_dist_partition_remote(bsort_dtype_t dtype, const void* dev_in, uint64_t n,
+                                           bsort_direction_t direction, const uint32_t* cuts,
+                                           const uint64_t* send_counts, int nranks,
+                                           const uint64_t* dst_addrs, void* workspace,
+                                           size_t workspace_bytes_, void* stream) {
+  DtypeInfo di;
+  bsort_status_t st = validate(dtype, dev_in, n, direction, &di);
+  if (st != BSORT_SUCCESS) return st;
+  if (di.bytes < 4) return BSORT_ERROR_UNSUPPORTED_DTYPE;
+  if (!cuts || !send_counts || !dst_addrs || nranks < 1 || nranks > BSORT_DIST_MAX_RANKS)
+    return BSORT_ERROR_INVALID_ARGUMENT;
+  if (cuts[0] != 0 || cuts[nranks] != BSORT_DIST_BINS) return BSORT_ERROR_INVALID_ARGUMENT;
+  for (int q = 0; q < nranks; ++q) {
+    if (cuts[q] > cuts[q + 1]) return BSORT_ERROR_INVALID_ARGUMENT;
+    if (send_counts[q] > 0 && (dst_addrs[q] == 0 || dst_addrs[q] % di.bytes != 0)) return BSORT_ERROR_INVALID_ARGUMENT;
+  }
+  if (n == 0) return BSORT_SUCCESS;
+  if (!workspace || !aligned_to(workspace, 256)) return BSORT_ERROR_INVALID_ARGUMENT;
+  return dist_partition(di, dev_in, n, direction == BSORT_DESCENDING, cuts, send_counts, nranks, nullptr,
+                        dst_addrs, workspace, workspace_bytes_, (cudaStream_t)stream);
 }
 
 // ------------------------------------------------------------------------ diagnostics

@@ -277,7 +277,7 @@ size_t part_layout(size_t* counters_off, size_t* bases_off, size_t* gcount_off) 
 
 template <int KIND, bool DESC, typename U>
 bsort_status_t part_run(const U* in, uint64_t n, const uint32_t* cuts, int nranks, U* out, unsigned char* ws,
-                        const unsigned long long* host_bases, cudaStream_t s) {
+                        const unsigned long long* host_bases, const unsigned long long* host_dst, cudaStream_t s) {
   size_t co, bo, go;
   const size_t total = part_layout(&co, &bo, &go);
   auto* counter = reinterpret_cast<uint32_t*>(ws + co);
@@ -287,10 +287,20 @@ bsort_status_t part_run(const U* in, uint64_t n, const uint32_t* cuts, int nrank
   // bases: exclusive offsets of each destination bucket (from the caller's send counts; the
   // pageable copy is staged before cudaMemcpyAsync returns).
   BSORT_CUDA(cudaMemcpyAsync(bases, host_bases, 256 * 8, cudaMemcpyHostToDevice, s));
+  auto fill = [&](auto& dg) {
+    for (int q = 0; q <= nranks; ++q) dg.cuts[q] = cuts[q];
+    for (int q = nranks + 1; q <= BSORT_DIST_MAX_RANKS; ++q) dg.cuts[q] = TOP_BINS;
+    dg.nranks = nranks;
+  };
+  if (host_dst != nullptr) {  // fused partition + exchange: write into the owners' buffers
+    RankDigit<KIND, DESC, U, true> dg;
+    fill(dg);
+    for (int q = 0; q < BSORT_DIST_MAX_RANKS; ++q) dg.dst_base[q] = q < nranks ? host_dst[q] : 0ull;
+    return launch_pass<U, RANK_UNSTABLE, uint32_t>(in, const_cast<U*>(in), n, dg, bases, (uint32_t*)nullptr, gcount,
+                                                   counter, nullptr, 0, s);
+  }
   RankDigit<KIND, DESC, U> dg;
-  for (int q = 0; q <= nranks; ++q) dg.cuts[q] = cuts[q];
-  for (int q = nranks + 1; q <= BSORT_DIST_MAX_RANKS; ++q) dg.cuts[q] = TOP_BINS;
-  dg.nranks = nranks;
+  fill(dg);
   return launch_pass<U, RANK_UNSTABLE, uint32_t>(in, out, n, dg, bases, (uint32_t*)nullptr, gcount, counter, nullptr,
                                                  0, s);
 }
@@ -322,8 +332,8 @@ size_t dist_partition_workspace_bytes(int bytes, uint64_t n, int nranks) {
 }
 
 bsort_status_t dist_partition(const DtypeInfo& di, const void* in, uint64_t n, bool desc, const uint32_t* cuts,
-                              const uint64_t* send_counts, int nranks, void* out, void* ws, size_t ws_bytes,
-                              cudaStream_t s) {
+                              const uint64_t* send_counts, int nranks, void* out, const uint64_t* dst_addrs,
+                              void* ws, size_t ws_bytes, cudaStream_t s) {
   if (ws_bytes < dist_partition_workspace_bytes(di.bytes, n, nranks)) return BSORT_ERROR_WORKSPACE_TOO_SMALL;
   if (n == 0) return BSORT_SUCCESS;
   unsigned long long hb[256];
@@ -334,17 +344,18 @@ bsort_status_t dist_partition(const DtypeInfo& di, const void* in, uint64_t n, b
   }
   if (acc != n) return BSORT_ERROR_INVALID_ARGUMENT;
   auto* w = static_cast<unsigned char*>(ws);
+  const auto* hd = reinterpret_cast<const unsigned long long*>(dst_addrs);
 #define PART(U_)                                                                                                  \
   {                                                                                                               \
     const U_* i_ = static_cast<const U_*>(in);                                                                    \
     U_* o_ = static_cast<U_*>(out);                                                                               \
     switch (di.kind * 2 + (desc ? 1 : 0)) {                                                                       \
-      case 0: return part_run<KIND_U, false, U_>(i_, n, cuts, nranks, o_, w, hb, s);                              \
-      case 1: return part_run<KIND_U, true, U_>(i_, n, cuts, nranks, o_, w, hb, s);                               \
-      case 2: return part_run<KIND_I, false, U_>(i_, n, cuts, nranks, o_, w, hb, s);                              \
-      case 3: return part_run<KIND_I, true, U_>(i_, n, cuts, nranks, o_, w, hb, s);                               \
-      case 4: return part_run<KIND_F, false, U_>(i_, n, cuts, nranks, o_, w, hb, s);                              \
-      default: return part_run<KIND_F, true, U_>(i_, n, cuts, nranks, o_, w, hb, s);                              \
+      case 0: return part_run<KIND_U, false, U_>(i_, n, cuts, nranks, o_, w, hb, hd, s);                              \
+      case 1: return part_run<KIND_U, true, U_>(i_, n, cuts, nranks, o_, w, hb, hd, s);                               \
+      case 2: return part_run<KIND_I, false, U_>(i_, n, cuts, nranks, o_, w, hb, hd, s);                              \
+      case 3: return part_run<KIND_I, true, U_>(i_, n, cuts, nranks, o_, w, hb, hd, s);                               \
+      case 4: return part_run<KIND_F, false, U_>(i_, n, cuts, nranks, o_, w, hb, hd, s);                              \
+      default: return part_run<KIND_F, true, U_>(i_, n, cuts, nranks, o_, w, hb, hd, s);                              \
     }                                                                                                             \
   }
   if (di.bytes == 4) PART(uint32_t)

@@ -114,6 +114,7 @@ struct PassPlan {
 // the digit is one funnel-shift + mask after the transform).
 template <int KIND, bool DESC, typename U, int SHIFT>
 struct RadixDigit {
+  static constexpr bool REMOTE = false;
   __device__ __forceinline__ uint32_t operator()(U x) const {
     return uint32_t(key_encode<KIND, DESC>(x) >> SHIFT) & 0xFFu;
   }
@@ -129,10 +130,15 @@ struct RadixDigit {
 };
 
 // Digit of the MSD partition: destination rank of the key's top-16-bit bin.
-template <int KIND, bool DESC, typename U>
+// REMOTE (fused partition + exchange, §8 N1): dst_base[q] is the byte address (peer-mapped
+// over NVLink when q is another GPU) of the first slot this rank owns in rank q's receive
+// buffer; the pass writes each key there directly instead of into a local bucketed copy.
+template <int KIND, bool DESC, typename U, bool REMOTE_ = false>
 struct RankDigit {
+  static constexpr bool REMOTE = REMOTE_;
   uint32_t cuts[BSORT_DIST_MAX_RANKS + 1];
   int nranks;
+  unsigned long long dst_base[REMOTE_ ? BSORT_DIST_MAX_RANKS : 1];
   __device__ __forceinline__ uint32_t operator()(U x) const {
     const uint32_t b = uint32_t(key_encode<KIND, DESC>(x) >> (sizeof(U) * 8 - 16));
     uint32_t lo = 0, hi = (uint32_t)nranks;  // largest q in [0,nranks) with cuts[q] <= b
@@ -779,7 +785,12 @@ __global__ void __launch_bounds__(THREADS, MINB)
         gofs[t] = jg0 - tile_excl;
         gofs[256 + t] = jg1 - (tile_excl + c0);
       } else {
-        gofs[t] = bases[t] + gbase - tile_excl;
+        if constexpr (DigitF::REMOTE)  // byte address of element 0 of this tile's run for t
+          gofs[t] = t < 256u && total ? digit.dst_base[t < (uint32_t)BSORT_DIST_MAX_RANKS ? t : 0] +
+                                            (gbase - tile_excl) * sizeof(U)
+                                      : 0ull;
+        else
+          gofs[t] = bases[t] + gbase - tile_excl;
       }
     }
     __syncthreads();  // (C)
@@ -795,7 +806,10 @@ __global__ void __launch_bounds__(THREADS, MINB)
           const uint32_t d = digit.digit_low(x, &lo);
           dst[gofs[d + (lo != low_first ? 256u : 0u)] + i] = x;
         } else {
-          dst[gofs[digit(x)] + i] = x;
+          if constexpr (DigitF::REMOTE)
+            reinterpret_cast<U*>(gofs[digit(x)])[i] = x;  // st.global to the owner's buffer
+          else
+            dst[gofs[digit(x)] + i] = x;
         }
       }
     }

@@ -24,9 +24,11 @@ bsort_status_t lsd_sort(const DtypeInfo& di, void* keys, uint64_t n, bool desc, 
 bsort_status_t dist_top_hist(const DtypeInfo& di, const void* keys, uint64_t n, bool desc,
                              uint64_t* dev_hist, cudaStream_t s);
 size_t dist_partition_workspace_bytes(int bytes, uint64_t n, int nranks);
+// dst_addrs == nullptr: bucketed copy into `out`; else (fused exchange) key of destination q
+// goes to the device byte address range starting at dst_addrs[q].
 bsort_status_t dist_partition(const DtypeInfo& di, const void* in, uint64_t n, bool desc,
                               const uint32_t* cuts, const uint64_t* send_counts, int nranks,
-                              void* out, void* ws,
+                              void* out, const uint64_t* dst_addrs, void* ws,
                               size_t ws_bytes, cudaStream_t s);
 
 }  // namespace bsort

@@ -17,11 +17,19 @@ The top bits of the transformed key are its most significant bits in the paper's
 rank r+1's and the concatenation over ranks is the global order.  Shard sizes are
 bin-granular (reading Q16).
 
+``fused=True`` (or env BSORT_FUSED_A2A=1) replaces a9 + a10 by the fused partition + exchange
+of §8 N1: every rank's receive buffer is torch symmetric memory, each rank learns where its
+keys start in every owner's buffer (one more tiny all-to-all), and ``partition_remote`` writes
+each key straight into the owner's buffer over NVLink (st.global to peer-mapped addresses) --
+no local bucketed copy, no NCCL keys all-to-all.  A barrier after the kernels precedes the
+local sort.
+
 ``ops`` lets the host-side orchestration run without a GPU (CPU/gloo tests substitute the
 three device steps); the product default is the CUDA path and nothing else.
 """
 from __future__ import annotations
 
+import os
 from dataclasses import dataclass
 from typing import Callable, Optional
 
@@ -52,15 +60,42 @@ class DistStats:
     recv_counts: np.ndarray
 
 
+_SYMM = {}  # (group name, dtype, device) -> (buffer, handle): receive buffers of the fused path
+
+
+def _symm_buffer(cap: int, dtype: torch.dtype, device, group):
+    """Symmetric-memory receive buffer of at least ``cap`` keys, shared across calls (grown
+    collectively when a call needs more; every rank passes the same all-reduced ``cap``)."""
+    import torch.distributed._symmetric_memory as symm_mem
+    pg = group if group is not None else dist.group.WORLD
+    key = (pg.group_name, dtype, str(device))
+    hit = _SYMM.get(key)
+    if hit is None or hit[0].numel() < cap:
+        buf = symm_mem.empty(max(cap, 1), dtype=dtype, device=device)
+        handle = symm_mem.rendezvous(buf, pg)
+        hit = (buf, handle)
+        _SYMM[key] = hit
+    return hit
+
+
+def fused_default() -> bool:
+    return os.environ.get("BSORT_FUSED_A2A", "0") == "1"
+
+
 def sort_dist(t: torch.Tensor, group=None, descending: bool = False,
               ops: Optional[DistOps] = None, return_stats: bool = False,
-              a2a_events: Optional[list] = None):
+              a2a_events: Optional[list] = None, fused: Optional[bool] = None):
     """Globally sort the keys held by all ranks of ``group``; returns this rank's shard.
 
     ``t`` (1-D, contiguous) may be clobbered.  The concatenation of the returned shards over
     ranks 0..P-1 is the sorted sequence of all keys, in the requested direction.
     ``a2a_events``: if a list is given (CUDA tensors only), a pair of timing events recorded
-    around the keys all-to-all on the current stream is appended to it."""
+    around the keys all-to-all on the current stream is appended to it.
+    ``fused``: partition straight into the owners' symmetric-memory buffers (§8 N1); the
+    returned shard is then a view of the group's receive buffer, valid until the next fused
+    ``sort_dist`` call on the same group, dtype and device."""
+    if fused is None:
+        fused = fused_default() and ops is None and t.is_cuda
     ops = ops or cuda_ops()
     P = dist.get_world_size(group)
     hl = ops.top_hist(t, descending)
@@ -74,6 +109,12 @@ def sort_dist(t: torch.Tensor, group=None, descending: bool = False,
     recv = torch.empty_like(send)
     dist.all_to_all_single(recv, send, group=group)
     rc = recv.cpu().numpy().astype(np.int64)
+    if fused:
+        out = _fused_exchange(t, cuts, sc, rc, descending, group, a2a_events)
+        ops.local_sort(out, descending)
+        if return_stats:
+            return out, DistStats(cuts=cuts, send_counts=sc, recv_counts=rc.astype(np.uint64))
+        return out
     bucketed = ops.partition(t, cuts, sc, descending)
     es = t.element_size()
     out = torch.empty(int(rc.sum()), dtype=t.dtype, device=t.device)
@@ -91,3 +132,34 @@ def sort_dist(t: torch.Tensor, group=None, descending: bool = False,
     if return_stats:
         return out, DistStats(cuts=cuts, send_counts=sc, recv_counts=rc.astype(np.uint64))
     return out
+
+
+def _fused_exchange(t, cuts, sc, rc, descending, group, a2a_events=None):
+    """§8 N1: partition every key straight into its owner's receive buffer (peer memory)."""
+    from . import partition_remote
+    P = dist.get_world_size(group)
+    es = t.element_size()
+    n_out = int(rc.sum())
+    # Owner q stores its sources in rank order: source r's keys start at sum_{r' < r} rc_q[r'].
+    starts = torch.from_numpy(np.concatenate([[0], np.cumsum(rc)[:-1]]).astype(np.int64)).to(t.device)
+    mine = torch.empty_like(starts)
+    dist.all_to_all_single(mine, starts, group=group)  # mine[q]: my first slot in q's buffer
+    cap = torch.tensor([n_out], dtype=torch.int64, device=t.device)
+    dist.all_reduce(cap, op=dist.ReduceOp.MAX, group=group)
+    buf, handle = _symm_buffer(int(cap.item()), t.dtype, t.device, group)
+    ptrs = handle.buffer_ptrs
+    mine_h = mine.cpu().numpy()
+    dst = np.array([int(ptrs[q]) + int(mine_h[q]) * es for q in range(P)], dtype=np.uint64)
+    ev = None
+    if a2a_events is not None:
+        ev = (torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+        ev[0].record()
+    dist.barrier(group=group)  # every owner finished reading its buffer from the previous call
+    partition_remote(t, cuts, sc, dst, descending)
+    torch.cuda.current_stream(t.device).synchronize()
+    dist.barrier(group=group)  # every rank's writes into my buffer have landed
+    if ev is not None:
+        ev[1].record()
+        me = dist.get_rank(group)
+        a2a_events.append((ev, int(sc.sum() - sc[me]) * es))
+    return buf[:n_out]

@@ -7,7 +7,10 @@
   slices; only the two collectives are stood in for by in-process tensor ops (there is one GPU
   in this pool, and ranks whose kernels wait on each other must not share a GPU).  The
   concatenated shards must equal the oracle's sort of all keys.
-* ``sort_dist`` end to end over a real one-rank NCCL process group.
+* ``sort_dist`` end to end over a real one-rank NCCL process group, with the NCCL keys
+  all-to-all and with the fused partition + exchange of §8 N1 (symmetric memory).
+* N1 on one GPU: every virtual rank's ``partition_remote`` writes straight into P owners'
+  receive buffers at the offsets the fused path computes (no overrun, exact shards).
 """
 import os
 import socket
@@ -150,5 +153,60 @@ def test_sort_dist_nccl_one_rank(B):
         out = B.sort_dist(x)
         torch.cuda.synchronize()
         assert host(out).tobytes() == ref.tobytes()
+    finally:
+        dist.destroy_process_group()
+
+
+def simulated_fused(B, parts, descending):
+    """§8 N1 on one GPU: each virtual rank's partition_remote writes its keys straight into the
+    P owners' receive buffers (here ordinary allocations on the same GPU; on a multi-GPU box the
+    same addresses are peer-mapped symmetric memory).  Offsets as _fused_exchange computes them."""
+    P = len(parts)
+    hl = [B.top_hist(p, descending) for p in parts]
+    hg_np = torch.stack([h.view(torch.int64) for h in hl]).sum(0).cpu().numpy().view(np.uint64)
+    cuts = B.splitters(hg_np, P)
+    send = np.stack([B.send_counts(h.view(torch.int64).cpu().numpy().view(np.uint64), cuts)
+                     for h in hl]).astype(np.int64)          # send[r][q]
+    recv_tot = send.sum(0)
+    bufs = [torch.full((int(recv_tot[q]) + 5,), -1, dtype=torch.int64 if parts[0].element_size() == 8
+                       else torch.int32, device="cuda").view(parts[0].dtype) for q in range(P)]
+    es = parts[0].element_size()
+    for r in range(P):
+        start = send[:r].sum(0)                               # r's first slot in each owner
+        dst = [bufs[q].data_ptr() + int(start[q]) * es for q in range(P)]
+        B.partition_remote(parts[r], cuts, send[r].astype(np.uint64), dst, descending)
+    torch.cuda.synchronize()
+    shards = []
+    for q in range(P):
+        tail = bufs[q][int(recv_tot[q]):]
+        assert bool((tail.view(torch.int64 if es == 8 else torch.int32) == -1).all())  # no overrun
+        shard = bufs[q][:int(recv_tot[q])].clone()
+        B.sort_(shard, descending)
+        shards.append(shard)
+    return shards
+
+
+@pytest.mark.parametrize("dtype,P,desc", [(torch.float64, 4, False), (torch.int32, 3, True),
+                                          (torch.float32, 8, False), (torch.uint64, 2, True)])
+def test_fused_partition_exchange_simulated(B, dtype, P, desc):
+    parts = [gen(dtype, 70_000 + 17 * r, 200 + r) for r in range(P)]
+    allkeys = np.concatenate([host(p) for p in parts])
+    shards = simulated_fused(B, parts, desc)
+    got = np.concatenate([host(s) for s in shards])
+    assert got.tobytes() == oracle.sort_native(allkeys, descending=desc).tobytes()
+
+
+def test_sort_dist_fused_nccl_one_rank(B):
+    """sort_dist(fused=True): symmetric-memory receive buffer, partition_remote, local sort."""
+    import torch.distributed as dist
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(_free_port()))
+    dist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device("cuda:0"))
+    try:
+        for seed in (1, 2):  # second call reuses the cached symmetric buffer
+            x = W.make("cfg5", "cuda", n=200_001 + seed, dtype=torch.float64)
+            ref = oracle.sort_native(host(x))
+            out = B.sort_dist(x, fused=True)
+            torch.cuda.synchronize()
+            assert host(out).tobytes() == ref.tobytes()
     finally:
         dist.destroy_process_group()
