@@ -29,14 +29,17 @@ fi
 CMD="python bench.py --steps 2 --warmup 3 --quick --no-cpu"
 if has launches; then
   timeout 600 $CMD > "$OUT/plain.log" 2>&1 &&
-  timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv \
+  timeout 900 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum \
+      --clock-control none --csv -k regex:"k_(count|onesweep|plan|copy|dist)" \
       --log-file "$OUT/launches.csv" $CMD > "$OUT/ncu_launches.log" 2>&1
   echo "ncu launches exit $?" >> "$OUT/status.txt"
 fi
 if has full; then
   PCMD="python tools/prof_sort.py --cfg cfg3 --reps 1"
   timeout 600 $PCMD > "$OUT/plain_prof.log" 2>&1 &&
-  timeout 1200 ncu --set full --clock-control none --import-source on -k regex:onesweep_pass -s 1 -c 1 \
+  # launch 4 of one cfg3 sort = pass 3, the stable (slowest) pass (0: pass 0, 1-2: the two
+  # pass-1 variants, 3: pass 2)
+  timeout 1200 ncu --set full --clock-control none --import-source on -k regex:onesweep_pass -s 4 -c 1 \
       -o "$OUT/pass" $PCMD > "$OUT/ncu_full.log" 2>&1
   echo "ncu full pass exit $?" >> "$OUT/status.txt"
 fi
