@@ -283,6 +283,22 @@ def bench_extra(B, dev, stream, args):
         x = W.make("cfg5", dev, n=1 << 30, dtype=dt)
         measure(f"cfg5_local_{nm}_2^30_1gpu", x, False, 136, reps=3)
         del x
+    # §8 N3: key-value sort (argsort payload: u32 values 0..n-1) of the cfg3 keys
+    x = W.make("cfg3", dev)
+    kw, vw = torch.empty_like(x), torch.empty(x.numel(), dtype=torch.int32, device=dev)
+    iota = torch.arange(x.numel(), dtype=torch.int32, device=dev)
+    restore = lambda: (kw.copy_(x), vw.copy_(iota))  # noqa: E731
+    run = lambda: B.sort_pairs_(kw, vw)  # noqa: E731
+    restore(); run(); torch.cuda.synchronize()  # noqa: E702
+    t = time_steps(run, restore, 3, stream)
+    ms = statistics.median(t)
+    hb, _ = load_peaks()
+    bpk = 4 + 4 * 2 * (4 + 4)  # histogram read + 4 passes of read+write of key and value
+    out["cfg3_f32_kv_argsort_2^30"] = {"keys_per_s": x.numel() / (ms / 1e3), "ms": ms,
+                                       "model_GBps": bpk * x.numel() / (ms / 1e3) / 1e9,
+                                       "model_bytes_per_key": bpk,
+                                       "frac_of_hbm": bpk * x.numel() / (ms / 1e3) / 1e9 / hb}
+    del x, kw, vw, iota
     torch.cuda.empty_cache()
     return out
 

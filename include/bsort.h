@@ -93,6 +93,20 @@ bsort_status_t bsort_sort_host(bsort_dtype_t dtype, void* host_keys, uint64_t n,
                                bsort_direction_t direction, void* dev_keys, void* workspace,
                                size_t workspace_bytes, void* stream);
 
+/* ----------------------------------------------------------- key-value sort
+ * Sort n keys of a 32/64-bit dtype (u32/i32/f32/u64/i64/f64; 8/16-bit keys return
+ * BSORT_ERROR_UNSUPPORTED_DTYPE) and move the n uint32 values at dev_values (device,
+ * 4-byte aligned) with them: afterwards value i is the one that was paired with key i.  Keys end
+ * up exactly as bsort_sort() leaves them; the order of the values of EQUAL keys is unspecified
+ * (the sort is not stable).  argsort: pass values 0..n-1.  The workspace holds an extra n
+ * uint32 ping-pong buffer.  Errors as bsort_sort(). */
+size_t bsort_pairs_workspace_bytes(bsort_dtype_t dtype, uint64_t n);
+bsort_status_t bsort_sort_pairs_ws(bsort_dtype_t dtype, void* dev_keys, uint32_t* dev_values, uint64_t n,
+                                   bsort_direction_t direction, void* workspace, size_t workspace_bytes,
+                                   void* stream);
+bsort_status_t bsort_sort_pairs(bsort_dtype_t dtype, void* dev_keys, uint32_t* dev_values, uint64_t n,
+                                bsort_direction_t direction, void* stream);
+
 /* ------------------------------------------------------ multi-GPU building blocks (MSD)
  * The distributed sort (BASELINE.json cfg5) is an MSD range partition on the top 16 bits of
  * the transformed key (the paper's sign -> exponent -> mantissa hierarchy, makes

@@ -23,7 +23,7 @@ import torch
 from . import _lib
 from ._lib import BsortError, check, lib
 
-__all__ = ["sort_", "sort", "Sorter", "sort_host", "sort_dist", "dtype_code", "workspace_bytes",
+__all__ = ["sort_", "sort", "sort_pairs_", "argsort", "Sorter", "sort_host", "sort_dist", "dtype_code", "workspace_bytes",
            "top_hist", "splitters", "send_counts", "partition", "partition_remote", "profile",
            "launch_count",
            "BsortError", "version"]
@@ -89,6 +89,32 @@ def sort_(t: torch.Tensor, descending: bool = False) -> torch.Tensor:
 
 def sort(t: torch.Tensor, descending: bool = False) -> torch.Tensor:
     return sort_(t.clone(), descending)
+
+
+def sort_pairs_(keys: torch.Tensor, values: torch.Tensor, descending: bool = False):
+    """Key-value sort in place (§8 N3): 32/64-bit keys, int32/uint32 values moved with them.
+    Not stable: the values of equal keys come out in unspecified order."""
+    _check_tensor(keys)
+    _check_tensor(values)
+    if values.dtype not in (torch.int32, torch.uint32) or values.numel() != keys.numel():
+        raise ValueError("sort_pairs_: values must be int32/uint32 with one value per key")
+    code = dtype_code(keys.dtype)
+    n = keys.numel()
+    if n <= 1:
+        return keys, values
+    wsb = int(lib.bsort_pairs_workspace_bytes(code, n))
+    ws = _workspace(wsb, keys.device)
+    check(lib.bsort_sort_pairs_ws(code, ctypes.c_void_p(keys.data_ptr()), ctypes.c_void_p(values.data_ptr()),
+                                  n, int(bool(descending)), ctypes.c_void_p(ws.data_ptr()), wsb,
+                                  _stream_ptr(keys.device)), "bsort_sort_pairs_ws")
+    return keys, values
+
+
+def argsort(t: torch.Tensor, descending: bool = False):
+    """(sorted keys, int32 indices into t) -- the paper's order, like torch.sort(stable=False)."""
+    keys = t.clone()
+    idx = torch.arange(t.numel(), dtype=torch.int32, device=t.device)
+    return sort_pairs_(keys, idx, descending)
 
 
 class Sorter:

@@ -110,7 +110,8 @@ bsort_status_t sort_ws_impl(const DtypeInfo& di, void* keys, uint64_t n, bsort_d
   if (n <= 1) return BSORT_SUCCESS;
   if (ws == nullptr || !aligned_to(ws, 256)) return BSORT_ERROR_INVALID_ARGUMENT;
   const bool desc = dir == BSORT_DESCENDING;
-  return di.bytes <= 2 ? counting_sort(di, keys, n, desc, ws, wsb, s) : lsd_sort(di, keys, n, desc, ws, wsb, s);
+  return di.bytes <= 2 ? counting_sort(di, keys, n, desc, ws, wsb, s)
+                       : lsd_sort(di, keys, nullptr, n, desc, ws, wsb, s);
 }
 
 }  // namespace
@@ -175,6 +176,55 @@ bsort_status_t bsort_sort_host(bsort_dtype_t dtype, void* host_keys, uint64_t n,
   BSORT_CUDA(cudaMemcpyAsync(host_keys, dev_keys, bytes, cudaMemcpyDeviceToHost, s));
   prof_end(PROF_D2H, s);
   return BSORT_SUCCESS;
+}
+
+// ----------------------------------------------------------------------- key-value (N3)
+
+size_t bsort_pairs_workspace_bytes(bsort_dtype_t dtype, uint64_t n) {
+  DtypeInfo di;
+  if (!dtype_info(dtype, &di) || di.bytes < 4 || n <= 1) return 0;
+  return lsd_workspace_bytes(di.bytes, n, true);
+}
+
+bsort_status_t bsort_sort_pairs_ws(bsort_dtype_t dtype, void* dev_keys, uint32_t* dev_values, uint64_t n,
+                                   bsort_direction_t direction, void* workspace, size_t workspace_bytes_,
+                                   void* stream) {
+  DtypeInfo di;
+  bsort_status_t st = validate(dtype, dev_keys, n, direction, &di);
+  if (st != BSORT_SUCCESS) return st;
+  if (di.bytes < 4) return BSORT_ERROR_UNSUPPORTED_DTYPE;
+  if (n > 0 && (dev_values == nullptr || !aligned_to(dev_values, 4))) return BSORT_ERROR_INVALID_ARGUMENT;
+  if (n <= 1) return BSORT_SUCCESS;
+  if (workspace == nullptr || !aligned_to(workspace, 256)) return BSORT_ERROR_INVALID_ARGUMENT;
+  if (workspace_bytes_ < lsd_workspace_bytes(di.bytes, n, true)) return BSORT_ERROR_WORKSPACE_TOO_SMALL;
+  return lsd_sort(di, dev_keys, dev_values, n, direction == BSORT_DESCENDING, workspace, workspace_bytes_,
+                  (cudaStream_t)stream);
+}
+
+bsort_status_t bsort_sort_pairs(bsort_dtype_t dtype, void* dev_keys, uint32_t* dev_values, uint64_t n,
+                                bsort_direction_t direction, void* stream) {
+  DtypeInfo di;
+  bsort_status_t st = validate(dtype, dev_keys, n, direction, &di);
+  if (st != BSORT_SUCCESS) return st;
+  if (di.bytes < 4) return BSORT_ERROR_UNSUPPORTED_DTYPE;
+  if (n > 0 && (dev_values == nullptr || !aligned_to(dev_values, 4))) return BSORT_ERROR_INVALID_ARGUMENT;
+  if (n <= 1) return BSORT_SUCCESS;
+  cudaStream_t s = (cudaStream_t)stream;
+  const size_t wsb = lsd_workspace_bytes(di.bytes, n, true);
+  void* ws = nullptr;
+  cudaError_t e = cudaMallocAsync(&ws, wsb, s);
+  if (e != cudaSuccess) {
+    set_last_cuda_error(e);
+    cudaGetLastError();
+    return BSORT_ERROR_OUT_OF_MEMORY;
+  }
+  st = lsd_sort(di, dev_keys, dev_values, n, direction == BSORT_DESCENDING, ws, wsb, s);
+  e = cudaFreeAsync(ws, s);
+  if (st == BSORT_SUCCESS && e != cudaSuccess) {
+    set_last_cuda_error(e);
+    return BSORT_ERROR_CUDA;
+  }
+  return st;
 }
 
 // ------------------------------------------------------------------------ distributed

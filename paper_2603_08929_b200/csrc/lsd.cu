@@ -17,18 +17,19 @@ namespace {
 // One 1024-thread CTA per SM shortens the look-back chains of a pure RUN2 pass (3.64 -> 3.38 ms)
 // but its 16384-key tiles break RUN2's two-run condition in pass 2 (runs of ~16K keys at
 // n = 2^30) and 8 keys per thread lose too much ILP (profiles/r1: cfg3 16.1 vs 16.6 / 19.7 ms).
-template <typename U, int MODE> struct PassCfg;
-template <int MODE> struct PassCfg<uint32_t, MODE> {
-  static constexpr int THREADS = 512, ITEMS = 16, MINB = 2, LBG = 8;
+// Key-value sorts (KV) carry ITEMS more registers and a second tile buffer pair: one CTA per SM.
+template <typename U, int MODE, bool KV = false> struct PassCfg;
+template <int MODE, bool KV> struct PassCfg<uint32_t, MODE, KV> {
+  static constexpr int THREADS = 512, ITEMS = 16, MINB = KV ? 1 : 2, LBG = 8;
 };
-template <int MODE> struct PassCfg<unsigned long long, MODE> {
-  static constexpr int THREADS = 384, ITEMS = 12, MINB = 2, LBG = 8;
+template <int MODE, bool KV> struct PassCfg<unsigned long long, MODE, KV> {
+  static constexpr int THREADS = 384, ITEMS = 12, MINB = KV ? 1 : 2, LBG = 8;
 };
 
 template <typename U> constexpr int hist_lanes() { return sizeof(U) == 4 ? 32 : 16; }
 
 struct LsdLayout {
-  size_t scratch, ghist, bases, gcount, joint, seg, plan, counters, lookback, total;
+  size_t scratch, vscratch, ghist, bases, gcount, joint, seg, plan, counters, lookback, total;
 };
 
 // Pass 1 may run look-back-free (RANK_J01) from the joint histogram of digits 0 and 1; below
@@ -37,7 +38,7 @@ struct LsdLayout {
 constexpr uint64_t JOINT_MIN_N = 1ull << 24;
 
 template <typename U>
-LsdLayout lsd_layout(uint64_t n) {
+LsdLayout lsd_layout(uint64_t n, bool kv = false) {
   using C = PassCfg<U, RANK_RUN2>;  // the look-back passes size the descriptor array
   constexpr uint64_t TILE = (uint64_t)C::THREADS * C::ITEMS;
   constexpr int P = sizeof(U);
@@ -46,6 +47,7 @@ LsdLayout lsd_layout(uint64_t n) {
   LsdLayout l;
   size_t off = 0;
   l.scratch = off;  off = align_up(off + n * sizeof(U), 256);
+  l.vscratch = off; off = align_up(off + (kv ? n * sizeof(uint32_t) : 0), 256);
   l.ghist = off;    off = align_up(off + P * 256 * 8, 256);
   l.bases = off;    off = align_up(off + P * 256 * 8, 256);
   l.gcount = off;   off = align_up(off + P * 256 * 8, 256);
@@ -59,13 +61,13 @@ LsdLayout lsd_layout(uint64_t n) {
   return l;
 }
 
-template <typename U, bool BULK, int RANK, typename DescT, typename DigitF>
+template <typename U, bool BULK, int RANK, bool KV, typename DescT, typename DigitF>
 bsort_status_t launch_pass_t(const U* a, U* b, uint64_t n, DigitF digit, const unsigned long long* bases,
                              DescT* lookback, unsigned long long* gcount, uint32_t* counter, const PassPlan* plan,
-                             int pass, cudaStream_t s) {
-  using C = PassCfg<U, RANK>;
-  using L = PassSmem<C::THREADS, C::ITEMS, U, RANK>;
-  auto kern = k_onesweep_pass<U, C::THREADS, C::ITEMS, C::MINB, BULK, DescT, DigitF, RANK, C::LBG>;
+                             int pass, KvPtrs kvp, cudaStream_t s) {
+  using C = PassCfg<U, RANK, KV>;
+  using L = PassSmem<C::THREADS, C::ITEMS, U, RANK, KV>;
+  auto kern = k_onesweep_pass<U, C::THREADS, C::ITEMS, C::MINB, BULK, DescT, DigitF, RANK, C::LBG, KV>;
   static int occ = 0;  // per instantiation; benign race (idempotent)
   if (occ == 0) {
     BSORT_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L::bytes));
@@ -78,20 +80,23 @@ bsort_status_t launch_pass_t(const U* a, U* b, uint64_t n, DigitF digit, const u
   const uint64_t grid = min64(tiles, (uint64_t)num_sms() * occ);
   BSORT_LAUNCH(PROF_PASS, s,
                kern<<<(unsigned)grid, C::THREADS, L::bytes, s>>>(a, b, n, digit, bases, lookback, gcount, counter,
-                                                                 (uint32_t)tiles, plan, pass));
+                                                                 (uint32_t)tiles, plan, pass, kvp));
   return BSORT_SUCCESS;
 }
 
 // TMA bulk prefetch needs 16-byte aligned sources: both ping-pong buffers (the scratch buffer
 // always is; the caller's array may be only element-aligned).
-template <typename U, int RANK, typename DescT, typename DigitF>
+template <typename U, int RANK, typename DescT, bool KV = false, typename DigitF>
 bsort_status_t launch_pass(const U* a, U* b, uint64_t n, DigitF digit, const unsigned long long* bases,
                            DescT* lookback, unsigned long long* gcount, uint32_t* counter, const PassPlan* plan,
-                           int pass, cudaStream_t s) {
-  const bool aligned = ((uintptr_t)a % 16 == 0) && (plan == nullptr || (uintptr_t)b % 16 == 0);
+                           int pass, cudaStream_t s, KvPtrs kvp = {}) {
+  bool aligned = ((uintptr_t)a % 16 == 0) && (plan == nullptr || (uintptr_t)b % 16 == 0);
+  if (KV) aligned = aligned && (uintptr_t)kvp.va % 16 == 0 && (uintptr_t)kvp.vb % 16 == 0;
   if (aligned)
-    return launch_pass_t<U, true, RANK, DescT>(a, b, n, digit, bases, lookback, gcount, counter, plan, pass, s);
-  return launch_pass_t<U, false, RANK, DescT>(a, b, n, digit, bases, lookback, gcount, counter, plan, pass, s);
+    return launch_pass_t<U, true, RANK, KV, DescT>(a, b, n, digit, bases, lookback, gcount, counter, plan, pass, kvp,
+                                                   s);
+  return launch_pass_t<U, false, RANK, KV, DescT>(a, b, n, digit, bases, lookback, gcount, counter, plan, pass, kvp,
+                                                  s);
 }
 
 bsort_status_t memset_async(void* p, size_t bytes, cudaStream_t s) {
@@ -99,14 +104,15 @@ bsort_status_t memset_async(void* p, size_t bytes, cudaStream_t s) {
   return BSORT_SUCCESS;
 }
 
-template <int KIND, bool DESC, typename U, typename DescT>
-bsort_status_t lsd_run(U* keys, uint64_t n, unsigned char* ws, cudaStream_t s) {
+template <int KIND, bool DESC, typename U, typename DescT, bool KV>
+bsort_status_t lsd_run(U* keys, uint32_t* vals, uint64_t n, unsigned char* ws, cudaStream_t s) {
   using C = PassCfg<U, RANK_RUN2>;
   constexpr int P = sizeof(U);
   constexpr int LANES = hist_lanes<U>();
   constexpr uint64_t TILE = (uint64_t)C::THREADS * C::ITEMS;
-  const LsdLayout l = lsd_layout<U>(n);
+  const LsdLayout l = lsd_layout<U>(n, KV);
   U* scratch = reinterpret_cast<U*>(ws + l.scratch);
+  const KvPtrs kvp{vals, reinterpret_cast<uint32_t*>(ws + l.vscratch)};
   auto* ghist = reinterpret_cast<unsigned long long*>(ws + l.ghist);
   auto* bases = reinterpret_cast<unsigned long long*>(ws + l.bases);
   auto* gcount = reinterpret_cast<unsigned long long*>(ws + l.gcount);
@@ -157,18 +163,18 @@ bsort_status_t lsd_run(U* keys, uint64_t n, unsigned char* ws, cudaStream_t s) {
     // The first LSD pass may order equal digits arbitrarily (the input order carries no
     // information); every later pass must be stable.
     if constexpr (p == 0)
-      st = launch_pass<U, RANK_UNSTABLE, DescT>(keys, scratch, n, RadixDigit<KIND, DESC, U, SH>{}, bases, lookback,
-                                                gcount, counters, plan, p, s);
+      st = launch_pass<U, RANK_UNSTABLE, DescT, KV>(keys, scratch, n, RadixDigit<KIND, DESC, U, SH>{}, bases,
+                                                    lookback, gcount, counters, plan, p, s, kvp);
     else
-      st = launch_pass<U, RANK_RUN2, DescT>(keys, scratch, n, RadixDigit<KIND, DESC, U, SH>{},
-                                                 bases + p * 256, lookback, gcount + p * 256, counters + p,
-                                                 plan, p, s);
+      st = launch_pass<U, RANK_RUN2, DescT, KV>(keys, scratch, n, RadixDigit<KIND, DESC, U, SH>{},
+                                                bases + p * 256, lookback, gcount + p * 256, counters + p,
+                                                plan, p, s, kvp);
     // pass 1 without look-back when the joint plan allows it (each launch checks plan->j01
     // and exactly one of the two does the work)
     if constexpr (p == 1)
       if (st == BSORT_SUCCESS && use_joint)
-        st = launch_pass<U, RANK_J01, DescT>(keys, scratch, n, RadixDigit<KIND, DESC, U, SH>{}, bases + 256,
-                                             lookback, seg, counters + 8, plan, p, s);
+        st = launch_pass<U, RANK_J01, DescT, KV>(keys, scratch, n, RadixDigit<KIND, DESC, U, SH>{}, bases + 256,
+                                                 lookback, seg, counters + 8, plan, p, s, kvp);
   };
   one_pass(std::integral_constant<int, 0>{});
   one_pass(std::integral_constant<int, 8>{});
@@ -183,40 +189,47 @@ bsort_status_t lsd_run(U* keys, uint64_t n, unsigned char* ws, cudaStream_t s) {
   if (st != BSORT_SUCCESS) return st;
   const int cgrid = (int)min64((n + 255) / 256, (uint64_t)num_sms() * 16);
   BSORT_LAUNCH(PROF_COPY, s, k_copy_back<U><<<cgrid, 256, 0, s>>>(keys, scratch, n, plan));
+  if constexpr (KV)
+    BSORT_LAUNCH(PROF_COPY, s, k_copy_back<uint32_t><<<cgrid, 256, 0, s>>>(vals, kvp.vb, n, plan));
   return BSORT_SUCCESS;
 }
 
 template <int KIND, bool DESC, typename U>
-bsort_status_t lsd_dispatch_desc(U* keys, uint64_t n, unsigned char* ws, cudaStream_t s) {
-  if (n <= (1ull << 30)) return lsd_run<KIND, DESC, U, uint32_t>(keys, n, ws, s);
-  return lsd_run<KIND, DESC, U, unsigned long long>(keys, n, ws, s);
+bsort_status_t lsd_dispatch_desc(U* keys, uint32_t* vals, uint64_t n, unsigned char* ws, cudaStream_t s) {
+  if (vals != nullptr) {
+    if (n <= (1ull << 30)) return lsd_run<KIND, DESC, U, uint32_t, true>(keys, vals, n, ws, s);
+    return lsd_run<KIND, DESC, U, unsigned long long, true>(keys, vals, n, ws, s);
+  }
+  if (n <= (1ull << 30)) return lsd_run<KIND, DESC, U, uint32_t, false>(keys, nullptr, n, ws, s);
+  return lsd_run<KIND, DESC, U, unsigned long long, false>(keys, nullptr, n, ws, s);
 }
 
 template <typename U>
-bsort_status_t lsd_dispatch(int kind, bool desc, U* keys, uint64_t n, unsigned char* ws, cudaStream_t s) {
+bsort_status_t lsd_dispatch(int kind, bool desc, U* keys, uint32_t* vals, uint64_t n, unsigned char* ws,
+                            cudaStream_t s) {
   switch (kind) {
     case KIND_U:
-      return desc ? lsd_dispatch_desc<KIND_U, true>(keys, n, ws, s) : lsd_dispatch_desc<KIND_U, false>(keys, n, ws, s);
+      return desc ? lsd_dispatch_desc<KIND_U, true>(keys, vals, n, ws, s) : lsd_dispatch_desc<KIND_U, false>(keys, vals, n, ws, s);
     case KIND_I:
-      return desc ? lsd_dispatch_desc<KIND_I, true>(keys, n, ws, s) : lsd_dispatch_desc<KIND_I, false>(keys, n, ws, s);
+      return desc ? lsd_dispatch_desc<KIND_I, true>(keys, vals, n, ws, s) : lsd_dispatch_desc<KIND_I, false>(keys, vals, n, ws, s);
     default:
-      return desc ? lsd_dispatch_desc<KIND_F, true>(keys, n, ws, s) : lsd_dispatch_desc<KIND_F, false>(keys, n, ws, s);
+      return desc ? lsd_dispatch_desc<KIND_F, true>(keys, vals, n, ws, s) : lsd_dispatch_desc<KIND_F, false>(keys, vals, n, ws, s);
   }
 }
 
 }  // namespace
 
-size_t lsd_workspace_bytes(int bytes, uint64_t n) {
+size_t lsd_workspace_bytes(int bytes, uint64_t n, bool kv) {
   if (n <= 1) return 0;
-  return bytes == 4 ? lsd_layout<uint32_t>(n).total : lsd_layout<unsigned long long>(n).total;
+  return bytes == 4 ? lsd_layout<uint32_t>(n, kv).total : lsd_layout<unsigned long long>(n, kv).total;
 }
 
-bsort_status_t lsd_sort(const DtypeInfo& di, void* keys, uint64_t n, bool desc, void* ws, size_t ws_bytes,
-                        cudaStream_t s) {
-  if (ws_bytes < lsd_workspace_bytes(di.bytes, n)) return BSORT_ERROR_WORKSPACE_TOO_SMALL;
+bsort_status_t lsd_sort(const DtypeInfo& di, void* keys, uint32_t* vals, uint64_t n, bool desc, void* ws,
+                        size_t ws_bytes, cudaStream_t s) {
+  if (ws_bytes < lsd_workspace_bytes(di.bytes, n, vals != nullptr)) return BSORT_ERROR_WORKSPACE_TOO_SMALL;
   auto* w = static_cast<unsigned char*>(ws);
-  if (di.bytes == 4) return lsd_dispatch<uint32_t>(di.kind, desc, static_cast<uint32_t*>(keys), n, w, s);
-  return lsd_dispatch<unsigned long long>(di.kind, desc, static_cast<unsigned long long*>(keys), n, w, s);
+  if (di.bytes == 4) return lsd_dispatch<uint32_t>(di.kind, desc, static_cast<uint32_t*>(keys), vals, n, w, s);
+  return lsd_dispatch<unsigned long long>(di.kind, desc, static_cast<unsigned long long*>(keys), vals, n, w, s);
 }
 
 // ---------------------------------------------------------------- MSD partition (a7, a9)

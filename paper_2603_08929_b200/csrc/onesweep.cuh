@@ -437,7 +437,7 @@ enum RankMode : int { RANK_STABLE = 0, RANK_UNSTABLE = 1, RANK_RUN2 = 2, RANK_J0
 // serialization is at most 32/BREP-way (skewed digits, runs of equal keys).
 constexpr int BREP = 4;  // the offset code below reads one uint4 per bin
 
-template <int THREADS, int ITEMS, typename U, int MODE>
+template <int THREADS, int ITEMS, typename U, int MODE, bool KV = false>
 struct PassSmem {
   static constexpr int WARPS = THREADS / 32;
   static constexpr int TILE = THREADS * ITEMS;
@@ -452,7 +452,14 @@ struct PassSmem {
   static constexpr size_t wt_off = align_up(gofs_off + sizeof(unsigned long long) * 512, 16);
   static constexpr size_t mbar_off = align_up(wt_off + sizeof(uint32_t) * (WARPS + 1), 16);
   static constexpr size_t tile_off = mbar_off + 16;  // uint32 tile id held by each buffer
-  static constexpr size_t bytes = align_up(tile_off + 16, 128);
+  static constexpr size_t vbuf_off = align_up(tile_off + 16, 128);  // KV: uint32 values [2][TILE]
+  static constexpr size_t bytes = align_up(vbuf_off + (KV ? 2 * sizeof(uint32_t) * TILE : 0), 128);
+};
+
+// Payload of a key-value sort (§8 N3): 32-bit values ping-ponged like the keys.
+struct KvPtrs {
+  const uint32_t* va;
+  uint32_t* vb;
 };
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -473,12 +480,9 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
         : "memory");
   } while (!done);
 }
-// One thread: arm `bar` for `bytes` and start a 1-D bulk copy global -> shared (bytes % 16 == 0,
-// both addresses 16-byte aligned).  bytes == 0 just arrives (phase completes at once).
-__device__ __forceinline__ void bulk_load(void* dst_smem, const void* src, uint32_t bytes, uint64_t* bar) {
-  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
-               : "memory");
+// One thread: arm `bar` for `bytes` (+ `bytes2`) and start 1-D bulk copies global -> shared
+// (sizes % 16 == 0, addresses 16-byte aligned).  Zero bytes just arrive.
+__device__ __forceinline__ void bulk_copy(void* dst_smem, const void* src, uint32_t bytes, uint64_t* bar) {
   if (bytes)
     asm volatile(
         "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
@@ -486,15 +490,23 @@ __device__ __forceinline__ void bulk_load(void* dst_smem, const void* src, uint3
         "l"(src), "r"(bytes), "r"(smem_u32(bar))
         : "memory");
 }
+__device__ __forceinline__ void bulk_load(void* dst_smem, const void* src, uint32_t bytes, uint64_t* bar,
+                                          void* dst2 = nullptr, const void* src2 = nullptr, uint32_t bytes2 = 0) {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes + bytes2)
+               : "memory");
+  bulk_copy(dst_smem, src, bytes, bar);
+  bulk_copy(dst2, src2, bytes2, bar);
+}
 
 template <typename U, int THREADS, int ITEMS, int MINB, bool BULK, typename DescT, typename DigitF, int MODE,
-          int LBG = 8>
+          int LBG = 8, bool KV = false>
 __global__ void __launch_bounds__(THREADS, MINB)
     k_onesweep_pass(const U* a_ptr, U* b_ptr, uint64_t n, DigitF digit,
                     const unsigned long long* __restrict__ bases, DescT* __restrict__ lookback,
                     unsigned long long* __restrict__ gcount, uint32_t* __restrict__ tile_counter,
-                    uint32_t num_tiles, const PassPlan* __restrict__ plan, int pass) {
-  using L = PassSmem<THREADS, ITEMS, U, MODE>;
+                    uint32_t num_tiles, const PassPlan* __restrict__ plan, int pass, KvPtrs kvp = {}) {
+  using L = PassSmem<THREADS, ITEMS, U, MODE, KV>;
   using LB = LookbackBits<DescT>;
   constexpr int TILE = L::TILE;
   constexpr int WARPS = L::WARPS;
@@ -515,6 +527,10 @@ __global__ void __launch_bounds__(THREADS, MINB)
 
   const U* src = a_ptr;
   U* dst = b_ptr;
+  uint32_t* vbufs = reinterpret_cast<uint32_t*>(smem + L::vbuf_off);
+  const uint32_t* vsrc = kvp.va;
+  uint32_t* vdst = kvp.vb;
+  (void)vbufs;
   if (plan != nullptr) {
     if (plan->skip[pass]) return;
     if constexpr (MODE == RANK_J01) {
@@ -525,6 +541,8 @@ __global__ void __launch_bounds__(THREADS, MINB)
     if (plan->src_alt[pass]) {
       src = b_ptr;
       dst = const_cast<U*>(a_ptr);
+      vsrc = kvp.vb;
+      vdst = const_cast<uint32_t*>(kvp.va);
     }
   }
   const uint32_t lane = threadIdx.x & 31;
@@ -547,6 +565,16 @@ __global__ void __launch_bounds__(THREADS, MINB)
   auto bulk_keys = [&](uint32_t valid) -> uint32_t {
     return (uint32_t)((valid * sizeof(U)) & ~(size_t)15) / (uint32_t)sizeof(U);
   };
+  auto bulk_vals = [&](uint32_t valid) -> uint32_t { return valid & ~3u; };
+  // arm buffer b's barrier and copy tile `id` (keys, and values for KV) into it
+  auto issue = [&](int b, uint32_t id) {
+    const uint32_t v = tile_valid(id);
+    if constexpr (KV)
+      bulk_load(bufs + b * TILE, src + (uint64_t)id * TILE, bulk_keys(v) * (uint32_t)sizeof(U), &mbar[b],
+                vbufs + b * TILE, vsrc + (uint64_t)id * TILE, bulk_vals(v) * 4u);
+    else
+      bulk_load(bufs + b * TILE, src + (uint64_t)id * TILE, bulk_keys(v) * (uint32_t)sizeof(U), &mbar[b]);
+  };
 
   uint32_t phase0 = 0, phase1 = 0;
   if constexpr (BULK) {
@@ -557,10 +585,7 @@ __global__ void __launch_bounds__(THREADS, MINB)
       for (int b = 0; b < 2; ++b) {
         const uint32_t id = atomicAdd(tile_counter, 1u);
         tile_s[b] = id;
-        if (id < num_tiles) {
-          const uint32_t v = tile_valid(id);
-          bulk_load(bufs + b * TILE, src + (uint64_t)id * TILE, bulk_keys(v) * (uint32_t)sizeof(U), &mbar[b]);
-        }
+        if (id < num_tiles) issue(b, id);
       }
     }
     __syncthreads();
@@ -602,6 +627,10 @@ __global__ void __launch_bounds__(THREADS, MINB)
     constexpr uint32_t IS = HALF_MAP ? 16u : 32u;  // index stride between items
     const uint32_t seg = HALF_MAP ? warp * SEG + half * (16 * ITEMS) + l16 : warp * SEG + lane;
     U keys[ITEMS];
+    uint32_t vals[KV ? ITEMS : 1];
+    uint32_t* vbuf = vbufs + cur * TILE;
+    (void)vals;
+    (void)vbuf;
     U first_key = U(0), last_key = U(0);
     if constexpr (BULK) {
       mbar_wait(&mbar[cur], cur ? phase1 : phase0);
@@ -609,6 +638,10 @@ __global__ void __launch_bounds__(THREADS, MINB)
       if (full) {
 #pragma unroll
         for (int k = 0; k < ITEMS; ++k) keys[k] = buf[seg + IS * k];
+        if constexpr (KV) {
+#pragma unroll
+          for (int k = 0; k < ITEMS; ++k) vals[k] = vbuf[seg + IS * k];
+        }
         if constexpr (RUNS) {
           first_key = buf[0];
           last_key = buf[TILE - 1];
@@ -619,6 +652,14 @@ __global__ void __launch_bounds__(THREADS, MINB)
         for (int k = 0; k < ITEMS; ++k) {
           const uint32_t i = seg + IS * k;
           keys[k] = i < bk ? buf[i] : (i < valid ? ldg_nc(src + tile_base + i) : U(0));
+        }
+        if constexpr (KV) {
+          const uint32_t bv = bulk_vals(valid);
+#pragma unroll
+          for (int k = 0; k < ITEMS; ++k) {
+            const uint32_t i = seg + IS * k;
+            vals[k] = i < bv ? vbuf[i] : (i < valid ? ldg_nc(vsrc + tile_base + i) : 0u);
+          }
         }
         if constexpr (RUNS) {
           first_key = bk > 0 ? buf[0] : ldg_nc(src + tile_base);
@@ -633,6 +674,11 @@ __global__ void __launch_bounds__(THREADS, MINB)
 #pragma unroll
         for (int k = 0; k < ITEMS; ++k)
           keys[k] = (seg + IS * k < valid) ? ldg_nc(src + tile_base + seg + IS * k) : U(0);
+      }
+      if constexpr (KV) {
+#pragma unroll
+        for (int k = 0; k < ITEMS; ++k)
+          vals[k] = (full || seg + IS * k < valid) ? ldg_nc(vsrc + tile_base + seg + IS * k) : 0u;
       }
       if constexpr (RUNS) {
         first_key = ldg_nc(src + tile_base);
@@ -766,10 +812,18 @@ __global__ void __launch_bounds__(THREADS, MINB)
     if (unstable_rank) {
 #pragma unroll
       for (int k = 0; k < ITEMS; ++k)
-        if (info[k] != 0xFFFFFFFFu) buf[bcnt[(info[k] & 0x1FFu) * BREP + (lane & (BREP - 1))] + (info[k] >> 9)] = keys[k];
+        if (info[k] != 0xFFFFFFFFu) {
+          const uint32_t pos = bcnt[(info[k] & 0x1FFu) * BREP + (lane & (BREP - 1))] + (info[k] >> 9);
+          buf[pos] = keys[k];
+          if constexpr (KV) vbuf[pos] = vals[k];
+        }
     } else {
 #pragma unroll
-      for (int k = 0; k < ITEMS; ++k) buf[wc[info[k] & 0xFFu] + (info[k] >> 9)] = keys[k];
+      for (int k = 0; k < ITEMS; ++k) {
+        const uint32_t pos = wc[info[k] & 0xFFu] + (info[k] >> 9);
+        buf[pos] = keys[k];
+        if constexpr (KV) vbuf[pos] = vals[k];
+      }
     }
 
     // 4. global digit offsets
@@ -801,15 +855,19 @@ __global__ void __launch_bounds__(THREADS, MINB)
       const uint32_t i = t + k * THREADS;
       if (full || i < valid) {
         const U x = buf[i];
-        if constexpr (MODE == RANK_J01) {
-          U lo;
-          const uint32_t d = digit.digit_low(x, &lo);
-          dst[gofs[d + (lo != low_first ? 256u : 0u)] + i] = x;
+        if constexpr (DigitF::REMOTE) {
+          reinterpret_cast<U*>(gofs[digit(x)])[i] = x;  // st.global to the owner's buffer
         } else {
-          if constexpr (DigitF::REMOTE)
-            reinterpret_cast<U*>(gofs[digit(x)])[i] = x;  // st.global to the owner's buffer
-          else
-            dst[gofs[digit(x)] + i] = x;
+          unsigned long long o;
+          if constexpr (MODE == RANK_J01) {
+            U lo;
+            const uint32_t d = digit.digit_low(x, &lo);
+            o = gofs[d + (lo != low_first ? 256u : 0u)] + i;
+          } else {
+            o = gofs[digit(x)] + i;
+          }
+          dst[o] = x;
+          if constexpr (KV) vdst[o] = vbuf[i];
         }
       }
     }
@@ -817,10 +875,7 @@ __global__ void __launch_bounds__(THREADS, MINB)
       __syncthreads();  // (D) buffer `cur` fully read: refill it with the tile after next
       if (t == 0) {
         tile_s[cur] = next_id;
-        if (next_id < num_tiles) {
-          const uint32_t v = tile_valid(next_id);
-          bulk_load(buf, src + (uint64_t)next_id * TILE, bulk_keys(v) * (uint32_t)sizeof(U), &mbar[cur]);
-        }
+        if (next_id < num_tiles) issue((int)cur, next_id);
       }
     }
   }

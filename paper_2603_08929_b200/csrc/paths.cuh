@@ -16,8 +16,9 @@ bsort_status_t counting_sort(const DtypeInfo& di, void* keys, uint64_t n, bool d
                              size_t ws_bytes, cudaStream_t s);
 
 // a3-a5: 32/64-bit one-sweep LSD path.
-size_t lsd_workspace_bytes(int bytes, uint64_t n);
-bsort_status_t lsd_sort(const DtypeInfo& di, void* keys, uint64_t n, bool desc, void* ws,
+// vals (nullable): 32-bit payload sorted along with the keys (key-value sort, §8 N3).
+size_t lsd_workspace_bytes(int bytes, uint64_t n, bool kv = false);
+bsort_status_t lsd_sort(const DtypeInfo& di, void* keys, uint32_t* vals, uint64_t n, bool desc, void* ws,
                         size_t ws_bytes, cudaStream_t s);
 
 // a7/a9: distributed building blocks.

@@ -242,3 +242,44 @@ def test_half_floats(B, dtype, descending):
         torch.cuda.synchronize()
         got = x.view(torch.int16).cpu().numpy().view(np.uint16)
         assert got.tobytes() == ref.tobytes(), f"{dtype} n={n}"
+
+
+def check_pairs(B, x, descending, what=""):
+    """Key-value sort (§8 N3) with values 0..n-1 (argsort): keys bit-exact vs the oracle; the
+    values a permutation; every value points at an input key with the same bits as the output
+    key beside it (equal keys may carry their values in any order)."""
+    n = x.numel()
+    ref = oracle.sort_native(host(x), descending=descending)
+    keys, idx = B.argsort(x, descending)
+    torch.cuda.synchronize()
+    assert host(keys).tobytes() == ref.tobytes(), f"{what}: keys"
+    ii = idx.to(torch.int64)
+    assert bool((torch.sort(ii).values == torch.arange(n, device=ii.device)).all()), f"{what}: not a permutation"
+    ib = {4: torch.int32, 8: torch.int64}[x.element_size()]
+    assert torch.equal(x.view(ib)[ii], keys.view(ib)), f"{what}: value does not follow its key"
+
+
+@pytest.mark.parametrize("dtype", [torch.float32, torch.int32, torch.uint32, torch.float64, torch.int64,
+                                   torch.uint64], ids=lambda d: str(d).split(".")[-1])
+def test_key_value_sort(B, dtype):
+    for n in (0, 1, 2, 1000, 8191, 8193, 65537, (1 << 20) + 7):
+        check_pairs(B, gen(dtype, n, 900 + n), n % 2 == 1, f"{dtype} n={n}")
+    x = sview(gen(dtype, 1, 5)).repeat(50_000).view(dtype)   # all equal: any permutation is fine
+    check_pairs(B, x, False, "all equal")
+
+
+@pytest.mark.parametrize("dtype", [torch.float32, torch.float64])
+def test_key_value_large_and_misaligned(B, dtype):
+    """n >= 2^24 (joint histogram, J01 pass 1) and a keys pointer that is not 16-byte aligned."""
+    n = (1 << 24) + 99
+    check_pairs(B, gen(dtype, n, 77), False, "large")
+    base = gen(dtype, 300_003, 78)
+    check_pairs(B, base[1:300_001], True, "misaligned")
+
+
+def test_key_value_rejects_small_keys(B):
+    from paper_2603_08929_b200 import BsortError
+    k = torch.zeros(100, dtype=torch.int16, device="cuda")
+    v = torch.zeros(100, dtype=torch.int32, device="cuda")
+    with pytest.raises(BsortError):
+        B.sort_pairs_(k, v)

@@ -148,18 +148,18 @@ void suite(uint64_t n) {
   // One pass on uniform keys with digit shift 0: RUN2 sees a single run (the fast path).
   if constexpr (sizeof(U) == 4) {
     run<U, 512, 16, 2, true, RANK_STABLE, 8>(in, out, n, bases, lookback, counter, gcount, ref, dbg);
+    run<U, 256, 16, 4, true, RANK_STABLE, 8>(in, out, n, bases, lookback, counter, gcount, ref, dbg);
+    run<U, 384, 16, 3, true, RANK_STABLE, 8>(in, out, n, bases, lookback, counter, gcount, ref, dbg);
+    run<U, 256, 24, 3, true, RANK_STABLE, 8>(in, out, n, bases, lookback, counter, gcount, ref, dbg);
     run<U, 512, 16, 2, true, RANK_RUN2, 8>(in, out, n, bases, lookback, counter, gcount, ref, dbg);
-    run<U, 512, 16, 2, true, RANK_RUN2, 16>(in, out, n, bases, lookback, counter, gcount, ref, dbg);
-    run<U, 512, 16, 2, true, RANK_RUN2, 32>(in, out, n, bases, lookback, counter, gcount, ref, dbg);
-    run<U, 1024, 16, 1, true, RANK_RUN2, 8>(in, out, n, bases, lookback, counter, gcount, ref, dbg);
-    run<U, 1024, 16, 1, true, RANK_RUN2, 16>(in, out, n, bases, lookback, counter, gcount, ref, dbg);
-    run<U, 1024, 16, 1, true, RANK_STABLE, 16>(in, out, n, bases, lookback, counter, gcount, ref, dbg);
+    run<U, 256, 16, 4, true, RANK_RUN2, 8>(in, out, n, bases, lookback, counter, gcount, ref, dbg);
+    run<U, 384, 16, 3, true, RANK_RUN2, 8>(in, out, n, bases, lookback, counter, gcount, ref, dbg);
     run<U, 512, 16, 2, true, RANK_UNSTABLE, 8>(in, out, n, bases, lookback, counter, gcount, ref, dbg);
+    run<U, 256, 16, 4, true, RANK_UNSTABLE, 8>(in, out, n, bases, lookback, counter, gcount, ref, dbg);
   } else {
     run<U, 384, 12, 2, true, RANK_STABLE, 8>(in, out, n, bases, lookback, counter, gcount, ref, dbg);
+    run<U, 256, 12, 3, true, RANK_STABLE, 8>(in, out, n, bases, lookback, counter, gcount, ref, dbg);
     run<U, 384, 12, 2, true, RANK_RUN2, 8>(in, out, n, bases, lookback, counter, gcount, ref, dbg);
-    run<U, 384, 12, 2, true, RANK_RUN2, 16>(in, out, n, bases, lookback, counter, gcount, ref, dbg);
-    run<U, 768, 12, 1, true, RANK_RUN2, 16>(in, out, n, bases, lookback, counter, gcount, ref, dbg);
     run<U, 384, 12, 2, true, RANK_UNSTABLE, 8>(in, out, n, bases, lookback, counter, gcount, ref, dbg);
   }
   cudaFree(in);
