@@ -1,379 +1,31 @@
-// lsd.cu — host orchestration of the 32/64-bit one-sweep LSD path (§8 rows a2-a5).
-//
-//   memset(hist) -> k_onesweep_hist -> k_plan -> P x { memset(look-back) ; k_onesweep_pass }
-//   -> k_copy_back (no-op unless an odd number of passes executed)
-// Everything is stream-ordered on the caller's stream; no host synchronisation.
-#include <cstdlib>
-#include <type_traits>
-
-#include "onesweep.cuh"
-#include "paths.cuh"
+// lsd.cu — entry points of the 32/64-bit LSD path (§8 rows a2-a5): workspace size and the
+// dispatch to the per-(key width, payload) translation units.
+#include "lsd_impl.cuh"
 
 namespace bsort {
-namespace {
 
-// Tile configuration per key width and ranking mode (tuned on B200 with tools/tune_pass.cu;
-// profiles/r1/tune_*.jsonl).  Two CTAs per SM of 512 (384) threads, 8192 (4608) keys per tile.
-// One 1024-thread CTA per SM shortens the look-back chains of a pure RUN2 pass (3.64 -> 3.38 ms)
-// but its 16384-key tiles break RUN2's two-run condition in pass 2 (runs of ~16K keys at
-// n = 2^30) and 8 keys per thread lose too much ILP (profiles/r1: cfg3 16.1 vs 16.6 / 19.7 ms).
-// Key-value sorts (KV) carry ITEMS more registers and a second tile buffer pair: one CTA per SM.
-template <typename U, int MODE, bool KV = false> struct PassCfg;
-template <int MODE, bool KV> struct PassCfg<uint32_t, MODE, KV> {
-  static constexpr int THREADS = 512, ITEMS = 16, MINB = KV ? 1 : 2, LBG = 8;
-};
-template <int MODE, bool KV> struct PassCfg<unsigned long long, MODE, KV> {
-  static constexpr int THREADS = 384, ITEMS = 12, MINB = KV ? 1 : 2, LBG = 8;
-};
-
-template <typename U> constexpr int hist_lanes() { return sizeof(U) == 4 ? 32 : 16; }
-
-struct LsdLayout {
-  size_t scratch, vscratch, ghist, bases, gcount, joint, seg, plan, counters, lookback, total;
-};
-
-// Pass 1 may run look-back-free (RANK_J01) from the joint histogram of digits 0 and 1; below
-// this size the digit-0 buckets are shorter than a tile anyway and the joint histogram's fixed
-// cost (65536 bins) is not worth it.
-constexpr uint64_t JOINT_MIN_N = 1ull << 24;
-
-template <typename U>
-LsdLayout lsd_layout(uint64_t n, bool kv = false) {
-  using C = PassCfg<U, RANK_RUN2>;  // the look-back passes size the descriptor array
-  constexpr uint64_t TILE = (uint64_t)C::THREADS * C::ITEMS;
-  constexpr int P = sizeof(U);
-  const uint64_t tiles = (n + TILE - 1) / TILE;
-  const size_t desc = (n <= (1ull << 30)) ? 4 : 8;
-  LsdLayout l;
-  size_t off = 0;
-  l.scratch = off;  off = align_up(off + n * sizeof(U), 256);
-  l.vscratch = off; off = align_up(off + (kv ? n * sizeof(uint32_t) : 0), 256);
-  l.ghist = off;    off = align_up(off + P * 256 * 8, 256);
-  l.bases = off;    off = align_up(off + P * 256 * 8, 256);
-  l.gcount = off;   off = align_up(off + P * 256 * 8, 256);
-  const size_t jbytes = n >= JOINT_MIN_N ? 65536 * 8 : 0;  // joint histogram + segment starts
-  l.joint = off;    off = align_up(off + jbytes, 256);
-  l.seg = off;      off = align_up(off + jbytes, 256);
-  l.plan = off;     off = align_up(off + sizeof(PassPlan), 256);
-  l.counters = off; off = align_up(off + 16 * 4, 256);
-  l.lookback = off; off = align_up(off + tiles * 256 * desc, 256);
-  l.total = off;
-  return l;
-}
-
-template <typename U, bool BULK, int RANK, bool KV, typename DescT, typename DigitF>
-bsort_status_t launch_pass_t(const U* a, U* b, uint64_t n, DigitF digit, const unsigned long long* bases,
-                             DescT* lookback, unsigned long long* gcount, uint32_t* counter, const PassPlan* plan,
-                             int pass, KvPtrs kvp, cudaStream_t s) {
-  using C = PassCfg<U, RANK, KV>;
-  using L = PassSmem<C::THREADS, C::ITEMS, U, RANK, KV>;
-  auto kern = k_onesweep_pass<U, C::THREADS, C::ITEMS, C::MINB, BULK, DescT, DigitF, RANK, C::LBG, KV>;
-  static int occ = 0;  // per instantiation; benign race (idempotent)
-  if (occ == 0) {
-    BSORT_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L::bytes));
-    int o = 0;
-    BSORT_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, kern, C::THREADS, L::bytes));
-    occ = o > 0 ? o : 1;
-  }
-  const uint64_t tiles = (n + L::TILE - 1) / L::TILE;
-  // persistent grid: every CTA resident at once (look-back forward progress)
-  const uint64_t grid = min64(tiles, (uint64_t)num_sms() * occ);
-  BSORT_LAUNCH(PROF_PASS, s,
-               kern<<<(unsigned)grid, C::THREADS, L::bytes, s>>>(a, b, n, digit, bases, lookback, gcount, counter,
-                                                                 (uint32_t)tiles, plan, pass, kvp));
-  return BSORT_SUCCESS;
-}
-
-// TMA bulk prefetch needs 16-byte aligned sources: both ping-pong buffers (the scratch buffer
-// always is; the caller's array may be only element-aligned).
-template <typename U, int RANK, typename DescT, bool KV = false, typename DigitF>
-bsort_status_t launch_pass(const U* a, U* b, uint64_t n, DigitF digit, const unsigned long long* bases,
-                           DescT* lookback, unsigned long long* gcount, uint32_t* counter, const PassPlan* plan,
-                           int pass, cudaStream_t s, KvPtrs kvp = {}) {
-  bool aligned = ((uintptr_t)a % 16 == 0) && (plan == nullptr || (uintptr_t)b % 16 == 0);
-  if (KV) aligned = aligned && (uintptr_t)kvp.va % 16 == 0 && (uintptr_t)kvp.vb % 16 == 0;
-  if (aligned)
-    return launch_pass_t<U, true, RANK, KV, DescT>(a, b, n, digit, bases, lookback, gcount, counter, plan, pass, kvp,
-                                                   s);
-  return launch_pass_t<U, false, RANK, KV, DescT>(a, b, n, digit, bases, lookback, gcount, counter, plan, pass, kvp,
-                                                  s);
-}
-
-bsort_status_t memset_async(void* p, size_t bytes, cudaStream_t s) {
-  BSORT_LAUNCH(PROF_MEMSET, s, cudaMemsetAsync(p, 0, bytes, s));
-  return BSORT_SUCCESS;
-}
-
-template <int KIND, bool DESC, typename U, typename DescT, bool KV>
-bsort_status_t lsd_run(U* keys, uint32_t* vals, uint64_t n, unsigned char* ws, cudaStream_t s) {
-  using C = PassCfg<U, RANK_RUN2>;
-  constexpr int P = sizeof(U);
-  constexpr int LANES = hist_lanes<U>();
-  constexpr uint64_t TILE = (uint64_t)C::THREADS * C::ITEMS;
-  const LsdLayout l = lsd_layout<U>(n, KV);
-  U* scratch = reinterpret_cast<U*>(ws + l.scratch);
-  const KvPtrs kvp{vals, reinterpret_cast<uint32_t*>(ws + l.vscratch)};
-  auto* ghist = reinterpret_cast<unsigned long long*>(ws + l.ghist);
-  auto* bases = reinterpret_cast<unsigned long long*>(ws + l.bases);
-  auto* gcount = reinterpret_cast<unsigned long long*>(ws + l.gcount);
-  auto* joint = reinterpret_cast<unsigned long long*>(ws + l.joint);
-  auto* seg = reinterpret_cast<unsigned long long*>(ws + l.seg);
-  auto* plan = reinterpret_cast<PassPlan*>(ws + l.plan);
-  auto* counters = reinterpret_cast<uint32_t*>(ws + l.counters);
-  auto* lookback = reinterpret_cast<DescT*>(ws + l.lookback);
-  const uint64_t tiles = (n + TILE - 1) / TILE;
-
-  static const bool joint_off = getenv("BSORT_NO_JOINT") != nullptr;  // A/B and debugging
-  const bool use_joint = n >= JOINT_MIN_N && !joint_off;
-  BSORT_LAUNCH(PROF_MEMSET, s, cudaMemsetAsync(ghist, 0, P * 256 * 8, s));
-  if (use_joint) {
-    constexpr int JL = sizeof(U) == 4 ? 32 : 8;  // lanes of the digit >= 2 counters
-    auto hk = k_onesweep_hist_joint<KIND, DESC, U, JL>;
-    constexpr int hsmem = (32768 + (P - 2) * 256 * JL) * 4;
-    static bool hattr = false;
-    if (!hattr) {
-      BSORT_CUDA(cudaFuncSetAttribute(hk, cudaFuncAttributeMaxDynamicSharedMemorySize, hsmem));
-      hattr = true;
-    }
-    BSORT_LAUNCH(PROF_MEMSET, s, cudaMemsetAsync(joint, 0, 65536 * 8, s));
-    BSORT_LAUNCH(PROF_HIST, s, hk<<<num_sms(), HIST_THREADS, hsmem, s>>>(keys, n, ghist, joint));
-  } else {
-    auto hk = k_onesweep_hist<KIND, DESC, U, LANES>;
-    constexpr int hsmem = P * 256 * LANES * 4;
-    static bool hattr = false;
-    if (!hattr) {
-      BSORT_CUDA(cudaFuncSetAttribute(hk, cudaFuncAttributeMaxDynamicSharedMemorySize, hsmem));
-      hattr = true;
-    }
-    BSORT_LAUNCH(PROF_HIST, s, hk<<<num_sms(), HIST_THREADS, hsmem, s>>>(keys, n, ghist));
-  }
-  BSORT_LAUNCH(PROF_SCAN, s,
-               k_plan<<<1, 256, 0, s>>>(ghist, n, P, bases, plan, counters, gcount, use_joint ? joint : nullptr));
-  if (use_joint)
-    BSORT_LAUNCH(PROF_SCAN, s, k_plan_joint<<<1, 256, 0, s>>>(joint, ghist, bases + 256, TILE, plan, seg));
-  bsort_status_t st = BSORT_SUCCESS;
-  auto one_pass = [&](auto shift_c) {
-    constexpr int SH = decltype(shift_c)::value;
-    constexpr int p = SH / 8;
-    if (p >= P || st != BSORT_SUCCESS) return;
-    if constexpr (p > 0) {
-      st = memset_async(lookback, tiles * 256 * sizeof(DescT), s);
-      if (st != BSORT_SUCCESS) return;
-    }
-    // The first LSD pass may order equal digits arbitrarily (the input order carries no
-    // information); every later pass must be stable.
-    if constexpr (p == 0)
-      st = launch_pass<U, RANK_UNSTABLE, DescT, KV>(keys, scratch, n, RadixDigit<KIND, DESC, U, SH>{}, bases,
-                                                    lookback, gcount, counters, plan, p, s, kvp);
-    else
-      st = launch_pass<U, RANK_RUN2, DescT, KV>(keys, scratch, n, RadixDigit<KIND, DESC, U, SH>{},
-                                                bases + p * 256, lookback, gcount + p * 256, counters + p,
-                                                plan, p, s, kvp);
-    // pass 1 without look-back when the joint plan allows it (each launch checks plan->j01
-    // and exactly one of the two does the work)
-    if constexpr (p == 1)
-      if (st == BSORT_SUCCESS && use_joint)
-        st = launch_pass<U, RANK_J01, DescT, KV>(keys, scratch, n, RadixDigit<KIND, DESC, U, SH>{}, bases + 256,
-                                                 lookback, seg, counters + 8, plan, p, s, kvp);
-  };
-  one_pass(std::integral_constant<int, 0>{});
-  one_pass(std::integral_constant<int, 8>{});
-  one_pass(std::integral_constant<int, 16>{});
-  one_pass(std::integral_constant<int, 24>{});
-  if constexpr (P == 8) {
-    one_pass(std::integral_constant<int, 32>{});
-    one_pass(std::integral_constant<int, 40>{});
-    one_pass(std::integral_constant<int, 48>{});
-    one_pass(std::integral_constant<int, 56>{});
-  }
-  if (st != BSORT_SUCCESS) return st;
-  const int cgrid = (int)min64((n + 255) / 256, (uint64_t)num_sms() * 16);
-  BSORT_LAUNCH(PROF_COPY, s, k_copy_back<U><<<cgrid, 256, 0, s>>>(keys, scratch, n, plan));
-  if constexpr (KV)
-    BSORT_LAUNCH(PROF_COPY, s, k_copy_back<uint32_t><<<cgrid, 256, 0, s>>>(vals, kvp.vb, n, plan));
-  return BSORT_SUCCESS;
-}
-
-template <int KIND, bool DESC, typename U>
-bsort_status_t lsd_dispatch_desc(U* keys, uint32_t* vals, uint64_t n, unsigned char* ws, cudaStream_t s) {
-  if (vals != nullptr) {
-    if (n <= (1ull << 30)) return lsd_run<KIND, DESC, U, uint32_t, true>(keys, vals, n, ws, s);
-    return lsd_run<KIND, DESC, U, unsigned long long, true>(keys, vals, n, ws, s);
-  }
-  if (n <= (1ull << 30)) return lsd_run<KIND, DESC, U, uint32_t, false>(keys, nullptr, n, ws, s);
-  return lsd_run<KIND, DESC, U, unsigned long long, false>(keys, nullptr, n, ws, s);
-}
-
-template <typename U>
-bsort_status_t lsd_dispatch(int kind, bool desc, U* keys, uint32_t* vals, uint64_t n, unsigned char* ws,
-                            cudaStream_t s) {
-  switch (kind) {
-    case KIND_U:
-      return desc ? lsd_dispatch_desc<KIND_U, true>(keys, vals, n, ws, s) : lsd_dispatch_desc<KIND_U, false>(keys, vals, n, ws, s);
-    case KIND_I:
-      return desc ? lsd_dispatch_desc<KIND_I, true>(keys, vals, n, ws, s) : lsd_dispatch_desc<KIND_I, false>(keys, vals, n, ws, s);
-    default:
-      return desc ? lsd_dispatch_desc<KIND_F, true>(keys, vals, n, ws, s) : lsd_dispatch_desc<KIND_F, false>(keys, vals, n, ws, s);
-  }
-}
-
-}  // namespace
+bsort_status_t lsd_sort_w4(int kind, bool desc, void* keys, uint32_t* vals, uint64_t n, unsigned char* ws,
+                           cudaStream_t s);
+bsort_status_t lsd_sort_w4_kv(int kind, bool desc, void* keys, uint32_t* vals, uint64_t n, unsigned char* ws,
+                              cudaStream_t s);
+bsort_status_t lsd_sort_w8(int kind, bool desc, void* keys, uint32_t* vals, uint64_t n, unsigned char* ws,
+                           cudaStream_t s);
+bsort_status_t lsd_sort_w8_kv(int kind, bool desc, void* keys, uint32_t* vals, uint64_t n, unsigned char* ws,
+                              cudaStream_t s);
 
 size_t lsd_workspace_bytes(int bytes, uint64_t n, bool kv) {
   if (n <= 1) return 0;
-  return bytes == 4 ? lsd_layout<uint32_t>(n, kv).total : lsd_layout<unsigned long long>(n, kv).total;
+  return bytes == 4 ? lsd_detail::lsd_layout<uint32_t>(n, kv).total
+                    : lsd_detail::lsd_layout<unsigned long long>(n, kv).total;
 }
 
 bsort_status_t lsd_sort(const DtypeInfo& di, void* keys, uint32_t* vals, uint64_t n, bool desc, void* ws,
                         size_t ws_bytes, cudaStream_t s) {
   if (ws_bytes < lsd_workspace_bytes(di.bytes, n, vals != nullptr)) return BSORT_ERROR_WORKSPACE_TOO_SMALL;
   auto* w = static_cast<unsigned char*>(ws);
-  if (di.bytes == 4) return lsd_dispatch<uint32_t>(di.kind, desc, static_cast<uint32_t*>(keys), vals, n, w, s);
-  return lsd_dispatch<unsigned long long>(di.kind, desc, static_cast<unsigned long long*>(keys), vals, n, w, s);
-}
-
-// ---------------------------------------------------------------- MSD partition (a7, a9)
-
-namespace {
-constexpr int TOP_BINS = BSORT_DIST_BINS;
-
-// Top-16-bit histogram of the transformed keys: 65536 u32 bins do not fit next to a useful
-// occupancy, so each CTA counts into a 16-bit-index smem table of 32768 u32 for its half of
-// the bins (CTA pairs, as in the 16-bit counting path) and flushes with global atomics.
-template <int KIND, bool DESC, typename U>
-__global__ void __launch_bounds__(1024, 1)
-    k_dist_tophist(const U* __restrict__ keys, uint64_t n, unsigned long long* __restrict__ hist) {
-  extern __shared__ uint32_t th[];
-  const uint32_t half = blockIdx.x & 1;
-  const uint32_t chunk = blockIdx.x >> 1;
-  const uint32_t pairs = gridDim.x >> 1;
-  for (int i = threadIdx.x; i < TOP_BINS / 2; i += 1024) th[i] = 0;
-  __syncthreads();
-  const uint64_t per = (n + pairs - 1) / pairs;
-  const uint64_t s0 = min64(n, (uint64_t)chunk * per), s1 = min64(n, s0 + per);
-  for (uint64_t i = s0 + threadIdx.x; i < s1; i += 1024) {
-    const uint32_t b = uint32_t(key_encode<KIND, DESC>(keys[i]) >> (sizeof(U) * 8 - 16));
-    if ((b >> 15) == half) atomicAdd(&th[b & 0x7FFF], 1u);
-  }
-  __syncthreads();
-  for (int b = threadIdx.x; b < TOP_BINS / 2; b += 1024)
-    if (th[b]) atomicAdd(&hist[half * (TOP_BINS / 2) + b], (unsigned long long)th[b]);
-}
-
-template <int KIND, bool DESC, typename U>
-bsort_status_t tophist_run(const U* keys, uint64_t n, uint64_t* hist, cudaStream_t s) {
-  auto* h = reinterpret_cast<unsigned long long*>(hist);
-  BSORT_LAUNCH(PROF_MEMSET, s, cudaMemsetAsync(h, 0, TOP_BINS * 8, s));
-  if (n == 0) return BSORT_SUCCESS;
-  auto k = k_dist_tophist<KIND, DESC, U>;
-  constexpr int smem = TOP_BINS / 2 * 4;
-  static bool attr = false;
-  if (!attr) {
-    BSORT_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-    attr = true;
-  }
-  const int pairs = max(1, num_sms() / 2);
-  BSORT_LAUNCH(PROF_DIST_HIST, s, k<<<2 * pairs, 1024, smem, s>>>(keys, n, h));
-  return BSORT_SUCCESS;
-}
-
-// Workspace of the MSD partition: tile counter, bucket bases, per-bucket running counts.  The
-// partition is an unstable pass (order inside a destination bucket is irrelevant: every rank
-// sorts what it receives), so it needs no look-back array.
-size_t part_layout(size_t* counters_off, size_t* bases_off, size_t* gcount_off) {
-  size_t off = 0;
-  *counters_off = off; off = align_up(off + 64, 256);
-  *bases_off = off;    off = align_up(off + 256 * 8, 256);
-  *gcount_off = off;   off = align_up(off + 256 * 8, 256);
-  return off;
-}
-
-template <int KIND, bool DESC, typename U>
-bsort_status_t part_run(const U* in, uint64_t n, const uint32_t* cuts, int nranks, U* out, unsigned char* ws,
-                        const unsigned long long* host_bases, const unsigned long long* host_dst, cudaStream_t s) {
-  size_t co, bo, go;
-  const size_t total = part_layout(&co, &bo, &go);
-  auto* counter = reinterpret_cast<uint32_t*>(ws + co);
-  auto* bases = reinterpret_cast<unsigned long long*>(ws + bo);
-  auto* gcount = reinterpret_cast<unsigned long long*>(ws + go);
-  BSORT_LAUNCH(PROF_MEMSET, s, cudaMemsetAsync(ws, 0, total, s));
-  // bases: exclusive offsets of each destination bucket (from the caller's send counts; the
-  // pageable copy is staged before cudaMemcpyAsync returns).
-  BSORT_CUDA(cudaMemcpyAsync(bases, host_bases, 256 * 8, cudaMemcpyHostToDevice, s));
-  auto fill = [&](auto& dg) {
-    for (int q = 0; q <= nranks; ++q) dg.cuts[q] = cuts[q];
-    for (int q = nranks + 1; q <= BSORT_DIST_MAX_RANKS; ++q) dg.cuts[q] = TOP_BINS;
-    dg.nranks = nranks;
-  };
-  if (host_dst != nullptr) {  // fused partition + exchange: write into the owners' buffers
-    RankDigit<KIND, DESC, U, true> dg;
-    fill(dg);
-    for (int q = 0; q < BSORT_DIST_MAX_RANKS; ++q) dg.dst_base[q] = q < nranks ? host_dst[q] : 0ull;
-    return launch_pass<U, RANK_UNSTABLE, uint32_t>(in, const_cast<U*>(in), n, dg, bases, (uint32_t*)nullptr, gcount,
-                                                   counter, nullptr, 0, s);
-  }
-  RankDigit<KIND, DESC, U> dg;
-  fill(dg);
-  return launch_pass<U, RANK_UNSTABLE, uint32_t>(in, out, n, dg, bases, (uint32_t*)nullptr, gcount, counter, nullptr,
-                                                 0, s);
-}
-
-}  // namespace
-
-bsort_status_t dist_top_hist(const DtypeInfo& di, const void* keys, uint64_t n, bool desc, uint64_t* hist,
-                             cudaStream_t s) {
-#define TOPH(U_)                                                                                                  \
-  switch (di.kind) {                                                                                              \
-    case KIND_U: return desc ? tophist_run<KIND_U, true>((const U_*)keys, n, hist, s)                             \
-                             : tophist_run<KIND_U, false>((const U_*)keys, n, hist, s);                           \
-    case KIND_I: return desc ? tophist_run<KIND_I, true>((const U_*)keys, n, hist, s)                             \
-                             : tophist_run<KIND_I, false>((const U_*)keys, n, hist, s);                           \
-    default: return desc ? tophist_run<KIND_F, true>((const U_*)keys, n, hist, s)                                 \
-                         : tophist_run<KIND_F, false>((const U_*)keys, n, hist, s);                               \
-  }
-  if (di.bytes == 4) { TOPH(uint32_t) }
-  TOPH(unsigned long long)
-#undef TOPH
-}
-
-size_t dist_partition_workspace_bytes(int bytes, uint64_t n, int nranks) {
-  (void)bytes;
-  (void)n;
-  (void)nranks;
-  size_t a, b, c;
-  return part_layout(&a, &b, &c);
-}
-
-bsort_status_t dist_partition(const DtypeInfo& di, const void* in, uint64_t n, bool desc, const uint32_t* cuts,
-                              const uint64_t* send_counts, int nranks, void* out, const uint64_t* dst_addrs,
-                              void* ws, size_t ws_bytes, cudaStream_t s) {
-  if (ws_bytes < dist_partition_workspace_bytes(di.bytes, n, nranks)) return BSORT_ERROR_WORKSPACE_TOO_SMALL;
-  if (n == 0) return BSORT_SUCCESS;
-  unsigned long long hb[256];
-  unsigned long long acc = 0;
-  for (int q = 0; q < 256; ++q) {
-    hb[q] = acc;
-    if (q < nranks) acc += send_counts[q];
-  }
-  if (acc != n) return BSORT_ERROR_INVALID_ARGUMENT;
-  auto* w = static_cast<unsigned char*>(ws);
-  const auto* hd = reinterpret_cast<const unsigned long long*>(dst_addrs);
-#define PART(U_)                                                                                                  \
-  {                                                                                                               \
-    const U_* i_ = static_cast<const U_*>(in);                                                                    \
-    U_* o_ = static_cast<U_*>(out);                                                                               \
-    switch (di.kind * 2 + (desc ? 1 : 0)) {                                                                       \
-      case 0: return part_run<KIND_U, false, U_>(i_, n, cuts, nranks, o_, w, hb, hd, s);                              \
-      case 1: return part_run<KIND_U, true, U_>(i_, n, cuts, nranks, o_, w, hb, hd, s);                               \
-      case 2: return part_run<KIND_I, false, U_>(i_, n, cuts, nranks, o_, w, hb, hd, s);                              \
-      case 3: return part_run<KIND_I, true, U_>(i_, n, cuts, nranks, o_, w, hb, hd, s);                               \
-      case 4: return part_run<KIND_F, false, U_>(i_, n, cuts, nranks, o_, w, hb, hd, s);                              \
-      default: return part_run<KIND_F, true, U_>(i_, n, cuts, nranks, o_, w, hb, hd, s);                              \
-    }                                                                                                             \
-  }
-  if (di.bytes == 4) PART(uint32_t)
-  PART(unsigned long long)
-#undef PART
+  if (di.bytes == 4)
+    return vals ? lsd_sort_w4_kv(di.kind, desc, keys, vals, n, w, s) : lsd_sort_w4(di.kind, desc, keys, nullptr, n, w, s);
+  return vals ? lsd_sort_w8_kv(di.kind, desc, keys, vals, n, w, s) : lsd_sort_w8(di.kind, desc, keys, nullptr, n, w, s);
 }
 
 }  // namespace bsort

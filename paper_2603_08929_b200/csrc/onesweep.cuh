@@ -323,7 +323,7 @@ __global__ void __launch_bounds__(HIST_THREADS, 1)
 // the pass-0 output meets at most two digit-0 runs.  Segment (d1 = a, d0 = b) of the pass-1
 // output starts at bases1[a] + sum_{b' < b} J[a][b']; those starts seed the allocation counters
 // (seg[b * 256 + a], the layout RANK_J01 indexes by (run's d0, digit)).
-__global__ void __launch_bounds__(256)
+static __global__ void __launch_bounds__(256)
     k_plan_joint(const unsigned long long* __restrict__ gjoint, const unsigned long long* __restrict__ ghist,
                  const unsigned long long* __restrict__ bases1, uint64_t tile, PassPlan* __restrict__ plan,
                  unsigned long long* __restrict__ seg) {
@@ -345,7 +345,7 @@ __global__ void __launch_bounds__(256)
 
 // Plan: exclusive scan of every digit histogram into global digit bases, trivial-digit
 // detection, ping-pong buffer assignment, tile-counter reset.  One CTA of 256 threads.
-__global__ void __launch_bounds__(256)
+static __global__ void __launch_bounds__(256)
     k_plan(unsigned long long* __restrict__ ghist, uint64_t n, int P, unsigned long long* __restrict__ bases,
            PassPlan* __restrict__ plan, uint32_t* __restrict__ tile_counters,
            unsigned long long* __restrict__ gcount, const unsigned long long* __restrict__ gjoint) {
