@@ -167,6 +167,35 @@ bsort_status_t bsort_dist_partition_remote(bsort_dtype_t dtype, const void* dev_
                                            const uint64_t* host_dst_addrs, void* workspace,
                                            size_t workspace_bytes, void* stream);
 
+/* Exact splitting: the building blocks that make every rank's shard exactly
+ * floor((r+1)N/P) - floor(rN/P) keys whatever the skew (paper_2603_08929_b200.sort_dist(...,
+ * exact=True) drives them).  All keys below are TRANSFORMED keys (the order key with the
+ * direction folded in), as unsigned integers of the dtype's width.
+ *
+ * bsort_dist_refine_hist: dev_hist (uint64, m * 65536, overwritten) counts, for each of the m
+ * prefixes (host, strictly increasing), the keys whose top `prefix_bits` bits equal
+ * prefixes[j], binned by their next 16 bits: dev_hist[j * 65536 + b].  prefix_bits is a
+ * multiple of 16 with prefix_bits + 16 <= key bits. */
+bsort_status_t bsort_dist_refine_hist(bsort_dtype_t dtype, const void* dev_keys, uint64_t n,
+                                      bsort_direction_t direction, const uint64_t* host_prefixes, int m,
+                                      int prefix_bits, uint64_t* dev_hist, void* stream);
+
+/* Classes against m distinct split keys values[0..m) (host, strictly increasing, transformed):
+ * class 2j holds the keys strictly between values[j-1] and values[j] (values[-1] = -inf,
+ * values[m] = +inf), class 2j+1 the keys equal to values[j].  bsort_dist_class_hist writes the
+ * 2m+1 class counts to dev_counts (uint64).  bsort_dist_partition_classes partitions the n keys
+ * into dev_out grouped by class in increasing class order (class c starts at the sum of
+ * host_class_counts[0..c)), order within a class unspecified; the counts must be this rank's
+ * (summing to n).  Workspace: bsort_dist_class_partition_workspace_bytes(). */
+bsort_status_t bsort_dist_class_hist(bsort_dtype_t dtype, const void* dev_keys, uint64_t n,
+                                     bsort_direction_t direction, const uint64_t* host_values, int m,
+                                     uint64_t* dev_counts, void* stream);
+size_t bsort_dist_class_partition_workspace_bytes(void);
+bsort_status_t bsort_dist_partition_classes(bsort_dtype_t dtype, const void* dev_in, uint64_t n,
+                                            bsort_direction_t direction, const uint64_t* host_values, int m,
+                                            const uint64_t* host_class_counts, void* dev_out,
+                                            void* workspace, size_t workspace_bytes, void* stream);
+
 /* ----------------------------------------------------------------------- diagnostics */
 
 const char* bsort_status_string(bsort_status_t status);

@@ -24,7 +24,8 @@ from . import _lib
 from ._lib import BsortError, check, lib
 
 __all__ = ["sort_", "sort", "sort_pairs_", "argsort", "Sorter", "sort_host", "sort_dist", "dtype_code", "workspace_bytes",
-           "top_hist", "splitters", "send_counts", "partition", "partition_remote", "profile",
+           "top_hist", "splitters", "send_counts", "partition", "partition_remote", "refine_hist",
+           "class_hist", "partition_classes", "profile",
            "launch_count",
            "BsortError", "version"]
 
@@ -234,6 +235,46 @@ def partition_remote(t: torch.Tensor, cuts: np.ndarray, counts: np.ndarray, dst_
                                           int(bool(descending)), _u32p(c), _u64p(sc), nranks,
                                           _u64p(da), ctypes.c_void_p(ws.data_ptr()), wsb,
                                           _stream_ptr(t.device)), "bsort_dist_partition_remote")
+
+
+def refine_hist(t: torch.Tensor, prefixes, prefix_bits: int, descending: bool = False) -> torch.Tensor:
+    """§8 N2: uint64[m, 65536] histogram of the next 16 transformed-key bits of the keys whose
+    top ``prefix_bits`` bits equal prefixes[j] (strictly increasing)."""
+    _check_tensor(t)
+    pre = np.ascontiguousarray(np.asarray(prefixes, dtype=np.uint64))
+    h = torch.empty(pre.size * _lib.DIST_BINS, dtype=torch.uint64, device=t.device)
+    check(lib.bsort_dist_refine_hist(dtype_code(t.dtype), ctypes.c_void_p(t.data_ptr()), t.numel(),
+                                     int(bool(descending)), _u64p(pre), pre.size, int(prefix_bits),
+                                     ctypes.c_void_p(h.data_ptr()), _stream_ptr(t.device)), "bsort_dist_refine_hist")
+    return h.view(pre.size, _lib.DIST_BINS)
+
+
+def class_hist(t: torch.Tensor, values, descending: bool = False) -> torch.Tensor:
+    """§8 N2: uint64[2m+1] counts of the key classes against the split keys ``values``."""
+    _check_tensor(t)
+    v = np.ascontiguousarray(np.asarray(values, dtype=np.uint64))
+    c = torch.empty(2 * v.size + 1, dtype=torch.uint64, device=t.device)
+    check(lib.bsort_dist_class_hist(dtype_code(t.dtype), ctypes.c_void_p(t.data_ptr()), t.numel(),
+                                    int(bool(descending)), _u64p(v), v.size, ctypes.c_void_p(c.data_ptr()),
+                                    _stream_ptr(t.device)), "bsort_dist_class_hist")
+    return c
+
+
+def partition_classes(t: torch.Tensor, values, class_counts, descending: bool = False) -> torch.Tensor:
+    """§8 N2: keys grouped by class (increasing), class c starting at sum(class_counts[:c])."""
+    _check_tensor(t)
+    v = np.ascontiguousarray(np.asarray(values, dtype=np.uint64))
+    cc = np.ascontiguousarray(np.asarray(class_counts, dtype=np.uint64))
+    out = torch.empty_like(t)
+    if t.numel() == 0:
+        return out
+    wsb = int(lib.bsort_dist_class_partition_workspace_bytes())
+    ws = _workspace(wsb, t.device)
+    check(lib.bsort_dist_partition_classes(dtype_code(t.dtype), ctypes.c_void_p(t.data_ptr()), t.numel(),
+                                           int(bool(descending)), _u64p(v), v.size, _u64p(cc),
+                                           ctypes.c_void_p(out.data_ptr()), ctypes.c_void_p(ws.data_ptr()), wsb,
+                                           _stream_ptr(t.device)), "bsort_dist_partition_classes")
+    return out
 
 
 from .dist import sort_dist  # noqa: E402  (needs the helpers above)

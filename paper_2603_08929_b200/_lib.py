@@ -27,6 +27,8 @@ EXPORTS = [
     "bsort_pairs_workspace_bytes", "bsort_sort_pairs_ws", "bsort_sort_pairs",
     "bsort_dist_top_hist", "bsort_dist_splitters", "bsort_dist_send_counts",
     "bsort_dist_partition_workspace_bytes", "bsort_dist_partition", "bsort_dist_partition_remote",
+    "bsort_dist_refine_hist", "bsort_dist_class_hist", "bsort_dist_class_partition_workspace_bytes",
+    "bsort_dist_partition_classes",
     "bsort_status_string", "bsort_last_cuda_error", "bsort_version", "bsort_launch_count",
     "bsort_profile_enable", "bsort_profile_read", "bsort_profile_kind_name",
 ]
@@ -65,6 +67,10 @@ def _load():
         "bsort_dist_partition_workspace_bytes": (sz, [i32, u64, i32]),
         "bsort_dist_partition": (i32, [i32, vp, u64, i32, u32p, u64p, i32, vp, vp, sz, vp]),
         "bsort_dist_partition_remote": (i32, [i32, vp, u64, i32, u32p, u64p, i32, u64p, vp, sz, vp]),
+        "bsort_dist_refine_hist": (i32, [i32, vp, u64, i32, u64p, i32, i32, vp, vp]),
+        "bsort_dist_class_hist": (i32, [i32, vp, u64, i32, u64p, i32, vp, vp]),
+        "bsort_dist_class_partition_workspace_bytes": (sz, []),
+        "bsort_dist_partition_classes": (i32, [i32, vp, u64, i32, u64p, i32, u64p, vp, vp, sz, vp]),
         "bsort_status_string": (ctypes.c_char_p, [i32]),
         "bsort_last_cuda_error": (i32, []),
         "bsort_version": (ctypes.c_char_p, []),

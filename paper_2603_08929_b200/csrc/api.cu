@@ -316,6 +316,63 @@ bsort_status_t bsort_dist_partition_remote(bsort_dtype_t dtype, const void* dev_
                         dst_addrs, workspace, workspace_bytes_, (cudaStream_t)stream);
 }
 
+// ------------------------------------------------------------- exact splitting (N2)
+
+namespace {
+bool increasing(const uint64_t* v, int m) {
+  for (int j = 1; j < m; ++j)
+    if (v[j] <= v[j - 1]) return false;
+  return true;
+}
+}  // namespace
+
+bsort_status_t bsort_dist_refine_hist(bsort_dtype_t dtype, const void* dev_keys, uint64_t n,
+                                      bsort_direction_t direction, const uint64_t* prefixes, int m,
+                                      int prefix_bits, uint64_t* dev_hist, void* stream) {
+  DtypeInfo di;
+  bsort_status_t st = validate(dtype, dev_keys, n, direction, &di);
+  if (st != BSORT_SUCCESS) return st;
+  if (di.bytes < 4) return BSORT_ERROR_UNSUPPORTED_DTYPE;
+  if (!prefixes || m < 1 || m > BSORT_DIST_MAX_RANKS || !increasing(prefixes, m)) return BSORT_ERROR_INVALID_ARGUMENT;
+  if (prefix_bits < 16 || prefix_bits % 16 != 0 || prefix_bits + 16 > di.bytes * 8) return BSORT_ERROR_INVALID_ARGUMENT;
+  if (!dev_hist || !aligned_to(dev_hist, 8)) return BSORT_ERROR_INVALID_ARGUMENT;
+  return dist_refine_hist(di, dev_keys, n, direction == BSORT_DESCENDING, prefixes, m, prefix_bits, dev_hist,
+                          (cudaStream_t)stream);
+}
+
+bsort_status_t bsort_dist_class_hist(bsort_dtype_t dtype, const void* dev_keys, uint64_t n,
+                                     bsort_direction_t direction, const uint64_t* values, int m,
+                                     uint64_t* dev_counts, void* stream) {
+  DtypeInfo di;
+  bsort_status_t st = validate(dtype, dev_keys, n, direction, &di);
+  if (st != BSORT_SUCCESS) return st;
+  if (di.bytes < 4) return BSORT_ERROR_UNSUPPORTED_DTYPE;
+  if (!values || m < 1 || m > BSORT_DIST_MAX_RANKS || !increasing(values, m)) return BSORT_ERROR_INVALID_ARGUMENT;
+  if (!dev_counts || !aligned_to(dev_counts, 8)) return BSORT_ERROR_INVALID_ARGUMENT;
+  return dist_class_hist(di, dev_keys, n, direction == BSORT_DESCENDING, values, m, dev_counts,
+                         (cudaStream_t)stream);
+}
+
+size_t bsort_dist_class_partition_workspace_bytes(void) { return dist_class_partition_workspace_bytes(); }
+
+bsort_status_t bsort_dist_partition_classes(bsort_dtype_t dtype, const void* dev_in, uint64_t n,
+                                            bsort_direction_t direction, const uint64_t* values, int m,
+                                            const uint64_t* class_counts, void* dev_out, void* workspace,
+                                            size_t workspace_bytes_, void* stream) {
+  DtypeInfo di;
+  bsort_status_t st = validate(dtype, dev_in, n, direction, &di);
+  if (st != BSORT_SUCCESS) return st;
+  if (di.bytes < 4) return BSORT_ERROR_UNSUPPORTED_DTYPE;
+  if (!values || !class_counts || m < 1 || m > BSORT_DIST_MAX_RANKS || !increasing(values, m))
+    return BSORT_ERROR_INVALID_ARGUMENT;
+  if (n == 0) return BSORT_SUCCESS;
+  if (!dev_out || !aligned_to(dev_out, di.bytes) || dev_out == dev_in) return BSORT_ERROR_INVALID_ARGUMENT;
+  if (!workspace || !aligned_to(workspace, 256)) return BSORT_ERROR_INVALID_ARGUMENT;
+  if (workspace_bytes_ < dist_class_partition_workspace_bytes()) return BSORT_ERROR_WORKSPACE_TOO_SMALL;
+  return dist_partition_classes(di, dev_in, n, direction == BSORT_DESCENDING, values, m, class_counts, dev_out,
+                                workspace, (cudaStream_t)stream);
+}
+
 // ------------------------------------------------------------------------ diagnostics
 
 const char* bsort_status_string(bsort_status_t s) {

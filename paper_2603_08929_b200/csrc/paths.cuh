@@ -32,4 +32,15 @@ bsort_status_t dist_partition(const DtypeInfo& di, const void* in, uint64_t n, b
                               void* out, const uint64_t* dst_addrs, void* ws,
                               size_t ws_bytes, cudaStream_t s);
 
+// §8 N2: exact splitting (csrc/exact.cu).
+bsort_status_t dist_refine_hist(const DtypeInfo& di, const void* keys, uint64_t n, bool desc,
+                                const uint64_t* prefixes, int m, int prefix_bits, uint64_t* hist,
+                                cudaStream_t s);
+bsort_status_t dist_class_hist(const DtypeInfo& di, const void* keys, uint64_t n, bool desc,
+                               const uint64_t* values, int m, uint64_t* counts, cudaStream_t s);
+size_t dist_class_partition_workspace_bytes();
+bsort_status_t dist_partition_classes(const DtypeInfo& di, const void* in, uint64_t n, bool desc,
+                                      const uint64_t* values, int m, const uint64_t* class_counts,
+                                      void* out, void* ws, cudaStream_t s);
+
 }  // namespace bsort
