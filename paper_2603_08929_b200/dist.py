@@ -45,19 +45,92 @@ class DistOps:
     send_counts: Callable     # (np.uint64[65536], cuts) -> np.uint64[nranks]
     partition: Callable       # (tensor, cuts, counts, descending) -> tensor (bucketed)
     local_sort: Callable      # (tensor, descending) -> tensor sorted in place
+    # exact splitting (§8 N2)
+    refine_hist: Optional[Callable] = None        # (tensor, prefixes, prefix_bits, desc) -> u64[m, 65536]
+    class_hist: Optional[Callable] = None         # (tensor, values, desc) -> u64[2m+1]
+    partition_classes: Optional[Callable] = None  # (tensor, values, class_counts, desc) -> tensor
 
 
 def cuda_ops() -> DistOps:
-    from . import partition, send_counts, sort_, splitters, top_hist
+    from . import (class_hist, partition, partition_classes, refine_hist, send_counts, sort_,
+                   splitters, top_hist)
     return DistOps(top_hist=top_hist, splitters=splitters, send_counts=send_counts,
-                   partition=partition, local_sort=sort_)
+                   partition=partition, local_sort=sort_, refine_hist=refine_hist,
+                   class_hist=class_hist, partition_classes=partition_classes)
 
 
 @dataclass
 class DistStats:
-    cuts: np.ndarray
+    cuts: Optional[np.ndarray]
     send_counts: np.ndarray
     recv_counts: np.ndarray
+    values: Optional[np.ndarray] = None   # exact mode: the distinct split keys (transformed)
+    quota: Optional[np.ndarray] = None    # exact mode: per boundary, equal keys sent left
+    levels: int = 0                       # exact mode: refinement histograms taken
+
+
+def exact_boundaries(hg: np.ndarray, nranks: int, width: int, refine: Callable):
+    """§8 N2 (host part): the transformed key K_r of global rank T_r = floor(r N / P) for every
+    boundary r = 1..P-1, and quota_r = T_r - #{keys < K_r} (how many keys equal to K_r precede
+    the boundary).  ``hg`` is the global top-16-bit histogram; ``refine(prefixes, bits)`` returns
+    the GLOBAL uint64[m, 65536] histogram of the next 16 bits below each ``bits``-bit prefix.
+
+    Each boundary descends the radix tree 16 bits at a time (the MSD digit order of P:427-433)
+    until its rank falls on a bin start (quota 0: K_r = the prefix followed by zeros, which need
+    not be a key) or the prefix is the whole key.  Returns (values: strictly increasing distinct
+    K's as np.uint64, idx: index of K_r in values, quota: np.int64, levels)."""
+    N = int(hg.astype(np.int64).sum())
+    R = nranks - 1
+    T = [(r * N) // nranks for r in range(1, nranks)]
+    pv, below, bits = [0] * R, [0] * R, [16] * R
+    cum = np.cumsum(hg.astype(np.int64))
+    for i in range(R):
+        b = int(np.searchsorted(cum, T[i], side="right"))  # bin holding the key of rank T_i
+        pv[i] = b
+        below[i] = int(cum[b - 1]) if b > 0 else 0
+    levels, level_bits = 0, 16
+    open_ = [i for i in range(R) if T[i] > below[i]]
+    while open_ and level_bits < width:
+        prefixes = sorted({pv[i] for i in open_})
+        H = np.asarray(refine(np.array(prefixes, dtype=np.uint64), level_bits)).astype(np.int64)
+        levels += 1
+        row = {p: j for j, p in enumerate(prefixes)}
+        for i in open_:
+            c = np.cumsum(H[row[pv[i]]])
+            sb = int(np.searchsorted(c, T[i] - below[i], side="right"))
+            below[i] += int(c[sb - 1]) if sb > 0 else 0
+            pv[i] = (pv[i] << 16) | sb
+            bits[i] += 16
+        level_bits += 16
+        open_ = [i for i in open_ if T[i] > below[i]]
+    K = [pv[i] << (width - bits[i]) for i in range(R)]
+    values = sorted(set(K))
+    vi = {v: j for j, v in enumerate(values)}
+    idx = np.array([vi[k] for k in K], dtype=np.int64)
+    quota = np.array([T[i] - below[i] for i in range(R)], dtype=np.int64)
+    return np.array(values, dtype=np.uint64), idx, quota, levels
+
+
+def exact_send_counts(class_counts_all: np.ndarray, me: int, idx: np.ndarray,
+                      quota: np.ndarray) -> np.ndarray:
+    """Per-destination send counts of rank ``me`` over its class-ordered keys (§8 N2).
+
+    ``class_counts_all[q]`` = rank q's 2m+1 class counts.  Boundary r cuts my buffer after all
+    classes below K_r (classes 0..2j) plus my share of the keys equal to K_r: the equal keys are
+    assigned to the left in rank order, quota_r of them in total, so my share is
+    clip(quota_r - (equal keys on ranks < me), 0, my equal keys).  Summed over ranks every
+    boundary lands exactly on global rank T_r."""
+    c = class_counts_all.astype(np.int64)
+    mine = c[me]
+    start = np.concatenate([[0], np.cumsum(mine)])
+    eq_before = c[:me, 1::2].sum(axis=0) if me > 0 else np.zeros(c.shape[1] // 2, dtype=np.int64)
+    splits = [0]
+    for r in range(len(idx)):
+        j = int(idx[r])
+        share = min(max(int(quota[r]) - int(eq_before[j]), 0), int(mine[2 * j + 1]))
+        splits.append(int(start[2 * j + 1]) + share)
+    splits.append(int(mine.sum()))
+    return np.diff(np.array(splits, dtype=np.int64)).astype(np.uint64)
 
 
 _SYMM = {}  # (group name, dtype, device) -> (buffer, handle): receive buffers of the fused path
@@ -84,7 +157,8 @@ def fused_default() -> bool:
 
 def sort_dist(t: torch.Tensor, group=None, descending: bool = False,
               ops: Optional[DistOps] = None, return_stats: bool = False,
-              a2a_events: Optional[list] = None, fused: Optional[bool] = None):
+              a2a_events: Optional[list] = None, fused: Optional[bool] = None,
+              exact: bool = False):
     """Globally sort the keys held by all ranks of ``group``; returns this rank's shard.
 
     ``t`` (1-D, contiguous) may be clobbered.  The concatenation of the returned shards over
@@ -93,7 +167,12 @@ def sort_dist(t: torch.Tensor, group=None, descending: bool = False,
     around the keys all-to-all on the current stream is appended to it.
     ``fused``: partition straight into the owners' symmetric-memory buffers (§8 N1); the
     returned shard is then a view of the group's receive buffer, valid until the next fused
-    ``sort_dist`` call on the same group, dtype and device."""
+    ``sort_dist`` call on the same group, dtype and device.
+    ``exact``: exact splitting (§8 N2) -- rank r receives exactly floor((r+1)N/P) - floor(rN/P)
+    keys whatever the key distribution (one refinement histogram per 16 further key bits a
+    boundary needs, plus a class histogram); default is the bin-granular split (reading Q16)."""
+    if exact:
+        return _sort_dist_exact(t, group, descending, ops or cuda_ops(), return_stats, a2a_events)
     if fused is None:
         fused = fused_default() and ops is None and t.is_cuda
     ops = ops or cuda_ops()
@@ -163,3 +242,64 @@ def _fused_exchange(t, cuts, sc, rc, descending, group, a2a_events=None):
         me = dist.get_rank(group)
         a2a_events.append((ev, int(sc.sum() - sc[me]) * es))
     return buf[:n_out]
+
+
+def _u64_allreduce(x: torch.Tensor, group) -> np.ndarray:
+    y = x.contiguous().view(torch.int64).clone()
+    dist.all_reduce(y, op=dist.ReduceOp.SUM, group=group)
+    return y.cpu().numpy().view(np.uint64)
+
+
+def _keys_all_to_all(t, bucketed, sc, group, a2a_events):
+    rc_t = torch.empty(len(sc), dtype=torch.int64, device=t.device)
+    dist.all_to_all_single(rc_t, torch.from_numpy(sc.astype(np.int64)).to(t.device), group=group)
+    rc = rc_t.cpu().numpy().astype(np.int64)
+    es = t.element_size()
+    out = torch.empty(int(rc.sum()), dtype=t.dtype, device=t.device)
+    ev = None
+    if a2a_events is not None and t.is_cuda:
+        ev = (torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+        ev[0].record()
+    dist.all_to_all_single(out.view(torch.uint8), bucketed.view(torch.uint8),
+                           output_split_sizes=[int(c) * es for c in rc],
+                           input_split_sizes=[int(c) * es for c in sc], group=group)
+    if ev is not None:
+        ev[1].record()
+        a2a_events.append((ev, int(sc.sum() - sc[dist.get_rank(group)]) * es))
+    return out, rc
+
+
+def _sort_dist_exact(t, group, descending, ops, return_stats, a2a_events):
+    """§8 N2: exact splitters by histogram refinement, class partition, one keys all-to-all."""
+    if ops.refine_hist is None or ops.class_hist is None or ops.partition_classes is None:
+        raise ValueError("exact splitting needs refine_hist, class_hist and partition_classes ops")
+    P = dist.get_world_size(group)
+    me = dist.get_rank(group)
+    width = t.element_size() * 8
+    hg = _u64_allreduce(ops.top_hist(t, descending), group)
+    N = int(hg.astype(np.int64).sum())
+
+    def done(out, sc, rc, values=None, quota=None, levels=0):
+        ops.local_sort(out, descending)
+        if return_stats:
+            return out, DistStats(cuts=None, send_counts=sc, recv_counts=rc.astype(np.uint64),
+                                  values=values, quota=quota, levels=levels)
+        return out
+
+    if P == 1 or N == 0:
+        sc = np.zeros(P, dtype=np.uint64)
+        sc[me] = t.numel()
+        return done(t, sc, sc.astype(np.int64))
+
+    def refine(prefixes, bits):
+        return _u64_allreduce(ops.refine_hist(t, prefixes, bits, descending), group).reshape(len(prefixes), -1)
+
+    values, idx, quota, levels = exact_boundaries(hg, P, width, refine)
+    cc = ops.class_hist(t, values, descending)
+    cc_all = [torch.empty_like(cc.view(torch.int64)) for _ in range(P)]
+    dist.all_gather(cc_all, cc.view(torch.int64).contiguous(), group=group)
+    C = np.stack([c.cpu().numpy() for c in cc_all]).astype(np.int64)
+    sc = exact_send_counts(C, me, idx, quota)
+    bucketed = ops.partition_classes(t, values, C[me].astype(np.uint64), descending)
+    out, rc = _keys_all_to_all(t, bucketed, sc, group, a2a_events)
+    return done(out, sc, rc, values, quota, levels)

@@ -28,13 +28,27 @@ def _free_port():
     return p
 
 
-def _enc_top16(arr: np.ndarray, descending: bool) -> np.ndarray:
+def _enc(arr: np.ndarray, descending: bool) -> np.ndarray:
+    """The oracle's total-order key with the direction folded in (np.uint64)."""
     scheme = oracle.NATIVE_SCHEMES[arr.dtype]
     w = scheme.width
     k = oracle.total_order_keys(arr.view(UINT[arr.itemsize]).astype(np.uint64), scheme)
     if descending:
         k = ~k & np.uint64((1 << w) - 1 if w < 64 else 0xFFFFFFFFFFFFFFFF)
-    return (k >> np.uint64(w - 16)).astype(np.int64)
+    return k
+
+
+def _enc_top16(arr: np.ndarray, descending: bool) -> np.ndarray:
+    w = arr.itemsize * 8
+    return (_enc(arr, descending) >> np.uint64(w - 16)).astype(np.int64)
+
+
+def _classes(t, values, desc):
+    k = _enc(t.numpy(), desc)
+    v = np.asarray(values, dtype=np.uint64)
+    lo = np.searchsorted(v, k, side="left")   # number of values < key
+    hi = np.searchsorted(v, k, side="right")
+    return 2 * lo + (hi - lo)                 # 2j+1 if key == values[j], else 2 * #{values < key}
 
 
 def cpu_ops():
@@ -56,8 +70,28 @@ def cpu_ops():
         t.copy_(torch.from_numpy(oracle.sort_native(t.numpy(), descending=desc)))
         return t
 
+    def refine_hist(t, prefixes, bits, desc):
+        w = t.element_size() * 8
+        k = _enc(t.numpy(), desc)
+        h = np.zeros((len(prefixes), 65536), dtype=np.int64)
+        for j, p in enumerate(prefixes):
+            sel = k[(k >> np.uint64(w - bits)) == np.uint64(p)]
+            h[j] = np.bincount(((sel >> np.uint64(w - bits - 16)) & np.uint64(0xFFFF)).astype(np.int64),
+                               minlength=65536)
+        return torch.from_numpy(h).view(torch.uint64)
+
+    def class_hist(t, values, desc):
+        c = np.bincount(_classes(t, values, desc), minlength=2 * len(values) + 1)
+        return torch.from_numpy(c.astype(np.int64)).view(torch.uint64)
+
+    def partition_classes(t, values, counts, desc):
+        cls = _classes(t, values, desc)
+        assert np.array_equal(np.bincount(cls, minlength=len(counts)), counts.astype(np.int64))
+        return torch.from_numpy(np.ascontiguousarray(t.numpy()[np.argsort(cls, kind="stable")]))
+
     return DistOps(top_hist=top_hist, splitters=B.splitters, send_counts=B.send_counts,
-                   partition=partition, local_sort=local_sort)
+                   partition=partition, local_sort=local_sort, refine_hist=refine_hist,
+                   class_hist=class_hist, partition_classes=partition_classes)
 
 
 def _make_local(dtype, n, rank, seed, skew):
@@ -65,6 +99,12 @@ def _make_local(dtype, n, rank, seed, skew):
     nd = NPD[dtype]
     if skew == "equal":
         a = np.full(n, 7, dtype=nd)
+    elif skew == "few":   # heavy duplicates, a handful of distinct keys spanning several bins
+        vals = np.array([-5, 0, 3, 3 + (1 << 20), 1 << 24], dtype=np.int64).astype(nd)
+        a = vals[rng.integers(0, len(vals), size=n)]
+    elif skew == "close":  # distinct keys sharing their top 16 (and for 64-bit, 32) bits
+        base = 1 << (np.dtype(nd).itemsize * 8 - 2)
+        a = (base + rng.integers(0, 1 << 12, size=n)).astype(nd)
     elif np.dtype(nd).kind == "f":
         a = np.concatenate([rng.standard_normal(n // 2), rng.uniform(-1e6, 1e6, n - n // 2)]).astype(nd)
         a[::97] = -0.0
@@ -75,7 +115,7 @@ def _make_local(dtype, n, rank, seed, skew):
     return a
 
 
-def _worker(rank, world, port, dtype, n_per, desc, skew, q):
+def _worker(rank, world, port, dtype, n_per, desc, skew, q, exact=False):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
@@ -83,9 +123,9 @@ def _worker(rank, world, port, dtype, n_per, desc, skew, q):
         n = n_per + 37 * rank  # uneven shards
         a = _make_local(dtype, n, rank, 5, skew)
         out, st = sort_dist(torch.from_numpy(a.copy()), descending=desc, ops=cpu_ops(),
-                            return_stats=True)
-        q.put((rank, a, out.numpy().copy(), st.cuts.copy(), st.send_counts.copy(),
-               st.recv_counts.copy()))
+                            return_stats=True, exact=exact)
+        q.put((rank, a, out.numpy().copy(), None if st.cuts is None else st.cuts.copy(),
+               st.send_counts.copy(), st.recv_counts.copy(), st.levels))
     finally:
         dist.destroy_process_group()
 
@@ -122,3 +162,33 @@ def test_sort_dist_gloo(world, dtype, desc, skew):
     assert [len(s) for s in shards] == list(recv.sum(axis=1))
     if skew == "equal":
         assert sum(1 for s in shards if len(s)) == 1  # bin-granular split (reading Q16)
+
+
+@pytest.mark.parametrize("world,dtype,desc,skew", [
+    (2, torch.int32, False, "equal"),
+    (3, torch.int64, True, "few"),
+    (3, torch.float32, False, "random"),
+    (2, torch.int64, False, "close"),
+    (3, torch.int32, True, "close"),
+])
+def test_sort_dist_exact_gloo(world, dtype, desc, skew):
+    """§8 N2: every shard holds exactly floor((r+1)N/P) - floor(rN/P) keys, whatever the skew."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    n_per = 6000
+    procs = [ctx.Process(target=_worker, args=(r, world, port, dtype, n_per, desc, skew, q, True))
+             for r in range(world)]
+    for p in procs:
+        p.start()
+    res = sorted([q.get(timeout=240) for _ in range(world)], key=lambda x: x[0])
+    for p in procs:
+        p.join(60)
+        assert p.exitcode == 0
+    inputs = np.concatenate([r[1] for r in res])
+    shards = [r[2] for r in res]
+    assert np.concatenate(shards).tobytes() == oracle.sort_native(inputs, descending=desc).tobytes()
+    N = len(inputs)
+    assert [len(s) for s in shards] == [(r + 1) * N // world - r * N // world for r in range(world)]
+    if skew == "close":
+        assert res[0][6] >= 1  # the boundaries needed at least one refinement histogram

@@ -210,3 +210,128 @@ def test_sort_dist_fused_nccl_one_rank(B):
             assert host(out).tobytes() == ref.tobytes()
     finally:
         dist.destroy_process_group()
+
+
+# ------------------------------------------------------------------ §8 N2 exact splitting
+
+def enc_oracle(arr: np.ndarray, descending: bool) -> np.ndarray:
+    """The oracle's total-order key, direction folded in (np.uint64)."""
+    s = oracle.NATIVE_SCHEMES[arr.dtype]
+    k = oracle.total_order_keys(arr.view(UINT[arr.itemsize]).astype(np.uint64), s)
+    if descending:
+        k = ~k & np.uint64((1 << s.width) - 1 if s.width < 64 else 0xFFFFFFFFFFFFFFFF)
+    return k
+
+
+def classes_oracle(k: np.ndarray, values: np.ndarray) -> np.ndarray:
+    lo = np.searchsorted(values, k, side="left")
+    hi = np.searchsorted(values, k, side="right")
+    return 2 * lo + (hi - lo)
+
+
+def clustered(dtype, n, seed):
+    """Keys sharing their top bits (so boundaries need refinement) with heavy duplicates."""
+    g = torch.Generator().manual_seed(seed)
+    w = torch.empty(0, dtype=dtype).element_size() * 8
+    idt = torch.int64 if w == 64 else torch.int32
+    low = torch.randint(0, 1 << 10, (n,), generator=g, dtype=torch.int64)
+    base = (0x1234 << (w - 20)) if w == 32 else (0x123456789 << 28)
+    x = (low + base).to(idt)
+    x[::3] = base + 77  # one heavily repeated key
+    return x.view(dtype).cuda()
+
+
+@pytest.mark.parametrize("dtype", [torch.int32, torch.float32, torch.uint64, torch.float64])
+@pytest.mark.parametrize("descending", [False, True])
+def test_refine_and_class_hist(B, dtype, descending):
+    n = 250_011
+    x = gen(dtype, n, 61) if dtype.is_floating_point else clustered(dtype, n, 61)
+    k = enc_oracle(host(x), descending)
+    w = x.element_size() * 8
+    # refine below the two most populated 16-bit prefixes
+    top = (k >> np.uint64(w - 16)).astype(np.int64)
+    pre = np.sort(np.argsort(np.bincount(top, minlength=65536))[-2:]).astype(np.uint64)
+    for bits in range(16, w, 16):
+        if bits > 16:
+            pre = np.unique(k >> np.uint64(w - bits))[:3]
+        h = B.refine_hist(x, pre, bits, descending).view(torch.int64).cpu().numpy()
+        for j, p in enumerate(pre):
+            sel = k[(k >> np.uint64(w - bits)) == p]
+            ref = np.bincount(((sel >> np.uint64(w - bits - 16)) & np.uint64(0xFFFF)).astype(np.int64),
+                              minlength=65536)
+            assert np.array_equal(h[j], ref), (bits, j)
+    vals = np.unique(k[:: n // 5])[:6]
+    vals = np.sort(np.concatenate([vals, vals[:1] + np.uint64(1)]))
+    vals = np.unique(vals)
+    c = B.class_hist(x, vals, descending).view(torch.int64).cpu().numpy()
+    assert np.array_equal(c, np.bincount(classes_oracle(k, vals), minlength=2 * len(vals) + 1))
+    out = B.partition_classes(x, vals, c.astype(np.uint64), descending)
+    torch.cuda.synchronize()
+    ko = enc_oracle(host(out), descending)
+    cls = classes_oracle(ko, vals)
+    assert (np.diff(cls) >= 0).all()  # grouped by class, increasing
+    assert np.array_equal(np.sort(ko), np.sort(k))
+
+
+def simulated_exact(B, parts, descending):
+    """sort_dist(exact=True) on one GPU: kernels per virtual rank, collectives as tensor ops."""
+    from paper_2603_08929_b200.dist import exact_boundaries, exact_send_counts
+    P = len(parts)
+    w = parts[0].element_size() * 8
+    hg = sum(B.top_hist(p, descending).view(torch.int64).cpu().numpy() for p in parts).view(np.uint64)
+
+    def refine(prefixes, bits):
+        return sum(B.refine_hist(p, prefixes, bits, descending).view(torch.int64).cpu().numpy()
+                   for p in parts).view(np.uint64)
+
+    values, idx, quota, levels = exact_boundaries(hg, P, w, refine)
+    C = np.stack([B.class_hist(p, values, descending).view(torch.int64).cpu().numpy() for p in parts])
+    sends = [exact_send_counts(C, r, idx, quota).astype(np.int64) for r in range(P)]
+    buckets = [B.partition_classes(p, values, C[r].astype(np.uint64), descending) for r, p in enumerate(parts)]
+    offs = [np.concatenate([[0], np.cumsum(sc)]) for sc in sends]
+    shards = []
+    for q in range(P):
+        recv = torch.cat([buckets[r][int(offs[r][q]):int(offs[r][q + 1])] for r in range(P)])
+        B.sort_(recv, descending)
+        shards.append(recv)
+    return shards, levels
+
+
+@pytest.mark.parametrize("dtype,P,desc,kind", [
+    (torch.int32, 4, False, "equal"), (torch.float64, 3, True, "clustered"),
+    (torch.uint64, 8, False, "clustered"), (torch.float32, 5, False, "random"),
+    (torch.int64, 2, True, "random")])
+def test_simulated_exact_split(B, dtype, P, desc, kind):
+    parts = []
+    for r in range(P):
+        n = 60_000 + 101 * r
+        if kind == "equal":
+            parts.append(torch.full((n,), 7, dtype=dtype, device="cuda"))
+        elif kind == "clustered":
+            parts.append(clustered(dtype, n, 300 + r) if not dtype.is_floating_point else
+                         clustered(torch.int64 if dtype == torch.float64 else torch.int32, n, 300 + r).view(dtype))
+        else:
+            parts.append(gen(dtype, n, 300 + r))
+    allkeys = np.concatenate([host(p) for p in parts])
+    shards, levels = simulated_exact(B, parts, desc)
+    torch.cuda.synchronize()
+    N = len(allkeys)
+    assert [s.numel() for s in shards] == [(q + 1) * N // P - q * N // P for q in range(P)]
+    got = np.concatenate([host(s) for s in shards])
+    assert got.tobytes() == oracle.sort_native(allkeys, descending=desc).tobytes()
+    if kind == "clustered":
+        assert levels >= 1
+
+
+def test_sort_dist_exact_nccl_one_rank(B):
+    import torch.distributed as dist
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(_free_port()))
+    dist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device("cuda:0"))
+    try:
+        x = W.make("cfg5", "cuda", n=100_003, dtype=torch.float64)
+        ref = oracle.sort_native(host(x))
+        out = B.sort_dist(x, exact=True)
+        torch.cuda.synchronize()
+        assert host(out).tobytes() == ref.tobytes()
+    finally:
+        dist.destroy_process_group()
