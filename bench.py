@@ -324,7 +324,7 @@ def bench_multi(args, B):
     restore = lambda: work.copy_(pristine)  # noqa: E731
     for _ in range(args.warmup):
         restore()
-        B.sort_dist(work)
+        B.sort_dist(work, exact=args.exact)
     torch.cuda.synchronize()
     dist.barrier()
     launches0 = B.launch_count()
@@ -343,7 +343,7 @@ def bench_multi(args, B):
                 restore()
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             e0.record(stream)
-            B.sort_dist(work, a2a_events=a2a)
+            B.sort_dist(work, a2a_events=a2a, exact=args.exact)
             e1.record(stream)
             step_ev.append((e0, e1))
         b.record(stream)
@@ -367,7 +367,7 @@ def bench_multi(args, B):
         ea, eb = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         ea.record(stream)
         work.copy_(host, non_blocking=True)
-        shard = B.sort_dist(work)
+        shard = B.sort_dist(work, exact=args.exact)
         res = shard.cpu()
         eb.record(stream)
         torch.cuda.synchronize()
@@ -388,7 +388,7 @@ def bench_multi(args, B):
             "config": {"workload": f"cfg3 distribution, {n} f32 keys per rank x {world} ranks, "
                                    "globally sorted shards (MSD top-16-bit split + NCCL all-to-all "
                                    "+ local one-sweep LSD)", "n_per_rank": n,
-                       "parallelism": f"msd-a2a x{world}",
+                       "parallelism": f"msd-a2a x{world}" + (" exact-split" if args.exact else ""),
                        "l2": "inputs of n*4 B per rank (4 GiB at the default n) >> L2; restored by D2D copy between steps"},
             "roofline": {"bound": "nvlink", "achieved": achieved, "peak": nv_peak, "unit": "GB/s",
                          "frac": (achieved / nv_peak) if achieved else None, "traffic": None,
@@ -447,6 +447,8 @@ def main():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--cpu-sample", type=int, default=1 << 25)
     ap.add_argument("--ref-sample", type=int, default=1 << 22)
+    ap.add_argument("--exact", action="store_true",
+                    help="N > 1: exact splitting (SURVEY §8 N2) instead of bin-granular cuts")
     ap.add_argument("--force-dist", action="store_true",
                     help="run the multi-GPU code path even at world size 1 (testing)")
     args = ap.parse_args()
