@@ -22,7 +22,7 @@ build/%.o: $(PKG)/csrc/%.cu $(CHDR)
 	@mkdir -p build
 	$(NVCC) $(NVFLAGS) -c -o $@ $<
 $(PKG)/libbsort.so: $(OBJS)
-	$(NVCC) $(ARCH) -shared -o $@ $(OBJS) -lcudart
+	$(NVCC) $(ARCH) -shared -o $@ $(OBJS) -lcudart -ldl
 
 clean:
 	rm -rf build oracle/liboracle.so $(PKG)/libbsort.so

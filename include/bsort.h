@@ -63,7 +63,9 @@ typedef enum {
   BSORT_ERROR_UNSUPPORTED_DTYPE = 2,  /* dtype not valid for this entry point               */
   BSORT_ERROR_OUT_OF_MEMORY = 3,      /* cudaMallocAsync of the internal workspace failed    */
   BSORT_ERROR_WORKSPACE_TOO_SMALL = 4,/* workspace_bytes < the *_workspace_bytes() figure    */
-  BSORT_ERROR_CUDA = 5                /* a CUDA runtime call or launch failed                */
+  BSORT_ERROR_CUDA = 5,               /* a CUDA runtime call or launch failed                */
+  BSORT_ERROR_NCCL = 6,               /* NCCL missing or an NCCL call failed (bsort_last_nccl_error) */
+  BSORT_ERROR_CAPACITY = 7            /* bsort_sort_dist: some rank's dev_out is too small    */
 } bsort_status_t;
 
 /* ----------------------------------------------------------------------- single GPU */
@@ -195,6 +197,38 @@ bsort_status_t bsort_dist_partition_classes(bsort_dtype_t dtype, const void* dev
                                             bsort_direction_t direction, const uint64_t* host_values, int m,
                                             const uint64_t* host_class_counts, void* dev_out,
                                             void* workspace, size_t workspace_bytes, void* stream);
+
+/* ------------------------------------------------ native multi-GPU sort (SURVEY §8 b)
+ * The complete MSD path (a7-a11) in one call over an NCCL communicator owned by the library:
+ * top-16-bit histogram + ncclAllReduce, host splitters (bsort_dist_splitters), ncclAllGather of
+ * every rank's send counts and capacity, P-way partition, grouped ncclSend/ncclRecv of the keys,
+ * local bsort_sort_ws.  NCCL is loaded at run time (libnccl.so.2); if it cannot be loaded these
+ * calls return BSORT_ERROR_NCCL.  One process (or thread) per GPU; each rank calls collectively
+ * with its own communicator.
+ *
+ * bsort_get_unique_id: a fresh ncclUniqueId (128 bytes) on one rank, to be broadcast by the
+ * caller.  bsort_comm_init: collective over the nranks ranks, on the CURRENT device; *out owns
+ * an ncclComm_t until bsort_comm_destroy.
+ *
+ * bsort_sort_dist: 32/64-bit dtypes (u32/i32/f32/u64/i64/f64; others UNSUPPORTED_DTYPE).
+ * dev_in (n_local keys) is read and may NOT be modified (kept intact); dev_out (device,
+ * out_capacity keys, distinct from dev_in) receives this rank's shard sorted in `direction`;
+ * the concatenation of the shards over ranks 0..P-1 is the global order.  Shard boundaries are
+ * bin-granular (reading Q16).  *n_out (host, nullable) = this rank's shard size.
+ * If any rank's shard exceeds its out_capacity, EVERY rank returns BSORT_ERROR_CAPACITY after
+ * the counts exchange with nothing written to dev_out (n_out still set).  Blocks the host twice
+ * (after the histogram all-reduce and after the counts all-gather); scratch is
+ * cudaMallocAsync'ed on `stream` (n_local keys + partition/sort workspace). */
+typedef struct bsort_comm* bsort_comm_t;
+bsort_status_t bsort_get_unique_id(uint8_t id[128]);
+bsort_status_t bsort_comm_init(bsort_comm_t* out, const uint8_t id[128], int nranks, int rank);
+bsort_status_t bsort_comm_destroy(bsort_comm_t comm);
+int bsort_comm_size(bsort_comm_t comm);
+int bsort_comm_rank(bsort_comm_t comm);
+bsort_status_t bsort_sort_dist(bsort_dtype_t dtype, const void* dev_in, uint64_t n_local, void* dev_out,
+                               uint64_t out_capacity, uint64_t* n_out, bsort_direction_t direction,
+                               bsort_comm_t comm, void* stream);
+int bsort_last_nccl_error(void);          /* raw ncclResult_t of the last NCCL failure (thread-local) */
 
 /* ----------------------------------------------------------------------- diagnostics */
 

@@ -25,7 +25,7 @@ from ._lib import BsortError, check, lib
 
 __all__ = ["sort_", "sort", "sort_pairs_", "argsort", "Sorter", "sort_host", "sort_dist", "dtype_code", "workspace_bytes",
            "top_hist", "splitters", "send_counts", "partition", "partition_remote", "refine_hist",
-           "class_hist", "partition_classes", "profile",
+           "class_hist", "partition_classes", "Comm", "sort_dist_native", "profile",
            "launch_count",
            "BsortError", "version"]
 
@@ -275,6 +275,72 @@ def partition_classes(t: torch.Tensor, values, class_counts, descending: bool = 
                                            ctypes.c_void_p(out.data_ptr()), ctypes.c_void_p(ws.data_ptr()), wsb,
                                            _stream_ptr(t.device)), "bsort_dist_partition_classes")
     return out
+
+
+class Comm:
+    """A library-owned NCCL communicator (bsort_comm_t) for the native distributed sort.
+
+    Collective: every rank of ``group`` (torch.distributed) constructs it with its own device
+    current; rank 0's ncclUniqueId is broadcast over ``group``.  ``Comm.local()`` makes a
+    one-rank communicator without torch.distributed."""
+
+    def __init__(self, group=None, _rank: int = None, _world: int = None):
+        if _world is None:
+            import torch.distributed as dist
+            rank, world = dist.get_rank(group), dist.get_world_size(group)
+            uid = [None]
+            if rank == 0:
+                buf = ctypes.create_string_buffer(128)
+                check(lib.bsort_get_unique_id(buf), "bsort_get_unique_id")
+                uid[0] = buf.raw
+            dist.broadcast_object_list(uid, src=dist.get_global_rank(group, 0) if group else 0, group=group)
+            raw = uid[0]
+        else:
+            rank, world = _rank, _world
+            buf = ctypes.create_string_buffer(128)
+            check(lib.bsort_get_unique_id(buf), "bsort_get_unique_id")
+            raw = buf.raw
+        self._h = ctypes.c_void_p()
+        check(lib.bsort_comm_init(ctypes.byref(self._h), raw, world, rank), "bsort_comm_init")
+        self.rank, self.size = rank, world
+
+    @classmethod
+    def local(cls) -> "Comm":
+        return cls(_rank=0, _world=1)
+
+    def close(self):
+        if self._h:
+            check(lib.bsort_comm_destroy(self._h), "bsort_comm_destroy")
+            self._h = ctypes.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def sort_dist_native(t: torch.Tensor, comm: Comm, descending: bool = False,
+                     capacity: int = None) -> torch.Tensor:
+    """§8 b ``bsort_sort_dist``: the whole MSD path in one libbsort call over ``comm`` (NCCL).
+    Returns this rank's shard (sorted); ``t`` is left intact.  Collective over comm's ranks.
+    If some rank's shard exceeds ``capacity`` (default 2 x n_local + 65,536) every rank gets
+    BSORT_ERROR_CAPACITY and the call is retried once, collectively, with the exact sizes."""
+    _check_tensor(t)
+    n = t.numel()
+    cap = capacity if capacity is not None else 2 * n + (1 << 16)
+    for attempt in range(2):
+        out = torch.empty(cap, dtype=t.dtype, device=t.device)
+        n_out = ctypes.c_uint64(0)
+        st = lib.bsort_sort_dist(dtype_code(t.dtype), ctypes.c_void_p(t.data_ptr()), n,
+                                 ctypes.c_void_p(out.data_ptr()), cap, ctypes.byref(n_out),
+                                 int(bool(descending)), comm._h, _stream_ptr(t.device))
+        if st == _lib.ERROR_CAPACITY and attempt == 0:
+            cap = int(n_out.value)
+            continue
+        check(st, "bsort_sort_dist")
+        return out[:int(n_out.value)]
+    raise AssertionError("unreachable")
 
 
 from .dist import sort_dist  # noqa: E402  (needs the helpers above)

@@ -21,6 +21,8 @@ DIST_MAX_RANKS = 64
 PROF_KINDS = 12
 
 SUCCESS = 0
+ERROR_NCCL = 6
+ERROR_CAPACITY = 7
 
 EXPORTS = [
     "bsort_workspace_bytes", "bsort_sort", "bsort_sort_ws", "bsort_sort_host",
@@ -29,6 +31,8 @@ EXPORTS = [
     "bsort_dist_partition_workspace_bytes", "bsort_dist_partition", "bsort_dist_partition_remote",
     "bsort_dist_refine_hist", "bsort_dist_class_hist", "bsort_dist_class_partition_workspace_bytes",
     "bsort_dist_partition_classes",
+    "bsort_get_unique_id", "bsort_comm_init", "bsort_comm_destroy", "bsort_comm_size", "bsort_comm_rank",
+    "bsort_sort_dist", "bsort_last_nccl_error",
     "bsort_status_string", "bsort_last_cuda_error", "bsort_version", "bsort_launch_count",
     "bsort_profile_enable", "bsort_profile_read", "bsort_profile_kind_name",
 ]
@@ -40,6 +44,8 @@ class BsortError(RuntimeError):
         extra = ""
         if status == 5:
             extra = f" (cudaError {lib.bsort_last_cuda_error()})"
+        elif status == 6:
+            extra = f" (ncclResult {lib.bsort_last_nccl_error()})"
         super().__init__(f"{where}: {msg}{extra}")
         self.status = status
 
@@ -71,6 +77,13 @@ def _load():
         "bsort_dist_class_hist": (i32, [i32, vp, u64, i32, u64p, i32, vp, vp]),
         "bsort_dist_class_partition_workspace_bytes": (sz, []),
         "bsort_dist_partition_classes": (i32, [i32, vp, u64, i32, u64p, i32, u64p, vp, vp, sz, vp]),
+        "bsort_get_unique_id": (i32, [ctypes.c_char_p]),
+        "bsort_comm_init": (i32, [ctypes.POINTER(vp), ctypes.c_char_p, i32, i32]),
+        "bsort_comm_destroy": (i32, [vp]),
+        "bsort_comm_size": (i32, [vp]),
+        "bsort_comm_rank": (i32, [vp]),
+        "bsort_sort_dist": (i32, [i32, vp, u64, vp, u64, u64p, i32, vp, vp]),
+        "bsort_last_nccl_error": (i32, []),
         "bsort_status_string": (ctypes.c_char_p, [i32]),
         "bsort_last_cuda_error": (i32, []),
         "bsort_version": (ctypes.c_char_p, []),

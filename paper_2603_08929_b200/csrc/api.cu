@@ -383,6 +383,8 @@ const char* bsort_status_string(bsort_status_t s) {
     case BSORT_ERROR_OUT_OF_MEMORY: return "out of device memory";
     case BSORT_ERROR_WORKSPACE_TOO_SMALL: return "workspace too small";
     case BSORT_ERROR_CUDA: return "CUDA error";
+    case BSORT_ERROR_NCCL: return "NCCL error";
+    case BSORT_ERROR_CAPACITY: return "output capacity too small";
     default: return "unknown status";
   }
 }

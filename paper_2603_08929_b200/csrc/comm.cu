@@ -1,0 +1,286 @@
+// comm.cu — native multi-GPU sort over NCCL (SURVEY §8 b: bsort_comm_* / bsort_sort_dist).
+//
+// The whole MSD path of §8 a7-a11 in one C call, built only from this library's own ABI
+// (bsort_dist_top_hist, bsort_dist_splitters, bsort_dist_send_counts, bsort_dist_partition,
+// bsort_sort_ws) plus NCCL collectives on the caller's stream:
+//
+//   a7  top-16-bit histogram            -> ncclAllReduce(sum) of 65,536 u64
+//   a8  splitters + send counts (host)  -> ncclAllGather of every rank's (send counts, capacity)
+//   a9  P-way partition by destination  (unstable one-sweep pass into a bucketed scratch copy)
+//   a10 grouped ncclSend / ncclRecv     (keys to their owners, rank-ordered in dev_out)
+//   a11 local one-sweep LSD sort of dev_out
+//
+// NCCL is bound at run time (dlopen "libnccl.so.2"): libbsort.so has no link-time NCCL
+// dependency, and inside a PyTorch process the already-loaded libnccl (same soname) is reused.
+// Two host syncs: after the histogram all-reduce (splitters are host math) and after the counts
+// all-gather (receive sizes and the capacity check, which every rank evaluates for every rank so
+// that a too-small dev_out makes ALL ranks return BSORT_ERROR_CAPACITY before any key moves).
+#include <dlfcn.h>
+#include <nccl.h>
+
+#include <algorithm>
+#include <cstring>
+#include <mutex>
+#include <vector>
+
+#include "bsort.h"
+#include "common.cuh"
+
+namespace {
+
+struct NcclApi {
+  bool ok = false;
+  ncclResult_t (*GetUniqueId)(ncclUniqueId*) = nullptr;
+  ncclResult_t (*CommInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+  ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
+  ncclResult_t (*AllReduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t,
+                            cudaStream_t) = nullptr;
+  ncclResult_t (*AllGather)(const void*, void*, size_t, ncclDataType_t, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*Send)(const void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*Recv)(void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*GroupStart)() = nullptr;
+  ncclResult_t (*GroupEnd)() = nullptr;
+};
+
+NcclApi& nccl() {
+  static NcclApi api;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+    if (!h) h = dlopen("libnccl.so", RTLD_NOW | RTLD_GLOBAL);
+    if (!h) return;
+    bool all = true;
+    auto get = [&](auto& fp, const char* name) {
+      fp = reinterpret_cast<std::remove_reference_t<decltype(fp)>>(dlsym(h, name));
+      all = all && fp != nullptr;
+    };
+    get(api.GetUniqueId, "ncclGetUniqueId");
+    get(api.CommInitRank, "ncclCommInitRank");
+    get(api.CommDestroy, "ncclCommDestroy");
+    get(api.AllReduce, "ncclAllReduce");
+    get(api.AllGather, "ncclAllGather");
+    get(api.Send, "ncclSend");
+    get(api.Recv, "ncclRecv");
+    get(api.GroupStart, "ncclGroupStart");
+    get(api.GroupEnd, "ncclGroupEnd");
+    api.ok = all;
+  });
+  return api;
+}
+
+thread_local int t_last_nccl = 0;
+
+bsort_status_t nccl_status(ncclResult_t r) {
+  if (r == ncclSuccess) return BSORT_SUCCESS;
+  t_last_nccl = (int)r;
+  return BSORT_ERROR_NCCL;
+}
+
+bsort_status_t cuda_status(cudaError_t e) {
+  if (e == cudaSuccess) return BSORT_SUCCESS;
+  bsort::set_last_cuda_error(e);
+  cudaGetLastError();
+  return BSORT_ERROR_CUDA;
+}
+
+#define NCCL_TRY(x)                                   \
+  do {                                                \
+    bsort_status_t st_ = nccl_status(x);              \
+    if (st_ != BSORT_SUCCESS) return st_;             \
+  } while (0)
+#define CUDA_TRY(x)                                   \
+  do {                                                \
+    bsort_status_t st_ = cuda_status(x);              \
+    if (st_ != BSORT_SUCCESS) return st_;             \
+  } while (0)
+#define BS_TRY(x)                                     \
+  do {                                                \
+    bsort_status_t st_ = (x);                         \
+    if (st_ != BSORT_SUCCESS) return st_;             \
+  } while (0)
+
+int key_bytes(bsort_dtype_t dt) {
+  switch (dt) {
+    case BSORT_U32: case BSORT_I32: case BSORT_F32: return 4;
+    case BSORT_U64: case BSORT_I64: case BSORT_F64: return 8;
+    default: return 0;
+  }
+}
+
+size_t round_up(size_t v, size_t a) { return (v + a - 1) / a * a; }
+
+}  // namespace
+
+struct bsort_comm {
+  ncclComm_t comm = nullptr;
+  int nranks = 0;
+  int rank = 0;
+  int device = 0;
+};
+
+namespace {
+
+// RAII for the call's single cudaMallocAsync block (freed stream-ordered on every exit path).
+struct StreamBlock {
+  void* p = nullptr;
+  cudaStream_t s = nullptr;
+  ~StreamBlock() {
+    if (p) cudaFreeAsync(p, s);
+  }
+};
+
+bsort_status_t sort_dist_impl(bsort_dtype_t dtype, const void* dev_in, uint64_t n, void* dev_out, uint64_t cap,
+                              uint64_t* n_out, bsort_direction_t dir, bsort_comm* c, cudaStream_t s) {
+  NcclApi& N = nccl();
+  const int P = c->nranks, me = c->rank;
+  const int es = key_bytes(dtype);
+
+  // One device block: [global hist | local hist | counts (P x (P+1)) | bucketed keys | ws]
+  // The local sort's workspace reuses the bucketed keys + partition workspace after the exchange.
+  const size_t hist_b = (size_t)BSORT_DIST_BINS * 8;
+  const size_t cnt_b = round_up((size_t)P * (P + 1) * 8, 256);
+  const size_t bucket_b = round_up((size_t)n * es, 256);
+  const size_t part_ws = bsort_dist_partition_workspace_bytes(dtype, n, P);
+  const size_t head = 2 * hist_b + cnt_b;
+  StreamBlock blk;
+  blk.s = s;
+  // the tail must hold the partition phase and, later, the local sort of up to `cap` keys
+  const size_t sort_ws_cap = bsort_workspace_bytes(dtype, cap);
+  const size_t tail = std::max(bucket_b + part_ws, sort_ws_cap);
+  if (cudaMallocAsync(&blk.p, head + tail, s) != cudaSuccess) {
+    cudaGetLastError();
+    blk.p = nullptr;
+    return BSORT_ERROR_OUT_OF_MEMORY;
+  }
+  char* base = static_cast<char*>(blk.p);
+  uint64_t* g_hist = reinterpret_cast<uint64_t*>(base);
+  uint64_t* l_hist = reinterpret_cast<uint64_t*>(base + hist_b);
+  uint64_t* d_cnt = reinterpret_cast<uint64_t*>(base + 2 * hist_b);
+  char* bucket = base + head;
+  char* ws = bucket + bucket_b;
+
+  // a7: local histogram, global = all-reduce(sum)
+  BS_TRY(bsort_dist_top_hist(dtype, dev_in, n, dir, l_hist, s));
+  NCCL_TRY(N.AllReduce(l_hist, g_hist, BSORT_DIST_BINS, ncclUint64, ncclSum, c->comm, s));
+  std::vector<uint64_t> hist(2 * (size_t)BSORT_DIST_BINS);
+  CUDA_TRY(cudaMemcpyAsync(hist.data(), g_hist, 2 * hist_b, cudaMemcpyDeviceToHost, s));
+  CUDA_TRY(cudaStreamSynchronize(s));
+
+  // a8: cuts from the global histogram; this rank's send counts; gather (counts, capacity)
+  std::vector<uint32_t> cuts(P + 1);
+  std::vector<uint64_t> mine(P + 1);
+  BS_TRY(bsort_dist_splitters(hist.data(), P, cuts.data()));
+  BS_TRY(bsort_dist_send_counts(hist.data() + BSORT_DIST_BINS, cuts.data(), P, mine.data()));
+  mine[P] = cap;
+  CUDA_TRY(cudaMemcpyAsync(d_cnt + (size_t)me * (P + 1), mine.data(), (P + 1) * 8, cudaMemcpyHostToDevice, s));
+  NCCL_TRY(N.AllGather(d_cnt + (size_t)me * (P + 1), d_cnt, P + 1, ncclUint64, c->comm, s));
+  std::vector<uint64_t> all((size_t)P * (P + 1));
+  CUDA_TRY(cudaMemcpyAsync(all.data(), d_cnt, all.size() * 8, cudaMemcpyDeviceToHost, s));
+  CUDA_TRY(cudaStreamSynchronize(s));
+  auto sent = [&](int src, int dst) { return all[(size_t)src * (P + 1) + dst]; };
+
+  // capacity: every rank checks every rank, so all return the same status
+  uint64_t recv_total = 0;
+  bool overflow = false;
+  for (int q = 0; q < P; ++q) {
+    uint64_t tot = 0;
+    for (int r = 0; r < P; ++r) tot += sent(r, q);
+    if (q == me) recv_total = tot;
+    if (tot > all[(size_t)q * (P + 1) + P]) overflow = true;
+  }
+  if (n_out) *n_out = recv_total;
+  if (overflow) return BSORT_ERROR_CAPACITY;
+
+  // a9: bucketed copy (bucket q = keys for rank q)
+  if (n > 0)
+    BS_TRY(bsort_dist_partition(dtype, dev_in, n, dir, cuts.data(), mine.data(), P, bucket, ws, part_ws, s));
+
+  // a10: grouped send/recv; rank r's keys land at sum_{r'<r} sent(r', me) in dev_out
+  NCCL_TRY(N.GroupStart());
+  ncclResult_t first = ncclSuccess;
+  uint64_t soff = 0, roff = 0;
+  for (int q = 0; q < P; ++q) {
+    const uint64_t sc = sent(me, q), rc = sent(q, me);
+    ncclResult_t r = ncclSuccess;
+    if (sc) r = N.Send(bucket + soff * es, sc * es, ncclUint8, q, c->comm, s);
+    if (first == ncclSuccess) first = r;
+    if (rc) r = N.Recv(static_cast<char*>(dev_out) + roff * es, rc * es, ncclUint8, q, c->comm, s);
+    if (first == ncclSuccess) first = r;
+    soff += sc;
+    roff += rc;
+  }
+  const ncclResult_t ge = N.GroupEnd();
+  NCCL_TRY(first);
+  NCCL_TRY(ge);
+
+  // a11: local sort of the received keys (workspace reuses the bucketed region, now dead)
+  if (recv_total > 1) {
+    const size_t wsb = bsort_workspace_bytes(dtype, recv_total);
+    BS_TRY(bsort_sort_ws(dtype, dev_out, recv_total, dir, bucket, wsb, s));
+  }
+  return BSORT_SUCCESS;
+}
+
+}  // namespace
+
+extern "C" {
+
+bsort_status_t bsort_get_unique_id(uint8_t id[128]) {
+  if (!id) return BSORT_ERROR_INVALID_ARGUMENT;
+  NcclApi& N = nccl();
+  if (!N.ok) return BSORT_ERROR_NCCL;
+  ncclUniqueId u;
+  NCCL_TRY(N.GetUniqueId(&u));
+  static_assert(sizeof(u) == 128, "ncclUniqueId is 128 bytes");
+  std::memcpy(id, &u, 128);
+  return BSORT_SUCCESS;
+}
+
+bsort_status_t bsort_comm_init(bsort_comm_t* out, const uint8_t id[128], int nranks, int rank) {
+  if (!out || !id || nranks < 1 || nranks > BSORT_DIST_MAX_RANKS || rank < 0 || rank >= nranks)
+    return BSORT_ERROR_INVALID_ARGUMENT;
+  NcclApi& N = nccl();
+  if (!N.ok) return BSORT_ERROR_NCCL;
+  ncclUniqueId u;
+  std::memcpy(&u, id, 128);
+  auto* c = new bsort_comm;
+  c->nranks = nranks;
+  c->rank = rank;
+  cudaGetDevice(&c->device);
+  ncclResult_t r = N.CommInitRank(&c->comm, nranks, u, rank);
+  if (r != ncclSuccess) {
+    delete c;
+    return nccl_status(r);
+  }
+  *out = c;
+  return BSORT_SUCCESS;
+}
+
+bsort_status_t bsort_comm_destroy(bsort_comm_t c) {
+  if (!c) return BSORT_ERROR_INVALID_ARGUMENT;
+  NcclApi& N = nccl();
+  ncclResult_t r = N.ok && c->comm ? N.CommDestroy(c->comm) : ncclSuccess;
+  delete c;
+  return nccl_status(r);
+}
+
+int bsort_comm_size(bsort_comm_t c) { return c ? c->nranks : 0; }
+int bsort_comm_rank(bsort_comm_t c) { return c ? c->rank : -1; }
+
+bsort_status_t bsort_sort_dist(bsort_dtype_t dtype, const void* dev_in, uint64_t n_local, void* dev_out,
+                               uint64_t out_capacity, uint64_t* n_out, bsort_direction_t direction,
+                               bsort_comm_t comm, void* stream) {
+  if (!comm || !comm->comm) return BSORT_ERROR_INVALID_ARGUMENT;
+  if (direction != BSORT_ASCENDING && direction != BSORT_DESCENDING) return BSORT_ERROR_INVALID_ARGUMENT;
+  const int es = key_bytes(dtype);
+  if (es == 0) return BSORT_ERROR_UNSUPPORTED_DTYPE;
+  if (n_local > 0 && (!dev_in || (uintptr_t)dev_in % es)) return BSORT_ERROR_INVALID_ARGUMENT;
+  if (out_capacity > 0 && (!dev_out || (uintptr_t)dev_out % es)) return BSORT_ERROR_INVALID_ARGUMENT;
+  if (dev_out && dev_in && dev_out == dev_in && n_local > 0) return BSORT_ERROR_INVALID_ARGUMENT;
+  return sort_dist_impl(dtype, dev_in, n_local, dev_out, out_capacity, n_out, direction, comm,
+                        (cudaStream_t)stream);
+}
+
+int bsort_last_nccl_error(void) { return t_last_nccl; }
+
+}  // extern "C"

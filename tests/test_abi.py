@@ -91,6 +91,16 @@ def test_argument_errors_return_before_launch(B):
     assert L.bsort_workspace_bytes(99, 100) == 0
     assert L.bsort_dist_top_hist(0, ctypes.c_void_p(256), 10, 0, ctypes.c_void_p(256), None) == 2
     assert L.bsort_status_string(4) == b"workspace too small"
+    # native distributed sort: argument errors before any NCCL or CUDA call
+    assert L.bsort_sort_dist(5, ctypes.c_void_p(256), 10, ctypes.c_void_p(512), 10, None, 0, None, None) == 1
+    h = ctypes.c_void_p()
+    assert L.bsort_comm_init(ctypes.byref(h), b"\0" * 128, 0, 0) == 1       # nranks < 1
+    assert L.bsort_comm_init(ctypes.byref(h), b"\0" * 128, 2, 2) == 1       # rank out of range
+    assert L.bsort_comm_init(ctypes.byref(h), b"\0" * 128, 65, 0) == 1      # > BSORT_DIST_MAX_RANKS
+    assert L.bsort_comm_destroy(None) == 1
+    assert L.bsort_comm_size(None) == 0 and L.bsort_comm_rank(None) == -1
+    assert L.bsort_status_string(6) == b"NCCL error"
+    assert L.bsort_status_string(7) == b"output capacity too small"
 
 
 def test_workspace_model(B):

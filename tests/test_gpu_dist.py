@@ -335,3 +335,59 @@ def test_sort_dist_exact_nccl_one_rank(B):
         assert host(out).tobytes() == ref.tobytes()
     finally:
         dist.destroy_process_group()
+
+
+# ------------------------------------------------- §8 b native bsort_sort_dist over NCCL
+
+@pytest.mark.parametrize("dtype,desc", [(torch.float64, False), (torch.int32, True),
+                                        (torch.uint64, False), (torch.float32, True)])
+def test_sort_dist_native_local_comm(B, dtype, desc):
+    """bsort_comm_init (one rank, no torch.distributed) + bsort_sort_dist: the whole MSD path in
+    libbsort (histogram, NCCL all-reduce / all-gather / send-recv, partition, local sort)."""
+    comm = B.Comm.local()
+    try:
+        for n in (0, 1, 5000, 300_007):
+            x = gen(dtype, n, 500 + n)
+            before = x.clone()
+            out = B.sort_dist_native(x, comm, desc)
+            torch.cuda.synchronize()
+            assert host(out).tobytes() == oracle.sort_native(host(before), descending=desc).tobytes()
+            assert torch.equal(x, before)  # dev_in left intact
+    finally:
+        comm.close()
+
+
+def test_sort_dist_native_capacity(B):
+    import ctypes
+    comm = B.Comm.local()
+    try:
+        x = gen(torch.int64, 10_000, 77)
+        out = torch.empty(100, dtype=torch.int64, device="cuda")
+        n_out = ctypes.c_uint64(0)
+        st = B.lib.bsort_sort_dist(8, ctypes.c_void_p(x.data_ptr()), x.numel(), ctypes.c_void_p(out.data_ptr()),
+                                   100, ctypes.byref(n_out), 0, comm._h, None)
+        torch.cuda.synchronize()
+        assert st == 7 and n_out.value == 10_000
+        got = B.sort_dist_native(x, comm, capacity=100)  # retried with the exact size
+        torch.cuda.synchronize()
+        assert host(got).tobytes() == oracle.sort_native(host(x)).tobytes()
+        assert B.lib.bsort_sort_dist(3, ctypes.c_void_p(x.data_ptr()), 10, ctypes.c_void_p(out.data_ptr()),
+                                     100, None, 0, comm._h, None) == 2  # i16: unsupported here
+    finally:
+        comm.close()
+
+
+def test_sort_dist_native_torch_group(B):
+    """Comm over a torch.distributed group (unique id broadcast by the group)."""
+    import torch.distributed as dist
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(_free_port()))
+    dist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device("cuda:0"))
+    try:
+        comm = B.Comm()
+        x = W.make("cfg5", "cuda", n=200_001, dtype=torch.float64)
+        out = B.sort_dist_native(x, comm)
+        torch.cuda.synchronize()
+        assert host(out).tobytes() == oracle.sort_native(host(x)).tobytes()
+        comm.close()
+    finally:
+        dist.destroy_process_group()
