@@ -82,7 +82,7 @@ void run(const U* in, U* out, uint64_t n, const unsigned long long* bases, uint3
     CK(cudaMemset(counter, 0, 4));
     CK(cudaMemset(gcount, 0, 256 * 8));
     CK(cudaEventRecord(a));
-    kern<<<grid, THREADS, L::bytes>>>(in, out, n, DigitF{}, bases, lookback, gcount, counter, (uint32_t)tiles, nullptr, 0);
+    kern<<<grid, THREADS, L::bytes>>>(in, out, n, DigitF{}, bases, lookback, gcount, counter, (uint32_t)tiles, nullptr, 0, KvPtrs{});
     CK(cudaEventRecord(b));
     CK(cudaEventSynchronize(b));
     CK(cudaGetLastError());
@@ -148,17 +148,10 @@ void suite(uint64_t n) {
   // One pass on uniform keys with digit shift 0: RUN2 sees a single run (the fast path).
   if constexpr (sizeof(U) == 4) {
     run<U, 512, 16, 2, true, RANK_STABLE, 8>(in, out, n, bases, lookback, counter, gcount, ref, dbg);
-    run<U, 256, 16, 4, true, RANK_STABLE, 8>(in, out, n, bases, lookback, counter, gcount, ref, dbg);
-    run<U, 384, 16, 3, true, RANK_STABLE, 8>(in, out, n, bases, lookback, counter, gcount, ref, dbg);
-    run<U, 256, 24, 3, true, RANK_STABLE, 8>(in, out, n, bases, lookback, counter, gcount, ref, dbg);
     run<U, 512, 16, 2, true, RANK_RUN2, 8>(in, out, n, bases, lookback, counter, gcount, ref, dbg);
-    run<U, 256, 16, 4, true, RANK_RUN2, 8>(in, out, n, bases, lookback, counter, gcount, ref, dbg);
-    run<U, 384, 16, 3, true, RANK_RUN2, 8>(in, out, n, bases, lookback, counter, gcount, ref, dbg);
     run<U, 512, 16, 2, true, RANK_UNSTABLE, 8>(in, out, n, bases, lookback, counter, gcount, ref, dbg);
-    run<U, 256, 16, 4, true, RANK_UNSTABLE, 8>(in, out, n, bases, lookback, counter, gcount, ref, dbg);
   } else {
     run<U, 384, 12, 2, true, RANK_STABLE, 8>(in, out, n, bases, lookback, counter, gcount, ref, dbg);
-    run<U, 256, 12, 3, true, RANK_STABLE, 8>(in, out, n, bases, lookback, counter, gcount, ref, dbg);
     run<U, 384, 12, 2, true, RANK_RUN2, 8>(in, out, n, bases, lookback, counter, gcount, ref, dbg);
     run<U, 384, 12, 2, true, RANK_UNSTABLE, 8>(in, out, n, bases, lookback, counter, gcount, ref, dbg);
   }
