@@ -298,7 +298,19 @@ def bench_extra(B, dev, stream, args):
                                        "model_GBps": bpk * x.numel() / (ms / 1e3) / 1e9,
                                        "model_bytes_per_key": bpk,
                                        "frac_of_hbm": bpk * x.numel() / (ms / 1e3) / 1e9 / hb}
-    del x, kw, vw, iota
+    del kw, vw, iota
+    # §8 N4: in-place mode (default chunk) on the cfg3 keys: time and scratch vs bsort_sort's
+    work = torch.empty_like(x)
+    restore = lambda: work.copy_(x)  # noqa: E731
+    run = lambda: B.sort_inplace_(work)  # noqa: E731
+    restore(); run(); torch.cuda.synchronize()  # noqa: E702
+    t = time_steps(run, restore, 3, stream)
+    ms = statistics.median(t)
+    out["cfg3_f32_inplace_2^30"] = {"keys_per_s": x.numel() / (ms / 1e3), "ms": ms,
+                                    "scratch_bytes": B.inplace_workspace_bytes(x.dtype, x.numel()),
+                                    "scratch_bytes_sort": B.workspace_bytes(x.dtype, x.numel()),
+                                    "note": "host-synchronising per partition; default chunk max(2^22, n/32)"}
+    del x, work
     torch.cuda.empty_cache()
     return out
 

@@ -109,6 +109,21 @@ bsort_status_t bsort_sort_pairs_ws(bsort_dtype_t dtype, void* dev_keys, uint32_t
 bsort_status_t bsort_sort_pairs(bsort_dtype_t dtype, void* dev_keys, uint32_t* dev_values, uint64_t n,
                                 bsort_direction_t direction, void* stream);
 
+/* ------------------------------------------------ in-place mode / hybrid
+ * Sorts like bsort_sort() (same order, same result bit for bit) with O(n/128 + SMs*128 KiB)
+ * scratch plus the LSD scratch of `chunk_keys` keys, instead of an n-key buffer: 256-way MSD
+ * partitions IN PLACE (the paper's Algorithm 1 generalised from one bit to one 8-bit digit,
+ * P:151-157, recursing MSD-first like Algorithm 2; Theorem 5's in-place property,
+ * P:761-775), until every group of consecutive buckets holds at most chunk_keys keys; each group
+ * is then sorted by the one-sweep LSD path (the paper's hybrid idea).
+ * chunk_keys = 0 picks max(2^22, n/32) (capped at n).  8/16-bit keys use the counting path, which
+ * is in place already.  Blocks the host once per partition (bucket sizes decide the recursion).
+ * Workspace: bsort_inplace_workspace_bytes(dtype, n, chunk_keys) bytes, 256-byte aligned. */
+size_t bsort_inplace_workspace_bytes(bsort_dtype_t dtype, uint64_t n, uint64_t chunk_keys);
+bsort_status_t bsort_sort_inplace_ws(bsort_dtype_t dtype, void* dev_keys, uint64_t n,
+                                     bsort_direction_t direction, uint64_t chunk_keys, void* workspace,
+                                     size_t workspace_bytes, void* stream);
+
 /* ------------------------------------------------------ multi-GPU building blocks (MSD)
  * The distributed sort (BASELINE.json cfg5) is an MSD range partition on the top 16 bits of
  * the transformed key (the paper's sign -> exponent -> mantissa hierarchy, makes

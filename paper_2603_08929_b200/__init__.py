@@ -23,7 +23,7 @@ import torch
 from . import _lib
 from ._lib import BsortError, check, lib
 
-__all__ = ["sort_", "sort", "sort_pairs_", "argsort", "Sorter", "sort_host", "sort_dist", "dtype_code", "workspace_bytes",
+__all__ = ["sort_", "sort", "sort_inplace_", "inplace_workspace_bytes", "sort_pairs_", "argsort", "Sorter", "sort_host", "sort_dist", "dtype_code", "workspace_bytes",
            "top_hist", "splitters", "send_counts", "partition", "partition_remote", "refine_hist",
            "class_hist", "partition_classes", "Comm", "sort_dist_native", "profile",
            "launch_count",
@@ -90,6 +90,27 @@ def sort_(t: torch.Tensor, descending: bool = False) -> torch.Tensor:
 
 def sort(t: torch.Tensor, descending: bool = False) -> torch.Tensor:
     return sort_(t.clone(), descending)
+
+
+def inplace_workspace_bytes(dtype: torch.dtype, n: int, chunk: int = 0) -> int:
+    return int(lib.bsort_inplace_workspace_bytes(dtype_code(dtype), n, chunk))
+
+
+def sort_inplace_(t: torch.Tensor, descending: bool = False, chunk: int = 0) -> torch.Tensor:
+    """§8 N4 in-place mode: same result as ``sort_`` with O(n/128 + chunk) scratch instead of n
+    keys (256-way in-place MSD partitions, then the LSD path on bucket groups of <= chunk keys;
+    chunk=0: max(2^22, n/32)).  Synchronises the host once per partition."""
+    _check_tensor(t)
+    code = dtype_code(t.dtype)
+    n = t.numel()
+    if n <= 1:
+        return t
+    wsb = int(lib.bsort_inplace_workspace_bytes(code, n, chunk))
+    ws = _workspace(wsb, t.device)
+    check(lib.bsort_sort_inplace_ws(code, ctypes.c_void_p(t.data_ptr()), n, int(bool(descending)), chunk,
+                                    ctypes.c_void_p(ws.data_ptr()), wsb, _stream_ptr(t.device)),
+          "bsort_sort_inplace_ws")
+    return t
 
 
 def sort_pairs_(keys: torch.Tensor, values: torch.Tensor, descending: bool = False):

@@ -27,6 +27,7 @@ ERROR_CAPACITY = 7
 EXPORTS = [
     "bsort_workspace_bytes", "bsort_sort", "bsort_sort_ws", "bsort_sort_host",
     "bsort_pairs_workspace_bytes", "bsort_sort_pairs_ws", "bsort_sort_pairs",
+    "bsort_inplace_workspace_bytes", "bsort_sort_inplace_ws",
     "bsort_dist_top_hist", "bsort_dist_splitters", "bsort_dist_send_counts",
     "bsort_dist_partition_workspace_bytes", "bsort_dist_partition", "bsort_dist_partition_remote",
     "bsort_dist_refine_hist", "bsort_dist_class_hist", "bsort_dist_class_partition_workspace_bytes",
@@ -67,6 +68,8 @@ def _load():
         "bsort_pairs_workspace_bytes": (sz, [i32, u64]),
         "bsort_sort_pairs_ws": (i32, [i32, vp, vp, u64, i32, vp, sz, vp]),
         "bsort_sort_pairs": (i32, [i32, vp, vp, u64, i32, vp]),
+        "bsort_inplace_workspace_bytes": (sz, [i32, u64, u64]),
+        "bsort_sort_inplace_ws": (i32, [i32, vp, u64, i32, u64, vp, sz, vp]),
         "bsort_dist_top_hist": (i32, [i32, vp, u64, i32, vp, vp]),
         "bsort_dist_splitters": (i32, [u64p, i32, u32p]),
         "bsort_dist_send_counts": (i32, [u64p, u32p, i32, u64p]),

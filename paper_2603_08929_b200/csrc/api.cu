@@ -134,6 +134,24 @@ bsort_status_t bsort_sort_ws(bsort_dtype_t dtype, void* dev_keys, uint64_t n, bs
   return sort_ws_impl(di, dev_keys, n, direction, workspace, workspace_bytes_, (cudaStream_t)stream);
 }
 
+size_t bsort_inplace_workspace_bytes(bsort_dtype_t dtype, uint64_t n, uint64_t chunk_keys) {
+  DtypeInfo di;
+  if (!dtype_info(dtype, &di)) return 0;
+  return inplace_workspace_bytes(di.bytes, n, chunk_keys);
+}
+
+bsort_status_t bsort_sort_inplace_ws(bsort_dtype_t dtype, void* dev_keys, uint64_t n, bsort_direction_t direction,
+                                     uint64_t chunk_keys, void* workspace, size_t workspace_bytes_, void* stream) {
+  DtypeInfo di;
+  bsort_status_t st = validate(dtype, dev_keys, n, direction, &di);
+  if (st != BSORT_SUCCESS) return st;
+  if (n <= 1) return BSORT_SUCCESS;
+  if (workspace_bytes_ < inplace_workspace_bytes(di.bytes, n, chunk_keys)) return BSORT_ERROR_WORKSPACE_TOO_SMALL;
+  if (workspace == nullptr || !aligned_to(workspace, 256)) return BSORT_ERROR_INVALID_ARGUMENT;
+  return inplace_sort(di, dev_keys, n, direction == BSORT_DESCENDING, chunk_keys, workspace, workspace_bytes_,
+                      (cudaStream_t)stream);
+}
+
 bsort_status_t bsort_sort(bsort_dtype_t dtype, void* dev_keys, uint64_t n, bsort_direction_t direction,
                           void* stream) {
   DtypeInfo di;

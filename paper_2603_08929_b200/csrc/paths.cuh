@@ -21,6 +21,12 @@ size_t lsd_workspace_bytes(int bytes, uint64_t n, bool kv = false);
 bsort_status_t lsd_sort(const DtypeInfo& di, void* keys, uint32_t* vals, uint64_t n, bool desc, void* ws,
                         size_t ws_bytes, cudaStream_t s);
 
+// §8 N4: in-place MSD partition(s) + LSD of bucket groups of at most `chunk` keys (inplace.cu).
+uint64_t inplace_default_chunk(uint64_t n);
+size_t inplace_workspace_bytes(int bytes, uint64_t n, uint64_t chunk);
+bsort_status_t inplace_sort(const DtypeInfo& di, void* keys, uint64_t n, bool desc, uint64_t chunk, void* ws,
+                            size_t ws_bytes, cudaStream_t s);
+
 // a7/a9: distributed building blocks.
 bsort_status_t dist_top_hist(const DtypeInfo& di, const void* keys, uint64_t n, bool desc,
                              uint64_t* dev_hist, cudaStream_t s);

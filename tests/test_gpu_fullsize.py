@@ -146,3 +146,15 @@ def test_cfg5_local_full(B, dtype):
     check_sorted(y, False)
     assert fingerprint(y) == fp
     check_order_stats(x.cpu().numpy(), y, False, samples=3)
+
+
+def test_cfg3_full_inplace(B):
+    """§8 N4 at full size: the in-place mode (default chunk) on 2^30 cfg3 keys."""
+    x = W.make("cfg3", "cuda")
+    fp = fingerprint(x)
+    y = x.clone()
+    B.sort_inplace_(y)
+    torch.cuda.synchronize()
+    check_sorted(y, False)
+    assert fingerprint(y) == fp
+    check_order_stats(x.cpu().numpy(), y, False, samples=3)
