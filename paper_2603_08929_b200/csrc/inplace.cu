@@ -37,11 +37,11 @@
 namespace bsort {
 namespace {
 
-constexpr int IP_THREADS = 512;
+constexpr int IP_THREADS = 1024;
 constexpr int IP_ITEMS = 8;
 constexpr int IP_TILE = IP_THREADS * IP_ITEMS;
 constexpr int IP_BLOCK_BYTES = 512;
-constexpr uint32_t F_EMPTY = 0, F_UNPROC = 1, F_READING = 2, F_FREE = 3, F_PLACED = 4;
+constexpr uint32_t F_EMPTY = 0, F_UNPROC = 1, F_READING = 2, F_FREE = 3;
 
 template <typename U> constexpr int ip_block() { return IP_BLOCK_BYTES / (int)sizeof(U); }
 
@@ -53,7 +53,10 @@ struct ShiftDigit {
   }
 };
 
-// P1.  grid = number of stripes; dynamic smem = 256 * B keys.
+// P1.  grid = number of stripes; dynamic smem = 256 * B keys of bucket buffers + one tile.
+// Per tile: rank by shared atomics, restage the tile bucket-sorted, then every block that a
+// bucket completes (its buffered keys + the first of its new keys) is copied out by one warp as
+// 512 contiguous bytes; the rest of the bucket's new keys refill its buffer.
 template <int KIND, bool DESC, typename U>
 __global__ void __launch_bounds__(IP_THREADS, 1)
     k_ip_classify(U* __restrict__ a, uint64_t n, int shift, uint64_t stripe_len, U* __restrict__ ovf,
@@ -63,7 +66,10 @@ __global__ void __launch_bounds__(IP_THREADS, 1)
   constexpr int NW = IP_THREADS / 32;
   extern __shared__ __align__(16) unsigned char ip_smem[];
   U* sbuf = reinterpret_cast<U*>(ip_smem);  // [256][B]
-  __shared__ uint32_t cbuf[256], cnt[256], nbk[256], boff[256], nbsum[256], tcount[256];
+  U* ts = sbuf + 256 * B;                    // [IP_TILE] the tile, bucket-sorted
+  __shared__ uint32_t cbuf[256], cnt[256], nbk[256], boff[256], toff[256], nbsum[256], tcount[256];
+  constexpr int MAXBLK = (IP_TILE + 256 * (B - 1)) / B;  // blocks one tile can complete
+  __shared__ uint8_t blkmap[MAXBLK];                      // completed block -> its bucket
   __shared__ uint32_t wt[NW + 1];
   __shared__ uint32_t tot_blocks;
   const ShiftDigit<KIND, DESC, U> dg{shift};
@@ -77,19 +83,29 @@ __global__ void __launch_bounds__(IP_THREADS, 1)
     tcount[t] = 0;
   }
   uint64_t wp = lo;
-  for (uint64_t ts = lo; ts < hi; ts += IP_TILE) {
+  // register double buffer: tile tb+IP_TILE is loaded while tile tb is processed (this
+  // iteration's writes end at or before tb+IP_TILE, the next one's are ordered after these
+  // loads by the barriers that follow their use in ranking)
+  U nxt[IP_ITEMS];
+  auto load = [&](uint64_t tb) {
+#pragma unroll
+    for (int k = 0; k < IP_ITEMS; ++k) {
+      const uint64_t i = tb + warp * (32 * IP_ITEMS) + k * 32 + lane;
+      nxt[k] = i < hi ? a[i] : U(0);
+    }
+  };
+  if (lo < hi) load(lo);
+  for (uint64_t tb = lo; tb < hi; tb += IP_TILE) {
     U keys[IP_ITEMS];
     uint32_t info[IP_ITEMS];
 #pragma unroll
-    for (int k = 0; k < IP_ITEMS; ++k) {
-      const uint64_t i = ts + warp * (32 * IP_ITEMS) + k * 32 + lane;
-      keys[k] = i < hi ? a[i] : U(0);
-    }
+    for (int k = 0; k < IP_ITEMS; ++k) keys[k] = nxt[k];
+    if (tb + IP_TILE < hi) load(tb + IP_TILE);
     if (t < 256) cnt[t] = 0;
-    __syncthreads();  // tile loaded by everyone (the writes below may land on it); cnt zeroed
+    __syncthreads();  // tile loaded by everyone (this iteration's writes may land on it); cnt zeroed
 #pragma unroll
     for (int k = 0; k < IP_ITEMS; ++k) {
-      const uint64_t i = ts + warp * (32 * IP_ITEMS) + k * 32 + lane;
+      const uint64_t i = tb + warp * (32 * IP_ITEMS) + k * 32 + lane;
       if (i < hi) {
         const uint32_t d = dg(keys[k]);
         info[k] = d | (atomicAdd(&cnt[d], 1u) << 8);
@@ -98,38 +114,53 @@ __global__ void __launch_bounds__(IP_THREADS, 1)
       }
     }
     __syncthreads();
-    uint32_t nb = 0;
+    // one scan of {blocks completed : 16 | tile count : 16} per bucket
+    uint32_t packed = 0;
     if (t < 256) {
-      nb = (cbuf[t] + cnt[t]) / (uint32_t)B;
+      const uint32_t nb = (cbuf[t] + cnt[t]) / (uint32_t)B;
       nbk[t] = nb;
       nbsum[t] += nb;
       tcount[t] += cnt[t];
+      packed = (nb << 16) | cnt[t];
     }
     uint32_t total = 0;
-    const uint32_t ex = block_exclusive_scan<IP_THREADS>(nb, wt, &total);
-    if (t < 256) boff[t] = ex;
-    if (t == 0) tot_blocks = total;
+    const uint32_t ex = block_exclusive_scan<IP_THREADS>(packed, wt, &total);
+    if (t < 256) {
+      boff[t] = ex >> 16;
+      toff[t] = ex & 0xFFFFu;
+    }
+    if (t == 0) tot_blocks = total >> 16;
     __syncthreads();
-    // buffered keys of buckets that complete a block: they open that bucket's first block
-    for (uint32_t b = warp; b < 256; b += NW)
-      if (nbk[b] > 0)
-        for (uint32_t v = lane; v < cbuf[b]; v += 32) a[wp + (uint64_t)boff[b] * B + v] = sbuf[b * B + v];
+#pragma unroll
+    for (int k = 0; k < IP_ITEMS; ++k)
+      if (info[k] != 0xFFFFFFFFu) ts[toff[info[k] & 0xFFu] + (info[k] >> 8)] = keys[k];
+    if (t < 256)
+      for (uint32_t j = 0; j < nbk[t]; ++j) blkmap[boff[t] + j] = (uint8_t)t;
     __syncthreads();
+    // completed blocks, one warp per block: 512 contiguous bytes at wp + g*B
+    const uint32_t nblk = tot_blocks;
+    for (uint32_t g = warp; g < nblk; g += NW) {
+      const uint32_t d = blkmap[g], j = g - boff[d], c = cbuf[d];
+#pragma unroll
+      for (int e = 0; e < B / 32; ++e) {
+        const uint32_t v = j * B + e * 32 + lane;
+        a[wp + (uint64_t)g * B + e * 32 + lane] = v < c ? sbuf[d * B + v] : ts[toff[d] + (v - c)];
+      }
+    }
+    __syncthreads();
+    // the rest of each bucket's new keys go to its buffer
 #pragma unroll
     for (int k = 0; k < IP_ITEMS; ++k) {
       if (info[k] != 0xFFFFFFFFu) {
         const uint32_t d = info[k] & 0xFFu;
         const uint32_t v = cbuf[d] + (info[k] >> 8);
         const uint32_t full = nbk[d] * (uint32_t)B;
-        if (v < full)
-          a[wp + (uint64_t)boff[d] * B + v] = keys[k];
-        else
-          sbuf[d * B + (v - full)] = keys[k];
+        if (v >= full) sbuf[d * B + (v - full)] = keys[k];
       }
     }
     __syncthreads();
     if (t < 256) cbuf[t] = cbuf[t] + cnt[t] - nbk[t] * (uint32_t)B;
-    wp += (uint64_t)tot_blocks * B;
+    wp += (uint64_t)nblk * B;
   }
   __syncthreads();
   if (t < 256) {
@@ -168,7 +199,12 @@ __device__ __forceinline__ void slot_write(U* a, U* tail, uint64_t n, uint64_t j
   }
 }
 
-// P2.  One warp = one worker.
+// P2.  One warp = one worker; slots are handed out 32 at a time.  Flag protocol: UNPROC (a
+// block not read yet) -> READING (claimed by the warp that will read it); a warp that read a
+// SOURCE slot marks it FREE, because the warp that later claims that slot as a destination must
+// not overwrite it before the read completed.  A destination slot that its claimer read itself
+// needs no mark (nobody else targets it).  The read of a destination is issued together with the
+// CAS that claims it: an UNPROC slot is never written, so the data is valid whenever the CAS wins.
 template <int KIND, bool DESC, typename U>
 __global__ void __launch_bounds__(256)
     k_ip_permute(U* __restrict__ a, uint64_t n, int shift, uint32_t* flags, uint64_t nslots,
@@ -178,53 +214,50 @@ __global__ void __launch_bounds__(256)
   const ShiftDigit<KIND, DESC, U> dg{shift};
   const uint32_t lane = threadIdx.x & 31;
   for (;;) {
-    unsigned long long j = 0;
-    if (lane == 0) j = atomicAdd(next_slot, 1ull);
-    j = __shfl_sync(0xFFFFFFFFu, j, 0);
-    if (j >= nslots) break;
-    uint32_t got = 0;
-    if (lane == 0) got = atomicCAS(&flags[j], F_UNPROC, F_READING) == F_UNPROC;
-    if (!__shfl_sync(0xFFFFFFFFu, got, 0)) continue;
-    U v[B / 32];
-    slot_read<U, B>(a, tail, n, j, v);
-    uint32_t bkt = dg(__shfl_sync(0xFFFFFFFFu, v[0], 0));
-    __syncwarp();
-    __threadfence();
-    if (lane == 0) atomicExch(&flags[j], F_FREE);
-    for (;;) {  // carry block v (bucket bkt) to its next destination slot
-      unsigned long long d = 0;
-      uint32_t prev = 0;
-      if (lane == 0) {
-        d = dstart[bkt] + atomicAdd(&wcnt[bkt], 1ull);
-        prev = atomicCAS(&flags[d], F_UNPROC, F_READING);
-      }
-      d = __shfl_sync(0xFFFFFFFFu, d, 0);
-      prev = __shfl_sync(0xFFFFFFFFu, prev, 0);
-      if (prev == F_UNPROC) {  // unread block there: take it along
-        U w[B / 32];
-        slot_read<U, B>(a, tail, n, d, w);
-        const uint32_t nb = dg(__shfl_sync(0xFFFFFFFFu, w[0], 0));
-        __syncwarp();
-        slot_write<U, B>(a, tail, n, d, v);
-        __threadfence();
-        __syncwarp();
-        if (lane == 0) atomicExch(&flags[d], F_PLACED);
-#pragma unroll
-        for (int k = 0; k < B / 32; ++k) v[k] = w[k];
-        bkt = nb;
-        continue;
-      }
-      if (prev == F_READING) {  // another warp is reading it: wait until it is free
-        if (lane == 0)
-          while (atomicAdd(&flags[d], 0u) != F_FREE) __nanosleep(64);
-        __syncwarp();
-        __threadfence();
-      }
-      slot_write<U, B>(a, tail, n, d, v);
-      __threadfence();
+    unsigned long long base = 0;
+    if (lane == 0) base = atomicAdd(next_slot, 32ull);
+    base = __shfl_sync(0xFFFFFFFFu, base, 0);
+    if (base >= nslots) break;
+    const uint64_t mine = base + lane;
+    uint32_t cand = __ballot_sync(0xFFFFFFFFu, mine < nslots && __ldcg(&flags[mine]) == F_UNPROC);
+    while (cand) {
+      const uint32_t l = __ffs(cand) - 1;
+      cand &= cand - 1;
+      const uint64_t j = base + l;
+      U v[B / 32];
+      slot_read<U, B>(a, tail, n, j, v);  // speculative: used only if the claim succeeds
+      uint32_t got = 0;
+      if (lane == 0) got = atomicCAS(&flags[j], F_UNPROC, F_READING) == F_UNPROC;
+      if (!__shfl_sync(0xFFFFFFFFu, got, 0)) continue;
+      uint32_t bkt = dg(__shfl_sync(0xFFFFFFFFu, v[0], 0));
+      __threadfence();  // our reads of slot j are complete (their values are in use above)
       __syncwarp();
-      if (lane == 0) atomicExch(&flags[d], F_PLACED);
-      break;
+      if (lane == 0) atomicExch(&flags[j], F_FREE);
+      for (;;) {  // carry block v (bucket bkt) to its next destination slot
+        unsigned long long d = 0;
+        if (lane == 0) d = dstart[bkt] + atomicAdd(&wcnt[bkt], 1ull);
+        d = __shfl_sync(0xFFFFFFFFu, d, 0);
+        U w[B / 32];
+        slot_read<U, B>(a, tail, n, d, w);  // speculative, as above
+        uint32_t prev = 0;
+        if (lane == 0) prev = atomicCAS(&flags[d], F_UNPROC, F_READING);
+        prev = __shfl_sync(0xFFFFFFFFu, prev, 0);
+        if (prev == F_UNPROC) {  // an unread block: take it along, put ours in its place
+          const uint32_t nb = dg(__shfl_sync(0xFFFFFFFFu, w[0], 0));
+          slot_write<U, B>(a, tail, n, d, v);
+#pragma unroll
+          for (int k = 0; k < B / 32; ++k) v[k] = w[k];
+          bkt = nb;
+          continue;
+        }
+        if (prev == F_READING) {  // a source being read by another warp: wait until free
+          if (lane == 0)
+            while (atomicAdd(&flags[d], 0u) != F_FREE) __nanosleep(32);
+          __syncwarp();
+        }
+        slot_write<U, B>(a, tail, n, d, v);
+        break;
+      }
     }
   }
 }
@@ -324,7 +357,7 @@ bsort_status_t ip_partition(U* a, uint64_t n, int shift, char* ws, const IpLayou
   const uint64_t grid = (n + stripe_len - 1) / stripe_len;
   static bool attr = false;
   auto k1 = k_ip_classify<KIND, DESC, U>;
-  const int smem = 256 * IP_BLOCK_BYTES;
+  const int smem = 256 * IP_BLOCK_BYTES + IP_TILE * (int)sizeof(U);
   if (!attr) {
     BSORT_CUDA(cudaFuncSetAttribute(k1, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
     attr = true;
