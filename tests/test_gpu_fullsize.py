@@ -158,3 +158,27 @@ def test_cfg3_full_inplace(B):
     check_sorted(y, False)
     assert fingerprint(y) == fp
     check_order_stats(x.cpu().numpy(), y, False, samples=3)
+
+
+def test_beyond_2_30_keys_f32(B):
+    """n > 2^30: 64-bit look-back descriptors and counts (32-bit ones cover n <= 2^30 only)."""
+    n = (1 << 30) + (1 << 20) + 3
+    x = W.make("cfg3", "cuda", n=n)
+    fp = fingerprint(x)
+    y = sort_like_bench(B, x, True)
+    check_sorted(y, True)
+    assert fingerprint(y) == fp
+    check_order_stats(x.cpu().numpy(), y, True, samples=2)
+
+
+def test_beyond_2_32_keys_u8(B):
+    """Counting path with one bin holding more than 2^32 keys (64-bit global counts)."""
+    n = (1 << 32) + 5
+    x = torch.full((n,), 200, dtype=torch.uint8, device="cuda")
+    x[:3] = 7
+    x[-2:] = 255
+    B.sort_(x)
+    torch.cuda.synchronize()
+    assert int(x[:3].to(torch.int32).sum()) == 21 and int(x[3].item()) == 200
+    assert int(x[-3].item()) == 200 and int(x[-2:].to(torch.int32).sum()) == 510
+    assert bool((x[3:-2] == 200).all())
