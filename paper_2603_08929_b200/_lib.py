@@ -9,7 +9,8 @@ import ctypes
 import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libbsort.so")
+# BSORT_LIB: an alternative build of the same library (experiments); default the in-tree one
+LIB_PATH = os.environ.get("BSORT_LIB") or os.path.join(_HERE, "libbsort.so")
 
 # bsort_dtype_t
 U8, I8, U16, I16, U32, I32, F32, U64, I64, F64, F16, BF16 = range(12)
