@@ -322,6 +322,18 @@ def nvlink_peak():
     return 770.0, "B200_PROFILING.md measured peer copy 770 GB/s per direction (900 nominal)"
 
 
+_JSON_FD = None  # multi-GPU runs: the real stdout (fd 1 is pointed at stderr meanwhile)
+
+
+def emit(text: str):
+    """Write the result line to the real stdout (NCCL prints its version banner on fd 1 at the
+    first communicator, whatever NCCL_DEBUG says; the contract is ONE JSON line on stdout)."""
+    if _JSON_FD is None:
+        print(text, flush=True)
+    else:
+        os.write(_JSON_FD, (text + "\n").encode())
+
+
 def bench_multi(args, B):
     """N > 1: one step = sort_dist of 2^30 cfg3-distributed f32 keys per rank (weak scaling)."""
     import torch.distributed as dist
@@ -372,6 +384,7 @@ def bench_multi(args, B):
 
     # end to end through the public API: pinned host keys -> H2D -> sort_dist -> D2H of the shard
     host = pristine.cpu().pin_memory()
+    host_out = torch.empty(2 * n, dtype=pristine.dtype).pin_memory()  # shard ~ n keys per rank
     e_times, out_bytes = [], 0
     for i in range(2):
         dist.barrier()
@@ -380,7 +393,10 @@ def bench_multi(args, B):
         ea.record(stream)
         work.copy_(host, non_blocking=True)
         shard = B.sort_dist(work, exact=args.exact)
-        res = shard.cpu()
+        if shard.numel() > host_out.numel():
+            host_out = torch.empty(shard.numel(), dtype=shard.dtype).pin_memory()
+        res = host_out[:shard.numel()]
+        res.copy_(shard, non_blocking=True)
         eb.record(stream)
         torch.cuda.synchronize()
         out_bytes = res.numel() * res.element_size()
@@ -415,7 +431,7 @@ def bench_multi(args, B):
             "gpu_launches": launches,
             "clocks": clk.summary(),
         }
-        print(json.dumps(line), flush=True)
+        emit(json.dumps(line))
 
 
 # ------------------------------------------------------------------------ reference arm
@@ -474,7 +490,19 @@ def main():
     import paper_2603_08929_b200 as B
     world = int(os.environ.get("WORLD_SIZE", "1"))
     if world > 1 or args.force_dist:
+        global _JSON_FD
+        sys.stdout.flush()
+        _JSON_FD = os.dup(1)
+        os.dup2(2, 1)
         import torch.distributed as dist
+        if "RANK" not in os.environ:  # --force-dist outside torchrun: a one-rank group
+            import socket
+            sk = socket.socket()
+            sk.bind(("127.0.0.1", 0))
+            port = sk.getsockname()[1]
+            sk.close()
+            os.environ.update(RANK="0", WORLD_SIZE="1", LOCAL_RANK="0", MASTER_ADDR="127.0.0.1",
+                              MASTER_PORT=str(port))
         local = int(os.environ.get("LOCAL_RANK", "0"))
         torch.cuda.set_device(local)
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
