@@ -322,6 +322,30 @@ def nvlink_peak():
     return 770.0, "B200_PROFILING.md measured peer copy 770 GB/s per direction (900 nominal)"
 
 
+def a2a_microbench(dev, bytes_per_pair=1 << 28, reps=5):
+    """NCCL all-to-all of `bytes_per_pair` per rank pair on this box; returns the
+    per-rank egress GB/s (max-over-ranks time), or None at world size 1."""
+    import torch.distributed as dist
+    world = dist.get_world_size()
+    if world < 2:
+        return None
+    send = torch.empty(bytes_per_pair * world, dtype=torch.uint8, device=dev)
+    recv = torch.empty_like(send)
+    dist.all_to_all_single(recv, send)
+    torch.cuda.synchronize()
+    dist.barrier()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record()
+    for _ in range(reps):
+        dist.all_to_all_single(recv, send)
+    b.record()
+    torch.cuda.synchronize()
+    t = torch.tensor([a.elapsed_time(b) / reps], dtype=torch.float64, device=dev)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    del send, recv
+    return bytes_per_pair * (world - 1) / (t.item() / 1e3) / 1e9
+
+
 _JSON_FD = None  # multi-GPU runs: the real stdout (fd 1 is pointed at stderr meanwhile)
 
 
@@ -404,9 +428,14 @@ def bench_multi(args, B):
             e_times.append(ea.elapsed_time(eb))
     te = torch.tensor([max(e_times)], dtype=torch.float64, device=dev)
     dist.all_reduce(te, op=dist.ReduceOp.MAX)
+    del host, host_out
+    a2a_gbs = a2a_microbench(dev)  # collective; None at world size 1
     total = n * world
     if rank == 0:
         nv_peak, nv_src = nvlink_peak()
+        if a2a_gbs is not None:
+            nv_peak, nv_src = a2a_gbs, ("measured here: NCCL all_to_all_single, 256 MiB per rank pair, "
+                                        "per-rank egress, max over ranks")
         per_rank_bytes = a2a_bytes / max(1, args.steps)
         achieved = per_rank_bytes / (a2a_max_ms / 1e3) / 1e9 if a2a_max_ms > 0 else None
         line = {
