@@ -269,6 +269,18 @@ def bench_extra(B, dev, stream, args):
         del work, s
 
     measure("cfg1_i32_2^20_asc", W.make("cfg1", dev), False, 36)
+    # cfg1 is launch/latency-bound: the same sort replayed as one CUDA graph
+    x = W.make("cfg1", dev)
+    work = x.clone()
+    s = B.Sorter(x.dtype, x.numel(), dev)
+    g = s.graph(work)
+    restore = lambda: work.copy_(x)  # noqa: E731
+    restore(); g.replay(); torch.cuda.synchronize()  # noqa: E702
+    t = time_steps(g.replay, restore, 20, stream)
+    ms = statistics.median(t)
+    out["cfg1_i32_2^20_asc_cuda_graph"] = {"keys_per_s": x.numel() / (ms / 1e3), "ms": ms,
+                                           "note": "Sorter.graph(): the whole path as one graph replay"}
+    del x, work, s, g
     for dt, nm in ((torch.uint8, "u8"), (torch.int8, "i8"), (torch.int16, "i16")):
         x = W.make("cfg2", dev, dtype=dt)
         bpk = 2 * x.element_size()

@@ -159,6 +159,17 @@ class Sorter:
                                 self.ws_bytes, _stream_ptr(t.device)), "bsort_sort_ws")
         return t
 
+    def graph(self, t: torch.Tensor, descending: bool = False) -> "torch.cuda.CUDAGraph":
+        """Capture the sort of ``t`` (fixed address and size) into a CUDA graph: every launch of
+        the path (memsets, histogram, plan, passes, final copy) is a graph node, so a replay
+        costs one launch.  ``g.replay()`` re-sorts whatever ``t`` holds at that time."""
+        self(t, descending)  # warm-up outside capture (one-time function attributes)
+        torch.cuda.synchronize(t.device)
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g):
+            self(t, descending)
+        return g
+
     def sort_host(self, host: torch.Tensor, dev_buf: torch.Tensor, descending: bool = False):
         """Enqueue H2D(host -> dev_buf), sort, D2H(dev_buf -> host) on the current stream."""
         if host.is_cuda or not host.is_contiguous() or host.dtype != self.dtype:
