@@ -243,7 +243,37 @@ int bsort_comm_rank(bsort_comm_t comm);
 bsort_status_t bsort_sort_dist(bsort_dtype_t dtype, const void* dev_in, uint64_t n_local, void* dev_out,
                                uint64_t out_capacity, uint64_t* n_out, bsort_direction_t direction,
                                bsort_comm_t comm, void* stream);
+/* bsort_sort_dist with options.  flags: 0 = as bsort_sort_dist; BSORT_DIST_EXACT = exact
+ * splitting: rank r's shard is exactly floor((r+1)N/P) - floor(rN/P) keys whatever
+ * the key distribution (equal keys are split across ranks in rank order).  Exact splitting adds
+ * one key read + an all-reduce of m x 65536 u64 per refinement level (bsort_dist_exact_boundaries)
+ * and a class histogram + all-gather; it blocks the host once more per level. */
+#define BSORT_DIST_EXACT 1u
+bsort_status_t bsort_sort_dist_ex(bsort_dtype_t dtype, const void* dev_in, uint64_t n_local, void* dev_out,
+                                  uint64_t out_capacity, uint64_t* n_out, bsort_direction_t direction,
+                                  unsigned flags, bsort_comm_t comm, void* stream);
 int bsort_last_nccl_error(void);          /* raw ncclResult_t of the last NCCL failure (thread-local) */
+
+/* Host planning of exact splitting (pure host code, no device work; used by
+ * bsort_sort_dist_ex(BSORT_DIST_EXACT)).  bsort_dist_exact_boundaries: from the GLOBAL top-16-bit
+ * histogram (BSORT_DIST_BINS entries) of N keys of `key_bits` (32 or 64) bits, finds for every
+ * boundary r = 1..nranks-1 the transformed key K_r of global rank T_r = floor(r N / nranks) and
+ * quota_r = T_r - #{keys < K_r}, descending the key 16 bits at a time (the MSD digit order of
+ * P:427-433).  `refine(ctx, prefixes, m, prefix_bits, hist)` must fill hist (m * 65536 u64) with
+ * the GLOBAL next-16-bit histograms below the m strictly increasing prefixes (for example
+ * bsort_dist_refine_hist + an all-reduce) and return 0.  Outputs: values[0..*m) the distinct
+ * K's (increasing), idx[r-1] the index of K_r in values, quota[r-1], *levels the number of
+ * refine calls.  Arrays hold nranks-1 entries.  N == 0 with nranks > 1 is INVALID_ARGUMENT.
+ * bsort_dist_exact_send_counts: this rank's per-destination counts over its keys grouped by the
+ * 2m+1 classes (bsort_dist_partition_classes order), given every rank's class counts
+ * (class_counts_all[q * (2m+1) + c]): the keys equal to values[j] go left of boundary r in rank
+ * order, quota_r of them in total, so every shard ends exactly at global rank T_r. */
+typedef int (*bsort_refine_fn)(void* ctx, const uint64_t* prefixes, int m, int prefix_bits, uint64_t* hist);
+bsort_status_t bsort_dist_exact_boundaries(const uint64_t* host_global_hist, int nranks, int key_bits,
+                                           bsort_refine_fn refine, void* ctx, uint64_t* values, int* m,
+                                           int* idx, uint64_t* quota, int* levels);
+bsort_status_t bsort_dist_exact_send_counts(const uint64_t* class_counts_all, int nranks, int m, int rank,
+                                            const int* idx, const uint64_t* quota, uint64_t* send_counts);
 
 /* ----------------------------------------------------------------------- diagnostics */
 

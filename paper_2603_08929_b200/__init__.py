@@ -353,24 +353,26 @@ class Comm:
 
 
 def sort_dist_native(t: torch.Tensor, comm: Comm, descending: bool = False,
-                     capacity: int = None) -> torch.Tensor:
+                     capacity: int = None, exact: bool = False) -> torch.Tensor:
     """§8 b ``bsort_sort_dist``: the whole MSD path in one libbsort call over ``comm`` (NCCL).
     Returns this rank's shard (sorted); ``t`` is left intact.  Collective over comm's ranks.
     If some rank's shard exceeds ``capacity`` (default 2 x n_local + 65,536) every rank gets
-    BSORT_ERROR_CAPACITY and the call is retried once, collectively, with the exact sizes."""
+    BSORT_ERROR_CAPACITY and the call is retried once, collectively, with the exact sizes.
+    ``exact``: exact splitting (§8 N2) inside libbsort (bsort_sort_dist_ex, BSORT_DIST_EXACT)."""
     _check_tensor(t)
     n = t.numel()
     cap = capacity if capacity is not None else 2 * n + (1 << 16)
     for attempt in range(2):
         out = torch.empty(cap, dtype=t.dtype, device=t.device)
         n_out = ctypes.c_uint64(0)
-        st = lib.bsort_sort_dist(dtype_code(t.dtype), ctypes.c_void_p(t.data_ptr()), n,
-                                 ctypes.c_void_p(out.data_ptr()), cap, ctypes.byref(n_out),
-                                 int(bool(descending)), comm._h, _stream_ptr(t.device))
+        st = lib.bsort_sort_dist_ex(dtype_code(t.dtype), ctypes.c_void_p(t.data_ptr()), n,
+                                    ctypes.c_void_p(out.data_ptr()), cap, ctypes.byref(n_out),
+                                    int(bool(descending)), _lib.DIST_EXACT if exact else 0, comm._h,
+                                    _stream_ptr(t.device))
         if st == _lib.ERROR_CAPACITY and attempt == 0:
             cap = int(n_out.value)
             continue
-        check(st, "bsort_sort_dist")
+        check(st, "bsort_sort_dist_ex")
         return out[:int(n_out.value)]
     raise AssertionError("unreachable")
 

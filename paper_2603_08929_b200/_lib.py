@@ -34,10 +34,17 @@ EXPORTS = [
     "bsort_dist_refine_hist", "bsort_dist_class_hist", "bsort_dist_class_partition_workspace_bytes",
     "bsort_dist_partition_classes",
     "bsort_get_unique_id", "bsort_comm_init", "bsort_comm_destroy", "bsort_comm_size", "bsort_comm_rank",
-    "bsort_sort_dist", "bsort_last_nccl_error",
+    "bsort_sort_dist", "bsort_sort_dist_ex", "bsort_last_nccl_error",
+    "bsort_dist_exact_boundaries", "bsort_dist_exact_send_counts",
     "bsort_status_string", "bsort_last_cuda_error", "bsort_version", "bsort_launch_count",
     "bsort_profile_enable", "bsort_profile_read", "bsort_profile_kind_name",
 ]
+
+
+# bsort_refine_fn: int (*)(void* ctx, const uint64_t* prefixes, int m, int prefix_bits, uint64_t* hist)
+REFINE_FN = ctypes.CFUNCTYPE(ctypes.c_int, ctypes.c_void_p, ctypes.POINTER(ctypes.c_uint64), ctypes.c_int,
+                             ctypes.c_int, ctypes.POINTER(ctypes.c_uint64))
+DIST_EXACT = 1
 
 
 class BsortError(RuntimeError):
@@ -61,6 +68,7 @@ def _load():
     vp, u64, sz, i32 = ctypes.c_void_p, ctypes.c_uint64, ctypes.c_size_t, ctypes.c_int
     u64p = ctypes.POINTER(ctypes.c_uint64)
     u32p = ctypes.POINTER(ctypes.c_uint32)
+    i32p = ctypes.POINTER(ctypes.c_int)
     sig = {
         "bsort_workspace_bytes": (sz, [i32, u64]),
         "bsort_sort": (i32, [i32, vp, u64, i32, vp]),
@@ -87,6 +95,9 @@ def _load():
         "bsort_comm_size": (i32, [vp]),
         "bsort_comm_rank": (i32, [vp]),
         "bsort_sort_dist": (i32, [i32, vp, u64, vp, u64, u64p, i32, vp, vp]),
+        "bsort_sort_dist_ex": (i32, [i32, vp, u64, vp, u64, u64p, i32, ctypes.c_uint, vp, vp]),
+        "bsort_dist_exact_boundaries": (i32, [u64p, i32, i32, REFINE_FN, vp, u64p, i32p, i32p, u64p, i32p]),
+        "bsort_dist_exact_send_counts": (i32, [u64p, i32, i32, i32, i32p, u64p, u64p]),
         "bsort_last_nccl_error": (i32, []),
         "bsort_status_string": (ctypes.c_char_p, [i32]),
         "bsort_last_cuda_error": (i32, []),

@@ -1,5 +1,6 @@
 // api.cu — the extern "C" boundary (include/bsort.h): validation, path selection (§8 a2),
 // workspace handling, the host-only splitter math of the MSD partition, diagnostics.
+#include <algorithm>
 #include <atomic>
 #include <mutex>
 #include <vector>
@@ -343,6 +344,100 @@ bool increasing(const uint64_t* v, int m) {
   return true;
 }
 }  // namespace
+
+// Host planning of exact splitting (pure host; the same logic as dist.exact_boundaries /
+// exact_send_counts in the Python orchestration, which tests pin against brute force).
+bsort_status_t bsort_dist_exact_boundaries(const uint64_t* hg, int nranks, int key_bits, bsort_refine_fn refine,
+                                           void* ctx, uint64_t* values, int* m_out, int* idx, uint64_t* quota,
+                                           int* levels_out) {
+  if (!hg || !refine || !values || !m_out || !idx || !quota || nranks < 1 || nranks > BSORT_DIST_MAX_RANKS)
+    return BSORT_ERROR_INVALID_ARGUMENT;
+  if (key_bits != 32 && key_bits != 64) return BSORT_ERROR_INVALID_ARGUMENT;
+  const int R = nranks - 1;
+  unsigned __int128 N = 0;
+  for (int b = 0; b < BSORT_DIST_BINS; ++b) N += hg[b];
+  std::vector<uint64_t> T(R), pv(R), below(R);
+  std::vector<int> bits(R, 16);
+  std::vector<uint64_t> cum(BSORT_DIST_BINS);
+  uint64_t acc = 0;
+  for (int b = 0; b < BSORT_DIST_BINS; ++b) cum[b] = (acc += hg[b]);
+  for (int i = 0; i < R; ++i) {
+    T[i] = (uint64_t)((N * (unsigned __int128)(i + 1)) / (unsigned __int128)nranks);
+    const int b = (int)(std::upper_bound(cum.begin(), cum.end(), T[i]) - cum.begin());  // bin of rank T_i
+    if (b >= BSORT_DIST_BINS) return BSORT_ERROR_INVALID_ARGUMENT;  // T_i >= N: empty input
+    pv[i] = (uint64_t)b;
+    below[i] = b > 0 ? cum[b - 1] : 0;
+  }
+  int levels = 0;
+  std::vector<uint64_t> H;
+  for (int level_bits = 16; level_bits < key_bits; level_bits += 16) {
+    std::vector<uint64_t> prefixes;
+    for (int i = 0; i < R; ++i)
+      if (T[i] > below[i]) prefixes.push_back(pv[i]);
+    if (prefixes.empty()) break;
+    std::sort(prefixes.begin(), prefixes.end());
+    prefixes.erase(std::unique(prefixes.begin(), prefixes.end()), prefixes.end());
+    const int mm = (int)prefixes.size();
+    H.assign((size_t)mm * BSORT_DIST_BINS, 0);
+    if (refine(ctx, prefixes.data(), mm, level_bits, H.data()) != 0) return BSORT_ERROR_CUDA;
+    ++levels;
+    for (int i = 0; i < R; ++i) {
+      if (T[i] <= below[i]) continue;
+      const int row = (int)(std::lower_bound(prefixes.begin(), prefixes.end(), pv[i]) - prefixes.begin());
+      const uint64_t* h = H.data() + (size_t)row * BSORT_DIST_BINS;
+      const uint64_t res = T[i] - below[i];
+      uint64_t c = 0;
+      int sb = 0;
+      for (; sb < BSORT_DIST_BINS; ++sb) {  // first sub-bin whose inclusive count exceeds res
+        if (c + h[sb] > res) break;
+        c += h[sb];
+      }
+      if (sb >= BSORT_DIST_BINS) return BSORT_ERROR_INVALID_ARGUMENT;  // inconsistent histograms
+      below[i] += c;
+      pv[i] = (pv[i] << 16) | (uint64_t)sb;
+      bits[i] += 16;
+    }
+  }
+  std::vector<uint64_t> K(R);
+  for (int i = 0; i < R; ++i) K[i] = pv[i] << (key_bits - bits[i]);
+  std::vector<uint64_t> v(K);
+  std::sort(v.begin(), v.end());
+  v.erase(std::unique(v.begin(), v.end()), v.end());
+  for (size_t j = 0; j < v.size(); ++j) values[j] = v[j];
+  for (int i = 0; i < R; ++i) {
+    idx[i] = (int)(std::lower_bound(v.begin(), v.end(), K[i]) - v.begin());
+    quota[i] = T[i] - below[i];
+  }
+  *m_out = (int)v.size();
+  if (levels_out) *levels_out = levels;
+  return BSORT_SUCCESS;
+}
+
+bsort_status_t bsort_dist_exact_send_counts(const uint64_t* cc, int nranks, int m, int rank, const int* idx,
+                                            const uint64_t* quota, uint64_t* send_counts) {
+  if (!cc || !send_counts || nranks < 1 || nranks > BSORT_DIST_MAX_RANKS || rank < 0 || rank >= nranks || m < 0)
+    return BSORT_ERROR_INVALID_ARGUMENT;
+  if (nranks > 1 && (!idx || !quota || m < 1)) return BSORT_ERROR_INVALID_ARGUMENT;
+  const int C = 2 * m + 1;
+  const uint64_t* mine = cc + (size_t)rank * C;
+  std::vector<uint64_t> start(C + 1, 0);
+  for (int c = 0; c < C; ++c) start[c + 1] = start[c] + mine[c];
+  uint64_t prev = 0;
+  for (int r = 0; r + 1 < nranks; ++r) {
+    const int j = idx[r];
+    if (j < 0 || j >= m) return BSORT_ERROR_INVALID_ARGUMENT;
+    uint64_t eq_before = 0;  // keys equal to values[j] on lower ranks
+    for (int q = 0; q < rank; ++q) eq_before += cc[(size_t)q * C + 2 * j + 1];
+    const uint64_t want = quota[r] > eq_before ? quota[r] - eq_before : 0;
+    const uint64_t share = std::min(want, mine[2 * j + 1]);
+    const uint64_t split = start[2 * j + 1] + share;
+    if (split < prev) return BSORT_ERROR_INVALID_ARGUMENT;
+    send_counts[r] = split - prev;
+    prev = split;
+  }
+  send_counts[nranks - 1] = start[C] - prev;
+  return BSORT_SUCCESS;
+}
 
 bsort_status_t bsort_dist_refine_hist(bsort_dtype_t dtype, const void* dev_keys, uint64_t n,
                                       bsort_direction_t direction, const uint64_t* prefixes, int m,

@@ -129,19 +129,48 @@ struct StreamBlock {
   }
 };
 
+struct RefineCtx {
+  NcclApi* N;
+  bsort_comm* c;
+  bsort_dtype_t dtype;
+  const void* keys;
+  uint64_t n;
+  bsort_direction_t dir;
+  uint64_t* dev_hist;  // BSORT_DIST_MAX_RANKS * 65536 u64
+  cudaStream_t s;
+};
+
+// bsort_refine_fn for the native exact mode: local refinement histograms, NCCL all-reduce, D2H.
+int refine_cb(void* p, const uint64_t* prefixes, int m, int prefix_bits, uint64_t* hist) {
+  auto* r = static_cast<RefineCtx*>(p);
+  if (bsort_dist_refine_hist(r->dtype, r->keys, r->n, r->dir, prefixes, m, prefix_bits, r->dev_hist, r->s) !=
+      BSORT_SUCCESS)
+    return 1;
+  const size_t cnt = (size_t)m * BSORT_DIST_BINS;
+  if (r->N->AllReduce(r->dev_hist, r->dev_hist, cnt, ncclUint64, ncclSum, r->c->comm, r->s) != ncclSuccess) return 2;
+  if (cudaMemcpyAsync(hist, r->dev_hist, cnt * 8, cudaMemcpyDeviceToHost, r->s) != cudaSuccess) return 3;
+  return cudaStreamSynchronize(r->s) == cudaSuccess ? 0 : 4;
+}
+
 bsort_status_t sort_dist_impl(bsort_dtype_t dtype, const void* dev_in, uint64_t n, void* dev_out, uint64_t cap,
-                              uint64_t* n_out, bsort_direction_t dir, bsort_comm* c, cudaStream_t s) {
+                              uint64_t* n_out, bsort_direction_t dir, bool exact, bsort_comm* c, cudaStream_t s) {
   NcclApi& N = nccl();
   const int P = c->nranks, me = c->rank;
   const int es = key_bytes(dtype);
+  exact = exact && P > 1;  // one rank: every key stays, both modes coincide
 
-  // One device block: [global hist | local hist | counts (P x (P+1)) | bucketed keys | ws]
+  // One device block: [global hist | local hist | counts | refinement hists | bucketed keys | ws]
   // The local sort's workspace reuses the bucketed keys + partition workspace after the exchange.
+  // Counts: bin mode P x (P+1) (send counts + capacity), exact mode P x (2(P-1)+2) (class counts +
+  // capacity).
   const size_t hist_b = (size_t)BSORT_DIST_BINS * 8;
-  const size_t cnt_b = round_up((size_t)P * (P + 1) * 8, 256);
+  const int CW = exact ? 2 * (P - 1) + 2 : P + 1;  // u64 words per rank in the gathered counts
+  const size_t cnt_b = round_up((size_t)P * CW * 8, 256);
+  const size_t ref_b = exact ? (size_t)(P - 1) * BSORT_DIST_BINS * 8 : 0;
   const size_t bucket_b = round_up((size_t)n * es, 256);
-  const size_t part_ws = bsort_dist_partition_workspace_bytes(dtype, n, P);
-  const size_t head = 2 * hist_b + cnt_b;
+  const size_t part_ws = exact ? bsort_dist_class_partition_workspace_bytes()
+                               : bsort_dist_partition_workspace_bytes(dtype, n, P);
+  const size_t head = 2 * hist_b + cnt_b + ref_b;
   StreamBlock blk;
   blk.s = s;
   // the tail must hold the partition phase and, later, the local sort of up to `cap` keys
@@ -166,18 +195,55 @@ bsort_status_t sort_dist_impl(bsort_dtype_t dtype, const void* dev_in, uint64_t 
   CUDA_TRY(cudaMemcpyAsync(hist.data(), g_hist, 2 * hist_b, cudaMemcpyDeviceToHost, s));
   CUDA_TRY(cudaStreamSynchronize(s));
 
-  // a8: cuts from the global histogram; this rank's send counts; gather (counts, capacity)
+  // a8: per-destination counts of every rank, all-gathered with every rank's capacity.
+  // sendm[src * P + dst] = keys src sends to dst; caps[q] = rank q's out_capacity.
+  std::vector<uint64_t> sendm((size_t)P * P), caps(P);
   std::vector<uint32_t> cuts(P + 1);
-  std::vector<uint64_t> mine(P + 1);
-  BS_TRY(bsort_dist_splitters(hist.data(), P, cuts.data()));
-  BS_TRY(bsort_dist_send_counts(hist.data() + BSORT_DIST_BINS, cuts.data(), P, mine.data()));
-  mine[P] = cap;
-  CUDA_TRY(cudaMemcpyAsync(d_cnt + (size_t)me * (P + 1), mine.data(), (P + 1) * 8, cudaMemcpyHostToDevice, s));
-  NCCL_TRY(N.AllGather(d_cnt + (size_t)me * (P + 1), d_cnt, P + 1, ncclUint64, c->comm, s));
-  std::vector<uint64_t> all((size_t)P * (P + 1));
-  CUDA_TRY(cudaMemcpyAsync(all.data(), d_cnt, all.size() * 8, cudaMemcpyDeviceToHost, s));
-  CUDA_TRY(cudaStreamSynchronize(s));
-  auto sent = [&](int src, int dst) { return all[(size_t)src * (P + 1) + dst]; };
+  std::vector<uint64_t> values(P), quota(P), my_classes;
+  std::vector<int> idx(P);
+  int m = 0;
+  if (!exact) {
+    std::vector<uint64_t> mine(P + 1);
+    BS_TRY(bsort_dist_splitters(hist.data(), P, cuts.data()));
+    BS_TRY(bsort_dist_send_counts(hist.data() + BSORT_DIST_BINS, cuts.data(), P, mine.data()));
+    mine[P] = cap;
+    CUDA_TRY(cudaMemcpyAsync(d_cnt + (size_t)me * CW, mine.data(), CW * 8, cudaMemcpyHostToDevice, s));
+    NCCL_TRY(N.AllGather(d_cnt + (size_t)me * CW, d_cnt, CW, ncclUint64, c->comm, s));
+    std::vector<uint64_t> all((size_t)P * CW);
+    CUDA_TRY(cudaMemcpyAsync(all.data(), d_cnt, all.size() * 8, cudaMemcpyDeviceToHost, s));
+    CUDA_TRY(cudaStreamSynchronize(s));
+    for (int q = 0; q < P; ++q) {
+      for (int d = 0; d < P; ++d) sendm[(size_t)q * P + d] = all[(size_t)q * CW + d];
+      caps[q] = all[(size_t)q * CW + P];
+    }
+  } else {
+    // §8 N2: exact boundaries by refinement histograms, then class counts of every rank
+    uint64_t N_total = 0;
+    for (int b = 0; b < BSORT_DIST_BINS; ++b) N_total += hist[b];
+    if (N_total > 0) {
+      RefineCtx rc{&N, c, dtype, dev_in, n, dir, reinterpret_cast<uint64_t*>(base + 2 * hist_b + cnt_b), s};
+      BS_TRY(bsort_dist_exact_boundaries(hist.data(), P, es * 8, refine_cb, &rc, values.data(), &m, idx.data(),
+                                         quota.data(), nullptr));
+      const int C = 2 * m + 1;
+      BS_TRY(bsort_dist_class_hist(dtype, dev_in, n, dir, values.data(), m, d_cnt + (size_t)me * CW, s));
+      CUDA_TRY(cudaMemcpyAsync(d_cnt + (size_t)me * CW + C, &cap, 8, cudaMemcpyHostToDevice, s));
+      NCCL_TRY(N.AllGather(d_cnt + (size_t)me * CW, d_cnt, CW, ncclUint64, c->comm, s));
+      std::vector<uint64_t> all((size_t)P * CW);
+      CUDA_TRY(cudaMemcpyAsync(all.data(), d_cnt, all.size() * 8, cudaMemcpyDeviceToHost, s));
+      CUDA_TRY(cudaStreamSynchronize(s));
+      std::vector<uint64_t> cc((size_t)P * C);
+      for (int q = 0; q < P; ++q) {
+        for (int k = 0; k < C; ++k) cc[(size_t)q * C + k] = all[(size_t)q * CW + k];
+        caps[q] = all[(size_t)q * CW + C];
+      }
+      for (int q = 0; q < P; ++q)  // every rank's send counts follow from the gathered classes
+        BS_TRY(bsort_dist_exact_send_counts(cc.data(), P, m, q, idx.data(), quota.data(), &sendm[(size_t)q * P]));
+      my_classes.assign(cc.begin() + (size_t)me * C, cc.begin() + (size_t)(me + 1) * C);
+    } else {  // no keys anywhere: nothing moves (capacities irrelevant)
+      for (int q = 0; q < P; ++q) caps[q] = ~0ull;
+    }
+  }
+  auto sent = [&](int src, int dst) { return sendm[(size_t)src * P + dst]; };
 
   // capacity: every rank checks every rank, so all return the same status
   uint64_t recv_total = 0;
@@ -186,14 +252,20 @@ bsort_status_t sort_dist_impl(bsort_dtype_t dtype, const void* dev_in, uint64_t 
     uint64_t tot = 0;
     for (int r = 0; r < P; ++r) tot += sent(r, q);
     if (q == me) recv_total = tot;
-    if (tot > all[(size_t)q * (P + 1) + P]) overflow = true;
+    if (tot > caps[q]) overflow = true;
   }
   if (n_out) *n_out = recv_total;
   if (overflow) return BSORT_ERROR_CAPACITY;
 
-  // a9: bucketed copy (bucket q = keys for rank q)
-  if (n > 0)
-    BS_TRY(bsort_dist_partition(dtype, dev_in, n, dir, cuts.data(), mine.data(), P, bucket, ws, part_ws, s));
+  // a9: bucketed copy (bucket q = keys for rank q, contiguous)
+  if (n > 0) {
+    if (exact)
+      BS_TRY(bsort_dist_partition_classes(dtype, dev_in, n, dir, values.data(), m, my_classes.data(), bucket, ws,
+                                          part_ws, s));
+    else
+      BS_TRY(bsort_dist_partition(dtype, dev_in, n, dir, cuts.data(), &sendm[(size_t)me * P], P, bucket, ws,
+                                  part_ws, s));
+  }
 
   // a10: grouped send/recv; rank r's keys land at sum_{r'<r} sent(r', me) in dev_out
   NCCL_TRY(N.GroupStart());
@@ -277,8 +349,23 @@ bsort_status_t bsort_sort_dist(bsort_dtype_t dtype, const void* dev_in, uint64_t
   if (n_local > 0 && (!dev_in || (uintptr_t)dev_in % es)) return BSORT_ERROR_INVALID_ARGUMENT;
   if (out_capacity > 0 && (!dev_out || (uintptr_t)dev_out % es)) return BSORT_ERROR_INVALID_ARGUMENT;
   if (dev_out && dev_in && dev_out == dev_in && n_local > 0) return BSORT_ERROR_INVALID_ARGUMENT;
-  return sort_dist_impl(dtype, dev_in, n_local, dev_out, out_capacity, n_out, direction, comm,
+  return sort_dist_impl(dtype, dev_in, n_local, dev_out, out_capacity, n_out, direction, false, comm,
                         (cudaStream_t)stream);
+}
+
+bsort_status_t bsort_sort_dist_ex(bsort_dtype_t dtype, const void* dev_in, uint64_t n_local, void* dev_out,
+                                  uint64_t out_capacity, uint64_t* n_out, bsort_direction_t direction,
+                                  unsigned flags, bsort_comm_t comm, void* stream) {
+  if ((flags & ~BSORT_DIST_EXACT) != 0) return BSORT_ERROR_INVALID_ARGUMENT;
+  if (!comm || !comm->comm) return BSORT_ERROR_INVALID_ARGUMENT;
+  if (direction != BSORT_ASCENDING && direction != BSORT_DESCENDING) return BSORT_ERROR_INVALID_ARGUMENT;
+  const int es = key_bytes(dtype);
+  if (es == 0) return BSORT_ERROR_UNSUPPORTED_DTYPE;
+  if (n_local > 0 && (!dev_in || (uintptr_t)dev_in % es)) return BSORT_ERROR_INVALID_ARGUMENT;
+  if (out_capacity > 0 && (!dev_out || (uintptr_t)dev_out % es)) return BSORT_ERROR_INVALID_ARGUMENT;
+  if (dev_out && dev_in && dev_out == dev_in && n_local > 0) return BSORT_ERROR_INVALID_ARGUMENT;
+  return sort_dist_impl(dtype, dev_in, n_local, dev_out, out_capacity, n_out, direction,
+                        (flags & BSORT_DIST_EXACT) != 0, comm, (cudaStream_t)stream);
 }
 
 int bsort_last_nccl_error(void) { return t_last_nccl; }

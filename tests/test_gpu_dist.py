@@ -349,7 +349,7 @@ def test_sort_dist_native_local_comm(B, dtype, desc):
         for n in (0, 1, 5000, 300_007):
             x = gen(dtype, n, 500 + n)
             before = x.clone()
-            out = B.sort_dist_native(x, comm, desc)
+            out = B.sort_dist_native(x, comm, desc, exact=(n % 2 == 1))  # both entry modes
             torch.cuda.synchronize()
             assert host(out).tobytes() == oracle.sort_native(host(before), descending=desc).tobytes()
             assert host(x).tobytes() == host(before).tobytes()  # dev_in left intact (bitwise)
@@ -373,6 +373,8 @@ def test_sort_dist_native_capacity(B):
         assert host(got).tobytes() == oracle.sort_native(host(x)).tobytes()
         assert B.lib.bsort_sort_dist(3, ctypes.c_void_p(x.data_ptr()), 10, ctypes.c_void_p(out.data_ptr()),
                                      100, None, 0, comm._h, None) == 2  # i16: unsupported here
+        assert B.lib.bsort_sort_dist_ex(8, ctypes.c_void_p(x.data_ptr()), 10, ctypes.c_void_p(out.data_ptr()),
+                                        100, None, 0, 2, comm._h, None) == 1  # unknown flag
     finally:
         comm.close()
 

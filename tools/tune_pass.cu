@@ -154,6 +154,18 @@ void suite(uint64_t n) {
     run<U, 384, 12, 2, true, RANK_STABLE, 8>(in, out, n, bases, lookback, counter, gcount, ref, dbg);
     run<U, 384, 12, 2, true, RANK_RUN2, 8>(in, out, n, bases, lookback, counter, gcount, ref, dbg);
     run<U, 384, 12, 2, true, RANK_UNSTABLE, 8>(in, out, n, bases, lookback, counter, gcount, ref, dbg);
+#ifdef TUNE_U64_SWEEP
+    run<U, 256, 16, 2, true, RANK_STABLE, 8>(in, out, n, bases, lookback, counter, gcount, ref, dbg);
+    run<U, 256, 16, 2, true, RANK_RUN2, 8>(in, out, n, bases, lookback, counter, gcount, ref, dbg);
+    run<U, 256, 16, 2, true, RANK_UNSTABLE, 8>(in, out, n, bases, lookback, counter, gcount, ref, dbg);
+    run<U, 512, 8, 2, true, RANK_STABLE, 8>(in, out, n, bases, lookback, counter, gcount, ref, dbg);
+    run<U, 512, 8, 2, true, RANK_RUN2, 8>(in, out, n, bases, lookback, counter, gcount, ref, dbg);
+    run<U, 512, 8, 2, true, RANK_UNSTABLE, 8>(in, out, n, bases, lookback, counter, gcount, ref, dbg);
+    run<U, 256, 12, 3, true, RANK_STABLE, 8>(in, out, n, bases, lookback, counter, gcount, ref, dbg);
+    run<U, 256, 12, 3, true, RANK_RUN2, 8>(in, out, n, bases, lookback, counter, gcount, ref, dbg);
+    run<U, 384, 16, 1, true, RANK_STABLE, 8>(in, out, n, bases, lookback, counter, gcount, ref, dbg);
+    run<U, 384, 16, 1, true, RANK_RUN2, 8>(in, out, n, bases, lookback, counter, gcount, ref, dbg);
+#endif
   }
   cudaFree(in);
   cudaFree(out);
