@@ -232,7 +232,8 @@ def bench_single(args, B):
                          "steps outside the timed events", "parallelism": "single GPU"},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
                      "frac": achieved / hbm_peak, "traffic": load_traffic("onesweep_pass"),
-                     "kernel": "k_onesweep_pass", "algorithmic_bytes_per_launch": pass_bytes,
+                     "kernel": "LSD scatter pass (k_onesweep_pass; k_onesweep_pass_ws for look-back passes)",
+                     "algorithmic_bytes_per_launch": pass_bytes,
                      "avg_launch_ms": pass_ms, "working_launches_per_step": 4,
                      "launches_per_step": pk["launches"] / len(times), "peak_source": peak_src,
                      "whole_sort_36B_per_key_GBps": sort_gbs, "whole_sort_frac": sort_gbs / hbm_peak,

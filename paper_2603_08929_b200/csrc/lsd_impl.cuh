@@ -11,6 +11,7 @@
 #include <type_traits>
 
 #include "onesweep.cuh"
+#include "onesweep_ws.cuh"
 #include "paths.cuh"
 
 namespace bsort {
@@ -104,6 +105,40 @@ bsort_status_t launch_pass(const U* a, U* b, uint64_t n, DigitF digit, const uns
                                                   s);
 }
 
+// Warp-specialised look-back pass (onesweep_ws.cuh) for 32-bit keys without payload: rankers
+// never wait for the look-back walk.  Same tile (512 x 16 keys) as PassCfg, one CTA of 768 threads
+// per SM.  BSORT_WS=0 selects k_onesweep_pass instead (A/B).
+constexpr int WS_RT = 512, WS_ITEMS = 16;
+inline bool ws_enabled() {
+  static const bool on = [] {
+    const char* e = getenv("BSORT_WS");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
+
+template <typename U, typename DescT, typename DigitF>
+bsort_status_t launch_pass_ws(const U* a, U* b, uint64_t n, DigitF digit, const unsigned long long* bases,
+                              DescT* lookback, uint32_t* counter, const PassPlan* plan, int pass, cudaStream_t s) {
+  using L = PassSmemWS<WS_RT, WS_ITEMS, U>;
+  static_assert(L::TILE == PassCfg<U, RANK_RUN2>::THREADS * PassCfg<U, RANK_RUN2>::ITEMS,
+                "same tiles as the look-back array is sized for");
+  auto kern = k_onesweep_pass_ws<U, WS_RT, WS_ITEMS, DescT, DigitF, RANK_RUN2, 8>;
+  static int occ = 0;
+  if (occ == 0) {
+    BSORT_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L::bytes));
+    int o = 0;
+    BSORT_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, kern, WS_RT + 256, L::bytes));
+    occ = o > 0 ? o : 1;
+  }
+  const uint64_t tiles = (n + L::TILE - 1) / L::TILE;
+  const uint64_t grid = min64(tiles, (uint64_t)num_sms() * occ);  // all resident (look-back progress)
+  BSORT_LAUNCH(PROF_PASS, s,
+               kern<<<(unsigned)grid, WS_RT + 256, L::bytes, s>>>(a, b, n, digit, bases, lookback, counter,
+                                                                  (uint32_t)tiles, plan, pass));
+  return BSORT_SUCCESS;
+}
+
 inline bsort_status_t memset_async(void* p, size_t bytes, cudaStream_t s) {
   BSORT_LAUNCH(PROF_MEMSET, s, cudaMemsetAsync(p, 0, bytes, s));
   return BSORT_SUCCESS;
@@ -170,10 +205,20 @@ bsort_status_t lsd_run(U* keys, uint32_t* vals, uint64_t n, unsigned char* ws, c
     if constexpr (p == 0)
       st = launch_pass<U, RANK_UNSTABLE, DescT, KV>(keys, scratch, n, RadixDigit<KIND, DESC, U, SH>{}, bases,
                                                     lookback, gcount, counters, plan, p, s, kvp);
-    else
-      st = launch_pass<U, RANK_RUN2, DescT, KV>(keys, scratch, n, RadixDigit<KIND, DESC, U, SH>{},
-                                                bases + p * 256, lookback, gcount + p * 256, counters + p,
-                                                plan, p, s, kvp);
+    else {
+      bool done = false;
+      if constexpr (sizeof(U) == 4 && !KV) {
+        if (ws_enabled() && (uintptr_t)keys % 16 == 0) {  // TMA on both buffers (scratch is aligned)
+          st = launch_pass_ws<U, DescT>(keys, scratch, n, RadixDigit<KIND, DESC, U, SH>{}, bases + p * 256,
+                                        lookback, counters + p, plan, p, s);
+          done = true;
+        }
+      }
+      if (!done)
+        st = launch_pass<U, RANK_RUN2, DescT, KV>(keys, scratch, n, RadixDigit<KIND, DESC, U, SH>{},
+                                                  bases + p * 256, lookback, gcount + p * 256, counters + p,
+                                                  plan, p, s, kvp);
+    }
     // pass 1 without look-back when the joint plan allows it (each launch checks plan->j01
     // and exactly one of the two does the work)
     if constexpr (p == 1)

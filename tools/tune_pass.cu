@@ -8,7 +8,7 @@
 #include <cstdlib>
 #include <vector>
 
-#include "onesweep.cuh"
+#include "onesweep_ws.cuh"
 
 namespace bsort {
 // The kernels only reference these through BSORT_LAUNCH, unused here.
@@ -107,6 +107,47 @@ void run(const U* in, U* out, uint64_t n, const unsigned long long* bases, uint3
   fflush(stdout);
 }
 
+template <typename U, int RT, int ITEMS, int RANK, int MINB = 1>
+void run_ws(const U* in, U* out, uint64_t n, const unsigned long long* bases, uint32_t* lookback, uint32_t* counter,
+            unsigned long long ref_sum, unsigned long long* dbg) {
+  using DigitF = RadixDigit<sizeof(U) == 4 ? KIND_F : KIND_I, false, U, 0>;
+  using L = PassSmemWS<RT, ITEMS, U>;
+  auto kern = k_onesweep_pass_ws<U, RT, ITEMS, uint32_t, DigitF, RANK, 8, MINB>;
+  CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L::bytes));
+  int occ = 0;
+  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, RT + 256, L::bytes));
+  const uint64_t tiles = (n + L::TILE - 1) / L::TILE;
+  const unsigned grid = (unsigned)min64(tiles, (uint64_t)148 * occ);
+  cudaFuncAttributes fa;
+  CK(cudaFuncGetAttributes(&fa, kern));
+  cudaEvent_t a, b;
+  CK(cudaEventCreate(&a));
+  CK(cudaEventCreate(&b));
+  float tot = 0.f;
+  const int reps = 6;
+  for (int r = 0; r < reps; ++r) {
+    CK(cudaMemset(lookback, 0, tiles * 256 * 4));
+    CK(cudaMemset(counter, 0, 4));
+    CK(cudaEventRecord(a));
+    kern<<<grid, RT + 256, L::bytes>>>(in, out, n, DigitF{}, bases, lookback, counter, (uint32_t)tiles, nullptr, 0);
+    CK(cudaEventRecord(b));
+    CK(cudaEventSynchronize(b));
+    CK(cudaGetLastError());
+    float ms;
+    CK(cudaEventElapsedTime(&ms, a, b));
+    if (r > 0) tot += ms;
+  }
+  CK(cudaMemset(dbg, 0, 16));
+  k_check<<<1184, 256>>>(out, n, DigitF{}, dbg, dbg + 1);
+  unsigned long long h[2];
+  CK(cudaMemcpy(h, dbg, 16, cudaMemcpyDeviceToHost));
+  const double avg = tot / (reps - 1);
+  printf("{\"ws\": 1, \"rank\": %d, \"key_bytes\": %d, \"threads\": %d, \"items\": %d, \"occ\": %d, \"regs\": %d, "
+         "\"local\": %zu, \"smem\": %zu, \"avg_ms\": %.4f, \"digit_sorted\": %d, \"perm\": %d}\n",
+         MINB, RANK, (int)sizeof(U), RT, ITEMS, occ, fa.numRegs, fa.localSizeBytes, L::bytes, avg, h[0] == 0, h[1] == ref_sum);
+  fflush(stdout);
+}
+
 template <typename U>
 void suite(uint64_t n) {
   U *in, *out;
@@ -147,6 +188,16 @@ void suite(uint64_t n) {
   const unsigned long long ref = h[1];
   // One pass on uniform keys with digit shift 0: RUN2 sees a single run (the fast path).
   if constexpr (sizeof(U) == 4) {
+#ifdef TUNE_WS
+    run_ws<U, 512, 16, RANK_STABLE>(in, out, n, bases, lookback, counter, ref, dbg);
+    run_ws<U, 512, 16, RANK_RUN2>(in, out, n, bases, lookback, counter, ref, dbg);
+    run_ws<U, 512, 8, RANK_STABLE, 2>(in, out, n, bases, lookback, counter, ref, dbg);
+    run_ws<U, 512, 8, RANK_RUN2, 2>(in, out, n, bases, lookback, counter, ref, dbg);
+    run_ws<U, 256, 16, RANK_STABLE, 2>(in, out, n, bases, lookback, counter, ref, dbg);
+    run_ws<U, 256, 16, RANK_RUN2, 2>(in, out, n, bases, lookback, counter, ref, dbg);
+    run_ws<U, 256, 16, RANK_STABLE, 3>(in, out, n, bases, lookback, counter, ref, dbg);
+    run_ws<U, 256, 16, RANK_RUN2, 3>(in, out, n, bases, lookback, counter, ref, dbg);
+#endif
     run<U, 512, 16, 2, true, RANK_STABLE, 8>(in, out, n, bases, lookback, counter, gcount, ref, dbg);
     run<U, 512, 16, 2, true, RANK_RUN2, 8>(in, out, n, bases, lookback, counter, gcount, ref, dbg);
     run<U, 512, 16, 2, true, RANK_UNSTABLE, 8>(in, out, n, bases, lookback, counter, gcount, ref, dbg);
