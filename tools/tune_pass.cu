@@ -142,7 +142,7 @@ void run_ws(const U* in, U* out, uint64_t n, const unsigned long long* bases, ui
   unsigned long long h[2];
   CK(cudaMemcpy(h, dbg, 16, cudaMemcpyDeviceToHost));
   const double avg = tot / (reps - 1);
-  printf("{\"ws\": 1, \"rank\": %d, \"key_bytes\": %d, \"threads\": %d, \"items\": %d, \"occ\": %d, \"regs\": %d, "
+  printf("{\"ws\": 1, \"minb\": %d, \"rank\": %d, \"key_bytes\": %d, \"threads\": %d, \"items\": %d, \"occ\": %d, \"regs\": %d, "
          "\"local\": %zu, \"smem\": %zu, \"avg_ms\": %.4f, \"digit_sorted\": %d, \"perm\": %d}\n",
          MINB, RANK, (int)sizeof(U), RT, ITEMS, occ, fa.numRegs, fa.localSizeBytes, L::bytes, avg, h[0] == 0, h[1] == ref_sum);
   fflush(stdout);
