@@ -105,10 +105,15 @@ bsort_status_t launch_pass(const U* a, U* b, uint64_t n, DigitF digit, const uns
                                                   s);
 }
 
-// Warp-specialised look-back pass (onesweep_ws.cuh) for 32-bit keys without payload: rankers
-// never wait for the look-back walk.  Same tile (512 x 16 keys) as PassCfg, one CTA of 768 threads
-// per SM.  BSORT_WS=0 selects k_onesweep_pass instead (A/B).
-constexpr int WS_RT = 512, WS_ITEMS = 16;
+// Warp-specialised look-back pass (onesweep_ws.cuh) for keys without payload: rankers never wait
+// for the look-back walk.  One CTA of 512 rankers + 256 writers per SM; 32-bit keys keep
+// PassCfg's 8192-key tile, 64-bit keys take 512 x 12 = 6144 (three 48 KB buffers; tools/tune_pass
+// -DTUNE_WS: stable 3.18 -> 2.77 ms, RUN2 2.73 -> 2.57 ms per 2^29 u64 keys).  Tiles at least as
+// large as PassCfg's, so the look-back array (sized by PassCfg) is large enough.
+// BSORT_WS=0 selects k_onesweep_pass instead (A/B).
+template <typename U> struct WsCfg;
+template <> struct WsCfg<uint32_t> { static constexpr int RT = 512, ITEMS = 16; };
+template <> struct WsCfg<unsigned long long> { static constexpr int RT = 512, ITEMS = 12; };
 inline bool ws_enabled() {
   static const bool on = [] {
     const char* e = getenv("BSORT_WS");
@@ -120,10 +125,11 @@ inline bool ws_enabled() {
 template <typename U, typename DescT, typename DigitF>
 bsort_status_t launch_pass_ws(const U* a, U* b, uint64_t n, DigitF digit, const unsigned long long* bases,
                               DescT* lookback, uint32_t* counter, const PassPlan* plan, int pass, cudaStream_t s) {
-  using L = PassSmemWS<WS_RT, WS_ITEMS, U>;
-  static_assert(L::TILE == PassCfg<U, RANK_RUN2>::THREADS * PassCfg<U, RANK_RUN2>::ITEMS,
-                "same tiles as the look-back array is sized for");
-  auto kern = k_onesweep_pass_ws<U, WS_RT, WS_ITEMS, DescT, DigitF, RANK_RUN2, 8>;
+  constexpr int WS_RT = WsCfg<U>::RT;
+  using L = PassSmemWS<WS_RT, WsCfg<U>::ITEMS, U>;
+  static_assert(L::TILE >= PassCfg<U, RANK_RUN2>::THREADS * PassCfg<U, RANK_RUN2>::ITEMS,
+                "no more tiles than the look-back array is sized for");
+  auto kern = k_onesweep_pass_ws<U, WS_RT, WsCfg<U>::ITEMS, DescT, DigitF, RANK_RUN2, 8>;
   static int occ = 0;
   if (occ == 0) {
     BSORT_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L::bytes));
@@ -207,7 +213,7 @@ bsort_status_t lsd_run(U* keys, uint32_t* vals, uint64_t n, unsigned char* ws, c
                                                     lookback, gcount, counters, plan, p, s, kvp);
     else {
       bool done = false;
-      if constexpr (sizeof(U) == 4 && !KV) {
+      if constexpr (!KV) {
         if (ws_enabled() && (uintptr_t)keys % 16 == 0) {  // TMA on both buffers (scratch is aligned)
           st = launch_pass_ws<U, DescT>(keys, scratch, n, RadixDigit<KIND, DESC, U, SH>{}, bases + p * 256,
                                         lookback, counters + p, plan, p, s);
