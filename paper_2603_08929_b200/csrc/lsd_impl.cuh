@@ -106,14 +106,16 @@ bsort_status_t launch_pass(const U* a, U* b, uint64_t n, DigitF digit, const uns
 }
 
 // Warp-specialised look-back pass (onesweep_ws.cuh) for keys without payload: rankers never wait
-// for the look-back walk.  One CTA of 512 rankers + 256 writers per SM; 32-bit keys keep
-// PassCfg's 8192-key tile, 64-bit keys take 512 x 12 = 6144 (three 48 KB buffers; tools/tune_pass
-// -DTUNE_WS: stable 3.18 -> 2.77 ms, RUN2 2.73 -> 2.57 ms per 2^29 u64 keys).  Tiles at least as
-// large as PassCfg's, so the look-back array (sized by PassCfg) is large enough.
+// for the look-back walk.  One CTA of 512 rankers + 256 writers per SM, larger tiles than
+// PassCfg's (the look-back array, sized by PassCfg, is then large enough): 32-bit keys 512 x 20 =
+// 10240 (three 40 KB buffers; tools/tune_pass -DTUNE_WS: stable 4.24 -> 3.79 ms, RUN2 3.65 -> 3.22
+// ms per 2^30 keys; x16 and x24 were slower), 64-bit keys 512 x 14 = 7168 (three 56 KB buffers,
+// 223 KB of shared memory: stable 3.18 -> 2.51 ms, RUN2 2.73 -> 2.27 ms per 2^29 keys; x12: 2.77 /
+// 2.57).  RUN2's two-run condition holds for pass 2 of 2^30 keys (runs of ~16K keys).
 // BSORT_WS=0 selects k_onesweep_pass instead (A/B).
 template <typename U> struct WsCfg;
-template <> struct WsCfg<uint32_t> { static constexpr int RT = 512, ITEMS = 16; };
-template <> struct WsCfg<unsigned long long> { static constexpr int RT = 512, ITEMS = 12; };
+template <> struct WsCfg<uint32_t> { static constexpr int RT = 512, ITEMS = 20; };
+template <> struct WsCfg<unsigned long long> { static constexpr int RT = 512, ITEMS = 14; };
 inline bool ws_enabled() {
   static const bool on = [] {
     const char* e = getenv("BSORT_WS");

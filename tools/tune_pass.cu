@@ -191,12 +191,10 @@ void suite(uint64_t n) {
 #ifdef TUNE_WS
     run_ws<U, 512, 16, RANK_STABLE>(in, out, n, bases, lookback, counter, ref, dbg);
     run_ws<U, 512, 16, RANK_RUN2>(in, out, n, bases, lookback, counter, ref, dbg);
-    run_ws<U, 512, 8, RANK_STABLE, 2>(in, out, n, bases, lookback, counter, ref, dbg);
-    run_ws<U, 512, 8, RANK_RUN2, 2>(in, out, n, bases, lookback, counter, ref, dbg);
-    run_ws<U, 256, 16, RANK_STABLE, 2>(in, out, n, bases, lookback, counter, ref, dbg);
-    run_ws<U, 256, 16, RANK_RUN2, 2>(in, out, n, bases, lookback, counter, ref, dbg);
-    run_ws<U, 256, 16, RANK_STABLE, 3>(in, out, n, bases, lookback, counter, ref, dbg);
-    run_ws<U, 256, 16, RANK_RUN2, 3>(in, out, n, bases, lookback, counter, ref, dbg);
+    run_ws<U, 512, 20, RANK_STABLE>(in, out, n, bases, lookback, counter, ref, dbg);
+    run_ws<U, 512, 20, RANK_RUN2>(in, out, n, bases, lookback, counter, ref, dbg);
+    run_ws<U, 512, 24, RANK_STABLE>(in, out, n, bases, lookback, counter, ref, dbg);
+    run_ws<U, 512, 24, RANK_RUN2>(in, out, n, bases, lookback, counter, ref, dbg);
 #endif
     run<U, 512, 16, 2, true, RANK_STABLE, 8>(in, out, n, bases, lookback, counter, gcount, ref, dbg);
     run<U, 512, 16, 2, true, RANK_RUN2, 8>(in, out, n, bases, lookback, counter, gcount, ref, dbg);
@@ -206,12 +204,10 @@ void suite(uint64_t n) {
     run<U, 384, 12, 2, true, RANK_RUN2, 8>(in, out, n, bases, lookback, counter, gcount, ref, dbg);
     run<U, 384, 12, 2, true, RANK_UNSTABLE, 8>(in, out, n, bases, lookback, counter, gcount, ref, dbg);
 #ifdef TUNE_WS
-    run_ws<U, 384, 12, RANK_STABLE>(in, out, n, bases, lookback, counter, ref, dbg);
-    run_ws<U, 384, 12, RANK_RUN2>(in, out, n, bases, lookback, counter, ref, dbg);
     run_ws<U, 512, 12, RANK_STABLE>(in, out, n, bases, lookback, counter, ref, dbg);
     run_ws<U, 512, 12, RANK_RUN2>(in, out, n, bases, lookback, counter, ref, dbg);
-    run_ws<U, 512, 8, RANK_STABLE>(in, out, n, bases, lookback, counter, ref, dbg);
-    run_ws<U, 512, 8, RANK_RUN2>(in, out, n, bases, lookback, counter, ref, dbg);
+    run_ws<U, 512, 14, RANK_STABLE>(in, out, n, bases, lookback, counter, ref, dbg);
+    run_ws<U, 512, 14, RANK_RUN2>(in, out, n, bases, lookback, counter, ref, dbg);
 #endif
 #ifdef TUNE_U64_SWEEP
     run<U, 256, 16, 2, true, RANK_STABLE, 8>(in, out, n, bases, lookback, counter, gcount, ref, dbg);
