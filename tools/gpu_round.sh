@@ -37,8 +37,8 @@ fi
 if has full; then
   PCMD="python tools/prof_sort.py --cfg cfg3 --reps 1"
   timeout 600 $PCMD > "$OUT/plain_prof.log" 2>&1 &&
-  # launch 4 of one cfg3 sort = pass 3, the stable (slowest) pass (0: pass 0, 1-2: the two
-  # pass-1 variants, 3: pass 2)
+  # launch 4 of one cfg3 sort = pass 3, the stable (slowest) pass, k_onesweep_pass_ws (0: pass 0,
+  # 1-2: the two pass-1 variants, 3: pass 2)
   timeout 1200 ncu --set full --clock-control none --import-source on -k regex:onesweep_pass -s 4 -c 1 \
       -o "$OUT/pass" $PCMD > "$OUT/ncu_full.log" 2>&1
   echo "ncu full pass exit $?" >> "$OUT/status.txt"
