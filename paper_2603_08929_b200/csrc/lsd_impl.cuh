@@ -38,11 +38,27 @@ template <int MODE, bool KV> struct PassCfg<unsigned long long, MODE, KV> {
   static constexpr int THREADS = 384, ITEMS = 12, MINB = KV ? 1 : 2, LBG = 8;
 };
 
+template <typename U, bool KV = false> struct WsCfg;
+template <> struct WsCfg<uint32_t, false> { static constexpr int RT = 512, ITEMS = 20; };
+template <> struct WsCfg<unsigned long long, false> { static constexpr int RT = 512, ITEMS = 14; };
+// key-value: three value buffers too; 512 x 16 (u32 keys, 192 KB + tables) / 512 x 10 (u64 keys)
+template <> struct WsCfg<uint32_t, true> { static constexpr int RT = 512, ITEMS = 12; };
+template <> struct WsCfg<unsigned long long, true> { static constexpr int RT = 512, ITEMS = 9; };
+
 template <typename U> constexpr int hist_lanes() { return sizeof(U) == 4 ? 32 : 16; }
 
 struct LsdLayout {
   size_t scratch, vscratch, ghist, bases, gcount, joint, seg, plan, counters, lookback, total;
+  uint64_t lb_tiles;  // look-back descriptor rows: tiles of the smallest look-back tile in use
 };
+
+// Smallest tile among the kernels that use the look-back array for (U, payload).
+template <typename U, bool KV>
+constexpr uint64_t lookback_tile() {
+  constexpr uint64_t a = (uint64_t)PassCfg<U, RANK_RUN2, KV>::THREADS * PassCfg<U, RANK_RUN2, KV>::ITEMS;
+  constexpr uint64_t b = (uint64_t)WsCfg<U, KV>::RT * WsCfg<U, KV>::ITEMS;
+  return a < b ? a : b;
+}
 
 // Pass 1 may run look-back-free (RANK_J01) from the joint histogram of digits 0 and 1; below
 // this size the digit-0 buckets are shorter than a tile anyway and the joint histogram's fixed
@@ -51,8 +67,7 @@ constexpr uint64_t JOINT_MIN_N = 1ull << 24;
 
 template <typename U>
 LsdLayout lsd_layout(uint64_t n, bool kv = false) {
-  using C = PassCfg<U, RANK_RUN2>;  // the look-back passes size the descriptor array
-  constexpr uint64_t TILE = (uint64_t)C::THREADS * C::ITEMS;
+  const uint64_t TILE = kv ? lookback_tile<U, true>() : lookback_tile<U, false>();
   constexpr int P = sizeof(U);
   const uint64_t tiles = (n + TILE - 1) / TILE;
   const size_t desc = (n <= (1ull << 30)) ? 4 : 8;
@@ -69,6 +84,7 @@ LsdLayout lsd_layout(uint64_t n, bool kv = false) {
   l.plan = off;     off = align_up(off + sizeof(PassPlan), 256);
   l.counters = off; off = align_up(off + 16 * 4, 256);
   l.lookback = off; off = align_up(off + tiles * 256 * desc, 256);
+  l.lb_tiles = tiles;
   l.total = off;
   return l;
 }
@@ -119,9 +135,7 @@ bsort_status_t launch_pass(const U* a, U* b, uint64_t n, DigitF digit, const uns
 // 223 KB of shared memory: stable 3.18 -> 2.51 ms, RUN2 2.73 -> 2.27 ms per 2^29 keys; x12: 2.77 /
 // 2.57).  RUN2's two-run condition holds for pass 2 of 2^30 keys (runs of ~16K keys).
 // BSORT_WS=0 selects k_onesweep_pass instead (A/B).
-template <typename U> struct WsCfg;
-template <> struct WsCfg<uint32_t> { static constexpr int RT = 512, ITEMS = 20; };
-template <> struct WsCfg<unsigned long long> { static constexpr int RT = 512, ITEMS = 14; };
+
 inline bool ws_enabled() {
   static const bool on = [] {
     const char* e = getenv("BSORT_WS");
@@ -130,14 +144,14 @@ inline bool ws_enabled() {
   return on;
 }
 
-template <typename U, typename DescT, typename DigitF>
+template <typename U, typename DescT, bool KV = false, typename DigitF>
 bsort_status_t launch_pass_ws(const U* a, U* b, uint64_t n, DigitF digit, const unsigned long long* bases,
-                              DescT* lookback, uint32_t* counter, const PassPlan* plan, int pass, cudaStream_t s) {
-  constexpr int WS_RT = WsCfg<U>::RT;
-  using L = PassSmemWS<WS_RT, WsCfg<U>::ITEMS, U>;
-  static_assert(L::TILE >= PassCfg<U, RANK_RUN2>::THREADS * PassCfg<U, RANK_RUN2>::ITEMS,
-                "no more tiles than the look-back array is sized for");
-  auto kern = k_onesweep_pass_ws<U, WS_RT, WsCfg<U>::ITEMS, DescT, DigitF, RANK_RUN2, 8>;
+                              DescT* lookback, uint32_t* counter, const PassPlan* plan, int pass, cudaStream_t s,
+                              KvPtrs kvp = {}) {
+  constexpr int WS_RT = WsCfg<U, KV>::RT;
+  using L = PassSmemWS<WS_RT, WsCfg<U, KV>::ITEMS, U, KV>;
+  static_assert(L::bytes <= 227 * 1024, "fits one CTA per SM");
+  auto kern = k_onesweep_pass_ws<U, WS_RT, WsCfg<U, KV>::ITEMS, DescT, DigitF, RANK_RUN2, 8, 1, KV>;
   static int occ = 0;
   if (occ == 0) {
     BSORT_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L::bytes));
@@ -149,7 +163,7 @@ bsort_status_t launch_pass_ws(const U* a, U* b, uint64_t n, DigitF digit, const 
   const uint64_t grid = min64(tiles, (uint64_t)num_sms() * occ);  // all resident (look-back progress)
   BSORT_LAUNCH(PROF_PASS, s,
                kern<<<(unsigned)grid, WS_RT + 256, L::bytes, s>>>(a, b, n, digit, bases, lookback, counter,
-                                                                  (uint32_t)tiles, plan, pass));
+                                                                  (uint32_t)tiles, plan, pass, kvp));
   return BSORT_SUCCESS;
 }
 
@@ -160,10 +174,10 @@ inline bsort_status_t memset_async(void* p, size_t bytes, cudaStream_t s) {
 
 template <int KIND, bool DESC, typename U, typename DescT, bool KV>
 bsort_status_t lsd_run(U* keys, uint32_t* vals, uint64_t n, unsigned char* ws, cudaStream_t s) {
-  using C = PassCfg<U, RANK_RUN2>;
+  // J01's eligibility (every nonzero digit-0 bucket at least one J01 tile) is planned for J01's tile
+  constexpr uint64_t J01_TILE = (uint64_t)PassCfg<U, RANK_J01, KV>::THREADS * PassCfg<U, RANK_J01, KV>::ITEMS;
   constexpr int P = sizeof(U);
   constexpr int LANES = hist_lanes<U>();
-  constexpr uint64_t TILE = (uint64_t)C::THREADS * C::ITEMS;
   const LsdLayout l = lsd_layout<U>(n, KV);
   U* scratch = reinterpret_cast<U*>(ws + l.scratch);
   const KvPtrs kvp{vals, reinterpret_cast<uint32_t*>(ws + l.vscratch)};
@@ -175,7 +189,6 @@ bsort_status_t lsd_run(U* keys, uint32_t* vals, uint64_t n, unsigned char* ws, c
   auto* plan = reinterpret_cast<PassPlan*>(ws + l.plan);
   auto* counters = reinterpret_cast<uint32_t*>(ws + l.counters);
   auto* lookback = reinterpret_cast<DescT*>(ws + l.lookback);
-  const uint64_t tiles = (n + TILE - 1) / TILE;
 
   static const bool joint_off = getenv("BSORT_NO_JOINT") != nullptr;  // A/B and debugging
   const bool use_joint = n >= JOINT_MIN_N && !joint_off;
@@ -204,14 +217,15 @@ bsort_status_t lsd_run(U* keys, uint32_t* vals, uint64_t n, unsigned char* ws, c
   BSORT_LAUNCH(PROF_SCAN, s,
                k_plan<<<1, 256, 0, s>>>(ghist, n, P, bases, plan, counters, gcount, use_joint ? joint : nullptr));
   if (use_joint)
-    BSORT_LAUNCH(PROF_SCAN, s, k_plan_joint<<<1, 256, 0, s>>>(joint, ghist, bases + 256, TILE, plan, seg));
+    BSORT_LAUNCH(PROF_SCAN, s,
+                 k_plan_joint<<<1, 256, 0, s>>>(joint, ghist, bases + 256, J01_TILE, plan, seg));
   bsort_status_t st = BSORT_SUCCESS;
   auto one_pass = [&](auto shift_c) {
     constexpr int SH = decltype(shift_c)::value;
     constexpr int p = SH / 8;
     if (p >= P || st != BSORT_SUCCESS) return;
     if constexpr (p > 0) {
-      st = memset_async(lookback, tiles * 256 * sizeof(DescT), s);
+      st = memset_async(lookback, l.lb_tiles * 256 * sizeof(DescT), s);
       if (st != BSORT_SUCCESS) return;
     }
     // The first LSD pass may order equal digits arbitrarily (the input order carries no
@@ -221,12 +235,11 @@ bsort_status_t lsd_run(U* keys, uint32_t* vals, uint64_t n, unsigned char* ws, c
                                                     lookback, gcount, counters, plan, p, s, kvp);
     else {
       bool done = false;
-      if constexpr (!KV) {
-        if (ws_enabled() && (uintptr_t)keys % 16 == 0) {  // TMA on both buffers (scratch is aligned)
-          st = launch_pass_ws<U, DescT>(keys, scratch, n, RadixDigit<KIND, DESC, U, SH>{}, bases + p * 256,
-                                        lookback, counters + p, plan, p, s);
-          done = true;
-        }
+      // TMA on both buffers (the scratch buffers are aligned)
+      if (ws_enabled() && (uintptr_t)keys % 16 == 0 && (!KV || (uintptr_t)vals % 16 == 0)) {
+        st = launch_pass_ws<U, DescT, KV>(keys, scratch, n, RadixDigit<KIND, DESC, U, SH>{}, bases + p * 256,
+                                          lookback, counters + p, plan, p, s, kvp);
+        done = true;
       }
       if (!done)
         st = launch_pass<U, RANK_RUN2, DescT, KV>(keys, scratch, n, RadixDigit<KIND, DESC, U, SH>{},

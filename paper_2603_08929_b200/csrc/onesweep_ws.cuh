@@ -51,7 +51,7 @@ __device__ __forceinline__ T group_exclusive_scan(T v, T* warp_tot) {
   return warp_tot[warp] + inc - v;
 }
 
-template <int RT, int ITEMS, typename U>
+template <int RT, int ITEMS, typename U, bool KV = false>
 struct PassSmemWS {
   static constexpr int RW = RT / 32;
   static constexpr int TILE = RT * ITEMS;
@@ -64,22 +64,25 @@ struct PassSmemWS {
   static constexpr size_t wt_off = align_up(gofs_off + 8 * 256, 16);        // u32[RW + 1], rankers
   static constexpr size_t mbar_off = align_up(wt_off + 4 * (RW + 1), 16);   // u64[3]
   static constexpr size_t tile_off = mbar_off + 32;                         // u32[3] tile id per buffer
-  static constexpr size_t bytes = align_up(tile_off + 16, 128);
+  static constexpr size_t vbuf_off = align_up(tile_off + 16, 128);          // KV: u32 values [3][TILE]
+  static constexpr size_t bytes = align_up(vbuf_off + (KV ? 3 * sizeof(uint32_t) * TILE : 0), 128);
 };
 
 constexpr uint32_t WS_BAR_R = 1, WS_BAR_W = 2, WS_BAR_STAGED = 3;  // + buffer index (3 ids)
 
-// Grid: one CTA of RT + 256 threads per SM (persistent).  BULK only (both ping-pong buffers
-// 16-byte aligned), no key-value payload, no remote write-out.
-template <typename U, int RT, int ITEMS, typename DescT, typename DigitF, int MODE, int LBG = 8, int MINB = 1>
+// Grid: one CTA of RT + 256 threads per SM (persistent).  BULK only (both ping-pong buffers, and
+// for KV both value buffers, 16-byte aligned), no remote write-out.  KV: a u32 payload per key
+// (§8 N3) is bulk-copied with its tile, restaged beside the keys and written out with them.
+template <typename U, int RT, int ITEMS, typename DescT, typename DigitF, int MODE, int LBG = 8, int MINB = 1,
+          bool KV = false>
 __global__ void __launch_bounds__(RT + 256, MINB)
     k_onesweep_pass_ws(const U* a_ptr, U* b_ptr, uint64_t n, DigitF digit,
                        const unsigned long long* __restrict__ bases, DescT* __restrict__ lookback,
                        uint32_t* __restrict__ tile_counter, uint32_t num_tiles, const PassPlan* __restrict__ plan,
-                       int pass) {
+                       int pass, KvPtrs kvp = {}) {
   static_assert(MODE == RANK_RUN2 || MODE == RANK_STABLE, "look-back modes only");
   static_assert(RT >= 256 && RT % 32 == 0, "at least one ranker per digit");
-  using L = PassSmemWS<RT, ITEMS, U>;
+  using L = PassSmemWS<RT, ITEMS, U, KV>;
   using LB = LookbackBits<DescT>;
   constexpr int TILE = L::TILE;
   constexpr int SEG = 32 * ITEMS;
@@ -97,9 +100,13 @@ __global__ void __launch_bounds__(RT + 256, MINB)
   uint32_t* wt = reinterpret_cast<uint32_t*>(smem + L::wt_off);
   uint64_t* mbar = reinterpret_cast<uint64_t*>(smem + L::mbar_off);
   volatile uint32_t* tile_s = reinterpret_cast<volatile uint32_t*>(smem + L::tile_off);
+  uint32_t* vbufs = reinterpret_cast<uint32_t*>(smem + L::vbuf_off);
+  (void)vbufs;
 
   const U* src = a_ptr;
   U* dst = b_ptr;
+  const uint32_t* vsrc = kvp.va;
+  uint32_t* vdst = kvp.vb;
   if (plan != nullptr) {
     if (plan->skip[pass]) return;
     if constexpr (MODE == RANK_RUN2) {
@@ -108,6 +115,8 @@ __global__ void __launch_bounds__(RT + 256, MINB)
     if (plan->src_alt[pass]) {
       src = b_ptr;
       dst = const_cast<U*>(a_ptr);
+      vsrc = kvp.vb;
+      vdst = const_cast<uint32_t*>(kvp.va);
     }
   }
   const uint32_t t = threadIdx.x;
@@ -119,14 +128,20 @@ __global__ void __launch_bounds__(RT + 256, MINB)
     return (uint32_t)((valid * sizeof(U)) & ~(size_t)15) / (uint32_t)sizeof(U);
   };
   // one thread: give buffer b the next tile (or, past the end, complete its phase empty)
+  auto bulk_vals = [&](uint32_t valid) -> uint32_t { return valid & ~3u; };
   auto refill = [&](int b) {
     const uint32_t id = atomicAdd(tile_counter, 1u);
     tile_s[b] = id;
-    if (id < num_tiles)
-      bulk_load(bufs + b * TILE, src + (uint64_t)id * TILE, bulk_keys(tile_valid(id)) * (uint32_t)sizeof(U),
-                &mbar[b]);
-    else
+    if (id < num_tiles) {
+      const uint32_t v = tile_valid(id);
+      if constexpr (KV)
+        bulk_load(bufs + b * TILE, src + (uint64_t)id * TILE, bulk_keys(v) * (uint32_t)sizeof(U), &mbar[b],
+                  vbufs + b * TILE, vsrc + (uint64_t)id * TILE, bulk_vals(v) * 4u);
+      else
+        bulk_load(bufs + b * TILE, src + (uint64_t)id * TILE, bulk_keys(v) * (uint32_t)sizeof(U), &mbar[b]);
+    } else {
       mbar_arrive(&mbar[b]);
+    }
   };
   if (t == 0) {
     for (int b = 0; b < 3; ++b) mbar_init(&mbar[b], 1);
@@ -159,12 +174,24 @@ __global__ void __launch_bounds__(RT + 256, MINB)
       // keys -> registers, half-warp index order (as k_onesweep_pass)
       const uint32_t seg = warp * SEG + half * (16 * ITEMS) + l16;
       U keys[ITEMS];
+      uint32_t vals[KV ? ITEMS : 1];
+      uint32_t* vbuf = vbufs + slot * TILE;
+      (void)vals;
+      (void)vbuf;
       U first_key = U(0), last_key = U(0);
       const uint32_t bk = bulk_keys(valid);
 #pragma unroll
       for (int k = 0; k < ITEMS; ++k) {
         const uint32_t i = seg + 16u * k;
         keys[k] = full ? buf[i] : (i < bk ? buf[i] : (i < valid ? ldg_nc(src + tile_base + i) : U(0)));
+      }
+      if constexpr (KV) {
+        const uint32_t bv = bulk_vals(valid);
+#pragma unroll
+        for (int k = 0; k < ITEMS; ++k) {
+          const uint32_t i = seg + 16u * k;
+          vals[k] = full ? vbuf[i] : (i < bv ? vbuf[i] : (i < valid ? ldg_nc(vsrc + tile_base + i) : 0u));
+        }
       }
       if constexpr (RUNS) {
         first_key = bk > 0 ? buf[0] : ldg_nc(src + tile_base);
@@ -269,11 +296,18 @@ __global__ void __launch_bounds__(RT + 256, MINB)
       if (unstable_rank) {
 #pragma unroll
         for (int k = 0; k < ITEMS; ++k)
-          if (info[k] != 0xFFFFFFFFu)
-            buf[bcnt[(info[k] & 0x1FFu) * BREP + (lane & (BREP - 1))] + (info[k] >> 9)] = keys[k];
+          if (info[k] != 0xFFFFFFFFu) {
+            const uint32_t pos = bcnt[(info[k] & 0x1FFu) * BREP + (lane & (BREP - 1))] + (info[k] >> 9);
+            buf[pos] = keys[k];
+            if constexpr (KV) vbuf[pos] = vals[k];
+          }
       } else {
 #pragma unroll
-        for (int k = 0; k < ITEMS; ++k) buf[wc[info[k] & 0xFFu] + (info[k] >> 9)] = keys[k];
+        for (int k = 0; k < ITEMS; ++k) {
+          const uint32_t pos = wc[info[k] & 0xFFu] + (info[k] >> 9);
+          buf[pos] = keys[k];
+          if constexpr (KV) vbuf[pos] = vals[k];
+        }
       }
       named_bar_arrive(WS_BAR_STAGED + slot, RT + 256);  // hand the staged tile to the writers
     }
@@ -285,6 +319,8 @@ __global__ void __launch_bounds__(RT + 256, MINB)
       const uint32_t tile = tile_s[slot];
       if (tile >= num_tiles) break;
       const U* buf = bufs + slot * TILE;
+      const uint32_t* vbuf = vbufs + slot * TILE;
+      (void)vbuf;
       named_bar_sync(WS_BAR_STAGED + slot, RT + 256);  // rankers staged this tile
       const uint2 m = meta[slot * 256 + w];
       DescT excl = 0;
@@ -298,7 +334,9 @@ __global__ void __launch_bounds__(RT + 256, MINB)
 #pragma unroll 4
       for (uint32_t i = w; i < valid; i += 256) {
         const U x = buf[i];
-        dst[gofs[digit(x)] + i] = x;
+        const unsigned long long o = gofs[digit(x)] + i;
+        dst[o] = x;
+        if constexpr (KV) vdst[o] = vbuf[i];
       }
       named_bar_sync(WS_BAR_W, 256);  // buffer and gofs fully read
       if (w == 0) refill((int)slot);
