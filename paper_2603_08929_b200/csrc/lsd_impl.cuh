@@ -144,14 +144,14 @@ inline bool ws_enabled() {
   return on;
 }
 
-template <typename U, typename DescT, bool KV = false, typename DigitF>
+template <typename U, typename DescT, bool KV = false, int MODE = RANK_RUN2, typename DigitF>
 bsort_status_t launch_pass_ws(const U* a, U* b, uint64_t n, DigitF digit, const unsigned long long* bases,
                               DescT* lookback, uint32_t* counter, const PassPlan* plan, int pass, cudaStream_t s,
-                              KvPtrs kvp = {}) {
+                              KvPtrs kvp = {}, unsigned long long* gcount = nullptr) {
   constexpr int WS_RT = WsCfg<U, KV>::RT;
   using L = PassSmemWS<WS_RT, WsCfg<U, KV>::ITEMS, U, KV>;
   static_assert(L::bytes <= 227 * 1024, "fits one CTA per SM");
-  auto kern = k_onesweep_pass_ws<U, WS_RT, WsCfg<U, KV>::ITEMS, DescT, DigitF, RANK_RUN2, 8, 1, KV>;
+  auto kern = k_onesweep_pass_ws<U, WS_RT, WsCfg<U, KV>::ITEMS, DescT, DigitF, MODE, 8, 1, KV>;
   static int occ = 0;
   if (occ == 0) {
     BSORT_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L::bytes));
@@ -163,7 +163,7 @@ bsort_status_t launch_pass_ws(const U* a, U* b, uint64_t n, DigitF digit, const 
   const uint64_t grid = min64(tiles, (uint64_t)num_sms() * occ);  // all resident (look-back progress)
   BSORT_LAUNCH(PROF_PASS, s,
                kern<<<(unsigned)grid, WS_RT + 256, L::bytes, s>>>(a, b, n, digit, bases, lookback, counter,
-                                                                  (uint32_t)tiles, plan, pass, kvp));
+                                                                  (uint32_t)tiles, plan, pass, kvp, gcount));
   return BSORT_SUCCESS;
 }
 
@@ -230,10 +230,22 @@ bsort_status_t lsd_run(U* keys, uint32_t* vals, uint64_t n, unsigned char* ws, c
     }
     // The first LSD pass may order equal digits arbitrarily (the input order carries no
     // information); every later pass must be stable.
-    if constexpr (p == 0)
-      st = launch_pass<U, RANK_UNSTABLE, DescT, KV>(keys, scratch, n, RadixDigit<KIND, DESC, U, SH>{}, bases,
-                                                    lookback, gcount, counters, plan, p, s, kvp);
-    else {
+    if constexpr (p == 0) {
+      // 64-bit keys: the warp-specialised kernel is faster for the unstable pass too (tune_pass
+      // -DTUNE_WS: 1.90 -> 1.78 ms per 2^29 keys); 32-bit keys keep two CTAs per SM (2.37 vs 2.81)
+      bool done = false;
+      if constexpr (sizeof(U) == 8 && !KV) {
+        if (ws_enabled() && (uintptr_t)keys % 16 == 0) {
+          st = launch_pass_ws<U, DescT, false, RANK_UNSTABLE>(keys, scratch, n, RadixDigit<KIND, DESC, U, SH>{},
+                                                              bases, lookback, counters, plan, p, s, KvPtrs{},
+                                                              gcount);
+          done = true;
+        }
+      }
+      if (!done)
+        st = launch_pass<U, RANK_UNSTABLE, DescT, KV>(keys, scratch, n, RadixDigit<KIND, DESC, U, SH>{}, bases,
+                                                      lookback, gcount, counters, plan, p, s, kvp);
+    } else {
       bool done = false;
       // TMA on both buffers (the scratch buffers are aligned)
       if (ws_enabled() && (uintptr_t)keys % 16 == 0 && (!KV || (uintptr_t)vals % 16 == 0)) {

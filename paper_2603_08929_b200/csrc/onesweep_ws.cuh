@@ -79,8 +79,9 @@ __global__ void __launch_bounds__(RT + 256, MINB)
     k_onesweep_pass_ws(const U* a_ptr, U* b_ptr, uint64_t n, DigitF digit,
                        const unsigned long long* __restrict__ bases, DescT* __restrict__ lookback,
                        uint32_t* __restrict__ tile_counter, uint32_t num_tiles, const PassPlan* __restrict__ plan,
-                       int pass, KvPtrs kvp = {}) {
-  static_assert(MODE == RANK_RUN2 || MODE == RANK_STABLE, "look-back modes only");
+                       int pass, KvPtrs kvp = {}, unsigned long long* __restrict__ gcount = nullptr) {
+  static_assert(MODE == RANK_RUN2 || MODE == RANK_STABLE || MODE == RANK_UNSTABLE, "no J01");
+  constexpr bool LOOKBACK = MODE != RANK_UNSTABLE;
   static_assert(RT >= 256 && RT % 32 == 0, "at least one ranker per digit");
   using L = PassSmemWS<RT, ITEMS, U, KV>;
   using LB = LookbackBits<DescT>;
@@ -166,9 +167,11 @@ __global__ void __launch_bounds__(RT + 256, MINB)
       const bool full = valid == (uint32_t)TILE;
       named_bar_sync(WS_BAR_R, RT);  // the previous tile's reads of the tables are done
 
+      if constexpr (MODE != RANK_UNSTABLE) {
 #pragma unroll
-      for (int j = 0; j < 16; ++j) wc[l16 + 16 * j] = 0;
-      if constexpr (MODE == RANK_RUN2)
+        for (int j = 0; j < 16; ++j) wc[l16 + 16 * j] = 0;
+      }
+      if constexpr (MODE != RANK_STABLE)
         for (int j = t; j < 512 * BREP / 4; j += RT) reinterpret_cast<uint4*>(bcnt)[j] = make_uint4(0, 0, 0, 0);
 
       // keys -> registers, half-warp index order (as k_onesweep_pass)
@@ -198,9 +201,11 @@ __global__ void __launch_bounds__(RT + 256, MINB)
         last_key = valid - 1 < bk ? buf[valid - 1] : ldg_nc(src + tile_base + valid - 1);
       }
 
-      bool unstable_rank = false;
+      bool unstable_rank = MODE == RANK_UNSTABLE;
       U low_first = U(0), low_last = U(0);
-      if constexpr (MODE == RANK_RUN2) {
+      if constexpr (MODE == RANK_UNSTABLE) {
+        named_bar_sync(WS_BAR_R, RT);  // counters zeroed before the atomics
+      } else if constexpr (MODE == RANK_RUN2) {
         U lo;
         digit.digit_low(first_key, &low_first);
         digit.digit_low(last_key, &low_last);
@@ -258,7 +263,8 @@ __global__ void __launch_bounds__(RT + 256, MINB)
           for (int h = 0; h < 2 * L::RW; ++h) total += rows[h * HW + t] >> 16;
           if (!full && t == 255) total -= (uint32_t)TILE - valid;
         }
-        st_relaxed(&lookback[(uint64_t)tile * 256 + t], (tile == 0 ? LB::INC : LB::AGG) | DescT(total));
+        if constexpr (LOOKBACK)
+          st_relaxed(&lookback[(uint64_t)tile * 256 + t], (tile == 0 ? LB::INC : LB::AGG) | DescT(total));
       }
       const uint32_t tile_excl = group_exclusive_scan<RT, WS_BAR_R>(t < 256 ? total : 0u, wt);
       if (t < 256) {
@@ -323,12 +329,17 @@ __global__ void __launch_bounds__(RT + 256, MINB)
       (void)vbuf;
       named_bar_sync(WS_BAR_STAGED + slot, RT + 256);  // rankers staged this tile
       const uint2 m = meta[slot * 256 + w];
-      DescT excl = 0;
-      if (tile > 0) {
-        excl = lookback_walk<LBG>(lookback, w, tile);
-        st_relaxed(&lookback[(uint64_t)tile * 256 + w], LB::INC | (excl + DescT(m.y)));
+      unsigned long long excl = 0;
+      if constexpr (LOOKBACK) {
+        if (tile > 0) {
+          const DescT e = lookback_walk<LBG>(lookback, w, tile);
+          st_relaxed(&lookback[(uint64_t)tile * 256 + w], LB::INC | (e + DescT(m.y)));
+          excl = (unsigned long long)e;
+        }
+      } else {
+        if (m.y) excl = atomicAdd(&gcount[w], (unsigned long long)m.y);  // tile order is free
       }
-      gofs[w] = bases[w] + (unsigned long long)excl - m.x;
+      gofs[w] = bases[w] + excl - m.x;
       named_bar_sync(WS_BAR_W, 256);
       const uint32_t valid = tile_valid(tile);
 #pragma unroll 4

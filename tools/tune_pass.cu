@@ -109,7 +109,7 @@ void run(const U* in, U* out, uint64_t n, const unsigned long long* bases, uint3
 
 template <typename U, int RT, int ITEMS, int RANK, int MINB = 1>
 void run_ws(const U* in, U* out, uint64_t n, const unsigned long long* bases, uint32_t* lookback, uint32_t* counter,
-            unsigned long long ref_sum, unsigned long long* dbg) {
+            unsigned long long ref_sum, unsigned long long* dbg, unsigned long long* gcount = nullptr) {
   using DigitF = RadixDigit<sizeof(U) == 4 ? KIND_F : KIND_I, false, U, 0>;
   using L = PassSmemWS<RT, ITEMS, U>;
   auto kern = k_onesweep_pass_ws<U, RT, ITEMS, uint32_t, DigitF, RANK, 8, MINB>;
@@ -128,8 +128,10 @@ void run_ws(const U* in, U* out, uint64_t n, const unsigned long long* bases, ui
   for (int r = 0; r < reps; ++r) {
     CK(cudaMemset(lookback, 0, tiles * 256 * 4));
     CK(cudaMemset(counter, 0, 4));
+    if (gcount) CK(cudaMemset(gcount, 0, 256 * 8));
     CK(cudaEventRecord(a));
-    kern<<<grid, RT + 256, L::bytes>>>(in, out, n, DigitF{}, bases, lookback, counter, (uint32_t)tiles, nullptr, 0);
+    kern<<<grid, RT + 256, L::bytes>>>(in, out, n, DigitF{}, bases, lookback, counter, (uint32_t)tiles, nullptr, 0,
+                                        KvPtrs{}, gcount);
     CK(cudaEventRecord(b));
     CK(cudaEventSynchronize(b));
     CK(cudaGetLastError());
@@ -195,6 +197,8 @@ void suite(uint64_t n) {
     run_ws<U, 512, 20, RANK_RUN2>(in, out, n, bases, lookback, counter, ref, dbg);
     run_ws<U, 512, 24, RANK_STABLE>(in, out, n, bases, lookback, counter, ref, dbg);
     run_ws<U, 512, 24, RANK_RUN2>(in, out, n, bases, lookback, counter, ref, dbg);
+    run_ws<U, 512, 20, RANK_UNSTABLE>(in, out, n, bases, lookback, counter, ref, dbg, gcount);
+    run_ws<U, 512, 16, RANK_UNSTABLE>(in, out, n, bases, lookback, counter, ref, dbg, gcount);
 #endif
     run<U, 512, 16, 2, true, RANK_STABLE, 8>(in, out, n, bases, lookback, counter, gcount, ref, dbg);
     run<U, 512, 16, 2, true, RANK_RUN2, 8>(in, out, n, bases, lookback, counter, gcount, ref, dbg);
@@ -214,6 +218,7 @@ void suite(uint64_t n) {
     run_ws<U, 512, 12, RANK_RUN2>(in, out, n, bases, lookback, counter, ref, dbg);
     run_ws<U, 512, 14, RANK_STABLE>(in, out, n, bases, lookback, counter, ref, dbg);
     run_ws<U, 512, 14, RANK_RUN2>(in, out, n, bases, lookback, counter, ref, dbg);
+    run_ws<U, 512, 14, RANK_UNSTABLE>(in, out, n, bases, lookback, counter, ref, dbg, gcount);
 #endif
 #ifdef TUNE_U64_SWEEP
     run<U, 256, 16, 2, true, RANK_STABLE, 8>(in, out, n, bases, lookback, counter, gcount, ref, dbg);
