@@ -4,13 +4,21 @@
 
 namespace bsort {
 
-bsort_status_t lsd_sort_w4(int kind, bool desc, void* keys, uint32_t* vals, uint64_t n, unsigned char* ws,
-                           cudaStream_t s);
-bsort_status_t lsd_sort_w4_kv(int kind, bool desc, void* keys, uint32_t* vals, uint64_t n, unsigned char* ws,
+bsort_status_t lsd_sort_w4_asc(int kind, void* keys, uint32_t* vals, uint64_t n, unsigned char* ws,
                               cudaStream_t s);
-bsort_status_t lsd_sort_w8(int kind, bool desc, void* keys, uint32_t* vals, uint64_t n, unsigned char* ws,
-                           cudaStream_t s);
-bsort_status_t lsd_sort_w8_kv(int kind, bool desc, void* keys, uint32_t* vals, uint64_t n, unsigned char* ws,
+bsort_status_t lsd_sort_w4_desc(int kind, void* keys, uint32_t* vals, uint64_t n, unsigned char* ws,
+                              cudaStream_t s);
+bsort_status_t lsd_sort_w4_kv_asc(int kind, void* keys, uint32_t* vals, uint64_t n, unsigned char* ws,
+                              cudaStream_t s);
+bsort_status_t lsd_sort_w4_kv_desc(int kind, void* keys, uint32_t* vals, uint64_t n, unsigned char* ws,
+                              cudaStream_t s);
+bsort_status_t lsd_sort_w8_asc(int kind, void* keys, uint32_t* vals, uint64_t n, unsigned char* ws,
+                              cudaStream_t s);
+bsort_status_t lsd_sort_w8_desc(int kind, void* keys, uint32_t* vals, uint64_t n, unsigned char* ws,
+                              cudaStream_t s);
+bsort_status_t lsd_sort_w8_kv_asc(int kind, void* keys, uint32_t* vals, uint64_t n, unsigned char* ws,
+                              cudaStream_t s);
+bsort_status_t lsd_sort_w8_kv_desc(int kind, void* keys, uint32_t* vals, uint64_t n, unsigned char* ws,
                               cudaStream_t s);
 
 size_t lsd_workspace_bytes(int bytes, uint64_t n, bool kv) {
@@ -23,9 +31,13 @@ bsort_status_t lsd_sort(const DtypeInfo& di, void* keys, uint32_t* vals, uint64_
                         size_t ws_bytes, cudaStream_t s) {
   if (ws_bytes < lsd_workspace_bytes(di.bytes, n, vals != nullptr)) return BSORT_ERROR_WORKSPACE_TOO_SMALL;
   auto* w = static_cast<unsigned char*>(ws);
-  if (di.bytes == 4)
-    return vals ? lsd_sort_w4_kv(di.kind, desc, keys, vals, n, w, s) : lsd_sort_w4(di.kind, desc, keys, nullptr, n, w, s);
-  return vals ? lsd_sort_w8_kv(di.kind, desc, keys, vals, n, w, s) : lsd_sort_w8(di.kind, desc, keys, nullptr, n, w, s);
+  const int k = di.kind;
+  if (di.bytes == 4) {
+    if (vals) return desc ? lsd_sort_w4_kv_desc(k, keys, vals, n, w, s) : lsd_sort_w4_kv_asc(k, keys, vals, n, w, s);
+    return desc ? lsd_sort_w4_desc(k, keys, nullptr, n, w, s) : lsd_sort_w4_asc(k, keys, nullptr, n, w, s);
+  }
+  if (vals) return desc ? lsd_sort_w8_kv_desc(k, keys, vals, n, w, s) : lsd_sort_w8_kv_asc(k, keys, vals, n, w, s);
+  return desc ? lsd_sort_w8_desc(k, keys, nullptr, n, w, s) : lsd_sort_w8_asc(k, keys, nullptr, n, w, s);
 }
 
 }  // namespace bsort

@@ -1,6 +1,6 @@
 // lsd_impl.cuh — host orchestration of the 32/64-bit one-sweep LSD path (§8 rows a2-a5) and the
-// launch helpers shared with the MSD partition.  Included by the per-(key width, payload)
-// translation units lsd_w4.cu, lsd_w4_kv.cu, lsd_w8.cu, lsd_w8_kv.cu and by dist.cu, so the
+// launch helpers shared with the MSD partition.  Included by the per-(key width, payload,
+// direction) translation units lsd_w{4,8}[_kv]_{asc,desc}.cu and by dist.cu / exact.cu, so the
 // kernel instantiations compile in parallel.
 //
 //   memset(hist) -> k_onesweep_hist[_joint] -> k_plan [-> k_plan_joint]
@@ -290,20 +290,17 @@ bsort_status_t lsd_dispatch_desc(U* keys, uint32_t* vals, uint64_t n, unsigned c
   return lsd_run<KIND, DESC, U, unsigned long long, KV>(keys, vals, n, ws, s);
 }
 
-// Instantiates the whole LSD path for one key width and payload mode (one translation unit each).
-template <typename U, bool KV>
-bsort_status_t lsd_dispatch(int kind, bool desc, U* keys, uint32_t* vals, uint64_t n, unsigned char* ws,
-                            cudaStream_t s) {
+// Instantiates the LSD path for one key width, payload mode and direction (one translation unit
+// each, so the 64-bit instantiations -- the longest -- compile in parallel halves).
+template <typename U, bool KV, bool DESC>
+bsort_status_t lsd_dispatch(int kind, U* keys, uint32_t* vals, uint64_t n, unsigned char* ws, cudaStream_t s) {
   switch (kind) {
     case KIND_U:
-      return desc ? lsd_dispatch_desc<KIND_U, true, U, KV>(keys, vals, n, ws, s)
-                  : lsd_dispatch_desc<KIND_U, false, U, KV>(keys, vals, n, ws, s);
+      return lsd_dispatch_desc<KIND_U, DESC, U, KV>(keys, vals, n, ws, s);
     case KIND_I:
-      return desc ? lsd_dispatch_desc<KIND_I, true, U, KV>(keys, vals, n, ws, s)
-                  : lsd_dispatch_desc<KIND_I, false, U, KV>(keys, vals, n, ws, s);
+      return lsd_dispatch_desc<KIND_I, DESC, U, KV>(keys, vals, n, ws, s);
     default:
-      return desc ? lsd_dispatch_desc<KIND_F, true, U, KV>(keys, vals, n, ws, s)
-                  : lsd_dispatch_desc<KIND_F, false, U, KV>(keys, vals, n, ws, s);
+      return lsd_dispatch_desc<KIND_F, DESC, U, KV>(keys, vals, n, ws, s);
   }
 }
 
