@@ -30,8 +30,12 @@ template <int MODE, bool KV> struct PassCfg<uint32_t, MODE, KV> {
 };
 // The first LSD pass and the MSD partitions (unstable, no look-back): 10240-key tiles rank a
 // little faster (tools/tune_pass -DTUNE_UNSTABLE: 2.45 -> 2.37 ms per 2^30 keys; x24 spills).
-// J01 keeps 8192 (its eligibility is planned for RUN2's tile) and so do the look-back passes.
+// The two-CTA look-back kernel keeps 8192 (the look-back array is sized for it).
 template <> struct PassCfg<uint32_t, RANK_UNSTABLE, false> {
+  static constexpr int THREADS = 512, ITEMS = 20, MINB = 2, LBG = 8;
+};
+// J01 (pass 1 without look-back) likewise; its eligibility is planned for this tile (J01_TILE).
+template <> struct PassCfg<uint32_t, RANK_J01, false> {
   static constexpr int THREADS = 512, ITEMS = 20, MINB = 2, LBG = 8;
 };
 template <int MODE, bool KV> struct PassCfg<unsigned long long, MODE, KV> {

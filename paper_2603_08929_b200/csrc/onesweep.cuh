@@ -444,7 +444,8 @@ struct PassSmem {
   // multisplit tables: per half-warp 256 words {count:16 | mask:16} (+16 words of padding so the
   // two halves of a warp start 16 banks apart); 512 x BREP block counters
   static constexpr int HALF_WORDS = 272;
-  static constexpr int rows = MODE == RANK_UNSTABLE ? 0 : WARPS;
+  // multisplit tables only where a tile may rank stably (J01 and unstable never do)
+  static constexpr int rows = (MODE == RANK_STABLE || MODE == RANK_RUN2) ? WARPS : 0;
   static constexpr size_t buf_off = 0;  // U[2][TILE]
   static constexpr size_t rows_off = align_up(buf_off + 2 * sizeof(U) * TILE, 16);
   static constexpr size_t bcnt_off = align_up(rows_off + 2 * HALF_WORDS * 4 * rows, 16);
@@ -611,7 +612,7 @@ __global__ void __launch_bounds__(THREADS, MINB)
     const bool full = valid == (uint32_t)TILE;
 
     // zero the counters (every read of them happened before the previous tile's last barrier)
-    if constexpr (MODE != RANK_UNSTABLE) {  // both half tables of this warp
+    if constexpr (MODE == RANK_STABLE || MODE == RANK_RUN2) {  // both half tables of this warp
 #pragma unroll
       for (int j = 0; j < 16; ++j) wc[l16 + 16 * j] = 0;
     }
@@ -724,7 +725,7 @@ __global__ void __launch_bounds__(THREADS, MINB)
           info[k] = 0xFFFFFFFFu;
         }
       }
-    } else if constexpr (MODE != RANK_UNSTABLE) {
+    } else if constexpr (MODE == RANK_STABLE || MODE == RANK_RUN2) {
       // Invalid tail slots take digit 255: they sit at the end of the tile in index order, so
       // they rank after every valid key of digit 255 and are dropped at write-out.
       __syncwarp();  // tables zeroed by this warp
