@@ -167,7 +167,7 @@ __global__ void __launch_bounds__(RT + 256, MINB)
       const bool full = valid == (uint32_t)TILE;
       named_bar_sync(WS_BAR_R, RT);  // the previous tile's reads of the tables are done
 
-      if constexpr (MODE != RANK_UNSTABLE) {
+      if constexpr (MODE == RANK_STABLE) {
 #pragma unroll
         for (int j = 0; j < 16; ++j) wc[l16 + 16 * j] = 0;
       }
@@ -232,6 +232,11 @@ __global__ void __launch_bounds__(RT + 256, MINB)
           }
         }
       } else {
+        if constexpr (MODE == RANK_RUN2) {  // a RUN2 tile that falls back: zero this warp's tables
+          // now (the previous tile's reads of them ended before its barrier B / our restage)
+#pragma unroll
+          for (int j = 0; j < 16; ++j) wc[l16 + 16 * j] = 0;
+        }
         __syncwarp();
 #pragma unroll
         for (int k = 0; k < ITEMS; ++k) {
