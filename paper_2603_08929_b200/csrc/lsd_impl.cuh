@@ -38,6 +38,9 @@ template <> struct PassCfg<uint32_t, RANK_UNSTABLE, false> {
 template <> struct PassCfg<uint32_t, RANK_J01, false> {
   static constexpr int THREADS = 512, ITEMS = 20, MINB = 2, LBG = 8;
 };
+template <> struct PassCfg<unsigned long long, RANK_J01, false> {
+  static constexpr int THREADS = 512, ITEMS = 12, MINB = 2, LBG = 8;
+};
 template <int MODE, bool KV> struct PassCfg<unsigned long long, MODE, KV> {
   static constexpr int THREADS = 384, ITEMS = 12, MINB = KV ? 1 : 2, LBG = 8;
 };
@@ -198,7 +201,7 @@ bsort_status_t lsd_run(U* keys, uint32_t* vals, uint64_t n, unsigned char* ws, c
   const bool use_joint = n >= JOINT_MIN_N && !joint_off;
   BSORT_LAUNCH(PROF_MEMSET, s, cudaMemsetAsync(ghist, 0, P * 256 * 8, s));
   if (use_joint) {
-    constexpr int JL = sizeof(U) == 4 ? 32 : 8;  // lanes of the digit >= 2 counters
+    constexpr int JL = sizeof(U) == 4 ? 32 : 16;  // lanes of the digit >= 2 counters (224 KB for u64)
     auto hk = k_onesweep_hist_joint<KIND, DESC, U, JL>;
     constexpr int hsmem = (32768 + (P - 2) * 256 * JL) * 4;
     static bool hattr = false;
