@@ -143,6 +143,9 @@ bsort_status_t launch_pass(const U* a, U* b, uint64_t n, DigitF digit, const uns
 // 2.57).  RUN2's two-run condition holds for pass 2 of 2^30 keys (runs of ~16K keys).
 // BSORT_WS=0 selects k_onesweep_pass instead (A/B).
 
+// Below this size a pass has too few tiles to keep the walk off the critical path anyway, and
+// the two-CTA kernel's smaller tiles spread a small input over more SMs (cfg1: 2^20 keys).
+constexpr uint64_t WS_MIN_N = 1ull << 22;
 inline bool ws_enabled() {
   static const bool on = [] {
     const char* e = getenv("BSORT_WS");
@@ -242,7 +245,7 @@ bsort_status_t lsd_run(U* keys, uint32_t* vals, uint64_t n, unsigned char* ws, c
       // -DTUNE_WS: 1.90 -> 1.78 ms per 2^29 keys); 32-bit keys keep two CTAs per SM (2.37 vs 2.81)
       bool done = false;
       if constexpr (sizeof(U) == 8 && !KV) {
-        if (ws_enabled() && (uintptr_t)keys % 16 == 0) {
+        if (n >= WS_MIN_N && ws_enabled() && (uintptr_t)keys % 16 == 0) {
           st = launch_pass_ws<U, DescT, false, RANK_UNSTABLE>(keys, scratch, n, RadixDigit<KIND, DESC, U, SH>{},
                                                               bases, lookback, counters, plan, p, s, KvPtrs{},
                                                               gcount);
@@ -255,7 +258,7 @@ bsort_status_t lsd_run(U* keys, uint32_t* vals, uint64_t n, unsigned char* ws, c
     } else {
       bool done = false;
       // TMA on both buffers (the scratch buffers are aligned)
-      if (ws_enabled() && (uintptr_t)keys % 16 == 0 && (!KV || (uintptr_t)vals % 16 == 0)) {
+      if (n >= WS_MIN_N && ws_enabled() && (uintptr_t)keys % 16 == 0 && (!KV || (uintptr_t)vals % 16 == 0)) {
         st = launch_pass_ws<U, DescT, KV>(keys, scratch, n, RadixDigit<KIND, DESC, U, SH>{}, bases + p * 256,
                                           lookback, counters + p, plan, p, s, kvp);
         done = true;
