@@ -304,3 +304,27 @@ def test_cuda_graph_capture_and_replay(B, dtype, n):
         g.replay()
         torch.cuda.synchronize()
         assert host(buf).tobytes() == ref.tobytes(), f"replay {seed}"
+
+
+@pytest.mark.parametrize("dtype", [torch.uint32, torch.float32, torch.int64, torch.float64],
+                         ids=lambda d: str(d).split(".")[-1])
+@pytest.mark.parametrize("descending", [False, True], ids=["asc", "desc"])
+def test_warp_specialised_sizes(B, dtype, descending):
+    """n >= 2^22 routes the look-back passes (and 64-bit pass 0) through k_onesweep_pass_ws:
+    ragged last tiles of its 10240 / 7168-key tiles, trivial high digits, and the key-value form."""
+    for n in ((1 << 22) + 1, (1 << 22) + 10239, 3 * (1 << 22) + 7167):
+        check_equal(B, gen(dtype, n, n % 1000), descending, f"ws n={n}")
+    es = torch.empty(0, dtype=dtype).element_size()
+    ib = {4: torch.int32, 8: torch.int64}[es]
+    low = (W.bits((1 << 22) + 5, 31, "cuda") & 0xFFFFF).to(ib).view(dtype)  # top digits trivial
+    check_equal(B, low, descending, "ws trivial digits")
+    keys = gen(dtype, (1 << 22) + 333, 32)
+    ref = oracle.sort_native(host(keys), descending=descending)
+    vals = torch.arange(keys.numel(), dtype=torch.int32, device="cuda")
+    orig = host(keys).copy()
+    B.sort_pairs_(keys, vals, descending)
+    torch.cuda.synchronize()
+    assert host(keys).tobytes() == ref.tobytes()
+    v = vals.cpu().numpy()
+    assert np.array_equal(np.sort(v), np.arange(v.size))
+    assert orig[v].tobytes() == ref.tobytes()  # every value followed its key
