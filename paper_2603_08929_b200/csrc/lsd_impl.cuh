@@ -82,7 +82,7 @@ LsdLayout lsd_layout(uint64_t n, bool kv = false) {
   size_t off = 0;
   l.scratch = off;  off = align_up(off + n * sizeof(U), 256);
   l.vscratch = off; off = align_up(off + (kv ? n * sizeof(uint32_t) : 0), 256);
-  l.ghist = off;    off = align_up(off + P * 256 * 8, 256);
+  l.ghist = off;    off = align_up(off + P * 256 * 8 + 16, 256);  // + the two order flags
   l.bases = off;    off = align_up(off + P * 256 * 8, 256);
   l.gcount = off;   off = align_up(off + P * 256 * 8, 256);
   const size_t jbytes = n >= JOINT_MIN_N ? 65536 * 8 : 0;  // joint histogram + segment starts
@@ -202,7 +202,9 @@ bsort_status_t lsd_run(U* keys, uint32_t* vals, uint64_t n, unsigned char* ws, c
 
   static const bool joint_off = getenv("BSORT_NO_JOINT") != nullptr;  // A/B and debugging
   const bool use_joint = n >= JOINT_MIN_N && !joint_off;
-  BSORT_LAUNCH(PROF_MEMSET, s, cudaMemsetAsync(ghist, 0, P * 256 * 8, s));
+  // digit histograms and, right after them, the presorted-input flags (k_onesweep_hist*)
+  auto* order = reinterpret_cast<uint32_t*>(ghist + P * 256);
+  BSORT_LAUNCH(PROF_MEMSET, s, cudaMemsetAsync(ghist, 0, P * 256 * 8 + 16, s));
   if (use_joint) {
     constexpr int JL = sizeof(U) == 4 ? 32 : 16;  // lanes of the digit >= 2 counters (224 KB for u64)
     auto hk = k_onesweep_hist_joint<KIND, DESC, U, JL>;
@@ -213,7 +215,7 @@ bsort_status_t lsd_run(U* keys, uint32_t* vals, uint64_t n, unsigned char* ws, c
       hattr = true;
     }
     BSORT_LAUNCH(PROF_MEMSET, s, cudaMemsetAsync(joint, 0, 65536 * 8, s));
-    BSORT_LAUNCH(PROF_HIST, s, hk<<<num_sms(), HIST_THREADS, hsmem, s>>>(keys, n, ghist, joint));
+    BSORT_LAUNCH(PROF_HIST, s, hk<<<num_sms(), HIST_THREADS, hsmem, s>>>(keys, n, ghist, joint, order));
   } else {
     auto hk = k_onesweep_hist<KIND, DESC, U, LANES>;
     constexpr int hsmem = P * 256 * LANES * 4;
@@ -222,10 +224,11 @@ bsort_status_t lsd_run(U* keys, uint32_t* vals, uint64_t n, unsigned char* ws, c
       BSORT_CUDA(cudaFuncSetAttribute(hk, cudaFuncAttributeMaxDynamicSharedMemorySize, hsmem));
       hattr = true;
     }
-    BSORT_LAUNCH(PROF_HIST, s, hk<<<num_sms(), HIST_THREADS, hsmem, s>>>(keys, n, ghist));
+    BSORT_LAUNCH(PROF_HIST, s, hk<<<num_sms(), HIST_THREADS, hsmem, s>>>(keys, n, ghist, order));
   }
   BSORT_LAUNCH(PROF_SCAN, s,
-               k_plan<<<1, 256, 0, s>>>(ghist, n, P, bases, plan, counters, gcount, use_joint ? joint : nullptr));
+               k_plan<<<1, 256, 0, s>>>(ghist, n, P, bases, plan, counters, gcount, use_joint ? joint : nullptr,
+                                        order));
   if (use_joint)
     BSORT_LAUNCH(PROF_SCAN, s,
                  k_plan_joint<<<1, 256, 0, s>>>(joint, ghist, bases + 256, J01_TILE, plan, seg));

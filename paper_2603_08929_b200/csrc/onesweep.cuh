@@ -107,7 +107,62 @@ struct PassPlan {
   uint32_t final_copy;  // odd number of executed passes: result is in scratch, copy back
   uint32_t executed;    // number of executed passes
   uint32_t j01;         // pass 1 runs as RANK_J01 (every nonzero digit-0 bucket >= one tile)
-  uint32_t pad[13];
+  uint32_t reverse;     // input already in the opposite order: no pass, k_copy_back reverses
+  uint32_t pad[12];
+};
+
+// Presorted-input check (§8 a3 "sortedness test"), folded into the histogram sweep: for every
+// adjacent pair (j, j+1) of the input, order[0] |= enc(x_j) > enc(x_j+1) (not already in the
+// requested order) and order[1] |= enc(x_j) < enc(x_j+1) (not in the opposite order).  The key
+// order is a total order on bit patterns, so an input with order[0] == 0 IS the sorted output,
+// and one with order[1] == 0 reversed is (equal keys have equal bits).
+struct OrderFlags {
+  uint32_t up = 0, down = 0;
+  template <typename U>
+  __device__ __forceinline__ void pair(U a, U b) {  // encoded keys, a before b
+    up |= a > b;
+    down |= a < b;
+  }
+  __device__ __forceinline__ bool done() const { return up & down; }  // both set: nothing to learn
+  // keys kv[0..V) at positions j0.., plus the pair (kv[V-1], x[j0+V]); once this thread has seen
+  // both violations (any unsorted input, within a vector or two) the check is skipped.  The
+  // next vector's first key comes from the next lane when it is active (consecutive lanes hold
+  // consecutive vectors), else from memory.
+  template <int KIND, bool DESC, typename U, int V>
+  __device__ __forceinline__ void vector(const U (&kv)[V], uint64_t j0, const U* keys, uint64_t n) {
+    const uint32_t m = __activemask();
+    if (__all_sync(m, done())) return;  // the common case for unsorted input: one vote
+    const uint32_t lane = threadIdx.x & 31;
+    const U nb = shfl_down_u(m, kv[0]);
+    if (done()) return;
+    U e[V];
+#pragma unroll
+    for (int j = 0; j < V; ++j) e[j] = key_encode<KIND, DESC>(kv[j]);
+#pragma unroll
+    for (int j = 0; j + 1 < V; ++j) pair(e[j], e[j + 1]);
+    const uint64_t nx = j0 + V;
+    if (nx < n) {
+      const bool have = lane < 31 && ((m >> (lane + 1)) & 1u);
+      pair(e[V - 1], key_encode<KIND, DESC>(have ? nb : keys[nx]));
+    }
+  }
+  template <typename U>
+  static __device__ __forceinline__ U shfl_down_u(uint32_t m, U v) {
+    if constexpr (sizeof(U) == 4) {
+      return U(__shfl_down_sync(m, (uint32_t)v, 1));
+    } else {
+      const uint32_t lo = __shfl_down_sync(m, (uint32_t)v, 1), hi = __shfl_down_sync(m, (uint32_t)(v >> 32), 1);
+      return U(lo) | (U(hi) << 32);
+    }
+  }
+  // block-wide reduce + one atomic per block (every thread of the block must call it)
+  __device__ __forceinline__ void flush(uint32_t* order) {
+    const int u = __syncthreads_or(up), d = __syncthreads_or(down);
+    if (threadIdx.x == 0 && order != nullptr) {
+      if (u) atomicOr(&order[0], 1u);
+      if (d) atomicOr(&order[1], 1u);
+    }
+  }
 };
 
 // Digit of LSD pass p: byte p of the transformed key (SHIFT = 8p is a compile-time constant so
@@ -162,8 +217,14 @@ constexpr int HIST_THREADS = 1024;
 
 template <int KIND, bool DESC, typename U, int LANES>
 __global__ void __launch_bounds__(HIST_THREADS, 1)
-    k_onesweep_hist(const U* __restrict__ keys, uint64_t n, unsigned long long* __restrict__ ghist) {
+    k_onesweep_hist(const U* __restrict__ keys, uint64_t n, unsigned long long* __restrict__ ghist,
+                    uint32_t* __restrict__ order = nullptr) {
   constexpr int P = sizeof(U);
+  OrderFlags of;
+  // pair (j, j+1) for a scalar key j
+  auto check1 = [&](uint64_t j, U kj) {
+    if (j + 1 < n) of.pair(kj, key_encode<KIND, DESC>(ldg_nc(keys + j + 1)));
+  };
   extern __shared__ uint32_t hs[];  // [P][256][LANES]
   for (int i = threadIdx.x; i < P * 256 * LANES; i += HIST_THREADS) hs[i] = 0;
   __syncthreads();
@@ -183,21 +244,31 @@ __global__ void __launch_bounds__(HIST_THREADS, 1)
   for (uint64_t i = gt; i < head; i += T) add(keys[i]);
   const uint4* v = reinterpret_cast<const uint4*>(keys + head);
   const uint64_t nv = (n - head) / PER_VEC;
-  auto vec = [&](uint4 q) {
+  // vector i: its keys, the pairs inside it and the pair (its last key, the next key)
+  auto vec = [&](uint4 q, uint64_t i) {
+    U kv[PER_VEC];
     if constexpr (sizeof(U) == 4) {
-      add(U(q.x)); add(U(q.y)); add(U(q.z)); add(U(q.w));
+      kv[0] = U(q.x); kv[1] = U(q.y); kv[2] = U(q.z); kv[3] = U(q.w);
     } else {
-      add(U(q.x) | (U(q.y) << 32));
-      add(U(q.z) | (U(q.w) << 32));
+      kv[0] = U(q.x) | (U(q.y) << 32);
+      kv[1] = U(q.z) | (U(q.w) << 32);
     }
+#pragma unroll
+    for (int j = 0; j < PER_VEC; ++j) add(kv[j]);
+    of.vector<KIND, DESC>(kv, head + i * PER_VEC, keys, n);
   };
+  for (uint64_t i = gt; i < head; i += T) check1(i, key_encode<KIND, DESC>(keys[i]));
   uint64_t i = gt;
   for (; i + 3 * T < nv; i += 4 * T) {
     uint4 q0 = __ldcs(v + i), q1 = __ldcs(v + i + T), q2 = __ldcs(v + i + 2 * T), q3 = __ldcs(v + i + 3 * T);
-    vec(q0); vec(q1); vec(q2); vec(q3);
+    vec(q0, i); vec(q1, i + T); vec(q2, i + 2 * T); vec(q3, i + 3 * T);
   }
-  for (; i < nv; i += T) vec(__ldcs(v + i));
-  for (uint64_t j = head + nv * PER_VEC + gt; j < n; j += T) add(keys[j]);
+  for (; i < nv; i += T) vec(__ldcs(v + i), i);
+  for (uint64_t j = head + nv * PER_VEC + gt; j < n; j += T) {
+    add(keys[j]);
+    check1(j, key_encode<KIND, DESC>(keys[j]));
+  }
+  of.flush(order);
   __syncthreads();
   for (int b = threadIdx.x; b < P * 256; b += HIST_THREADS) {
     uint32_t s = 0;
@@ -216,8 +287,12 @@ __global__ void __launch_bounds__(HIST_THREADS, 1)
 template <int KIND, bool DESC, typename U, int LANES>
 __global__ void __launch_bounds__(HIST_THREADS, 1)
     k_onesweep_hist_joint(const U* __restrict__ keys, uint64_t n, unsigned long long* __restrict__ ghist,
-                          unsigned long long* __restrict__ gjoint) {
+                          unsigned long long* __restrict__ gjoint, uint32_t* __restrict__ order = nullptr) {
   constexpr int P = sizeof(U);
+  OrderFlags of;
+  auto check1 = [&](uint64_t j, U kj) {
+    if (j + 1 < n) of.pair(kj, key_encode<KIND, DESC>(ldg_nc(keys + j + 1)));
+  };
   extern __shared__ uint32_t hs[];  // [32768 joint words][P-2][256][LANES]
   uint32_t* hj = hs;
   uint32_t* hd = hs + 32768;
@@ -278,32 +353,49 @@ __global__ void __launch_bounds__(HIST_THREADS, 1)
   for (uint64_t i = gt; i < head; i += T) add(keys[i]);
   const uint4* v = reinterpret_cast<const uint4*>(keys + head);
   const uint64_t nv = (n - head) / PER_VEC;
-  auto vec = [&](uint4 q) {
+  auto order_vec = [&](const U (&kv)[PER_VEC], uint64_t i) { of.vector<KIND, DESC>(kv, head + i * PER_VEC, keys, n); };
+  auto vec = [&](uint4 q, uint64_t i, bool check) {
     if constexpr (sizeof(U) == 4) {
       const U kv[4] = {U(q.x), U(q.y), U(q.z), U(q.w)};
       add_vec(kv);
+      if (check) order_vec(kv, i);
     } else {
       const U kv[2] = {U(q.x) | (U(q.y) << 32), U(q.z) | (U(q.w) << 32)};
       add_vec(kv);
+      if (check) order_vec(kv, i);
     }
   };
+  for (uint64_t i = gt; i < head; i += T) check1(i, key_encode<KIND, DESC>(keys[i]));
   // whole warps iterate together (collectives inside): the loop bound is warp-uniform
   const uint64_t wbase = gt & ~uint64_t(31);
   uint64_t i = gt;
+  // order check only until every lane of the warp has seen both violations (an unsorted input:
+  // the first iteration or two), then the plain loop
+  for (; wbase + (i - gt) + 3 * T + 31 < nv && !__all_sync(0xffffffffu, of.done()); i += 4 * T) {
+    uint4 q0 = __ldcs(v + i), q1 = __ldcs(v + i + T), q2 = __ldcs(v + i + 2 * T), q3 = __ldcs(v + i + 3 * T);
+    vec(q0, i, true); vec(q1, i + T, true); vec(q2, i + 2 * T, true); vec(q3, i + 3 * T, true);
+  }
   for (; wbase + (i - gt) + 3 * T + 31 < nv; i += 4 * T) {
     uint4 q0 = __ldcs(v + i), q1 = __ldcs(v + i + T), q2 = __ldcs(v + i + 2 * T), q3 = __ldcs(v + i + 3 * T);
-    vec(q0); vec(q1); vec(q2); vec(q3);
+    vec(q0, i, false); vec(q1, i + T, false); vec(q2, i + 2 * T, false); vec(q3, i + 3 * T, false);
   }
   for (; i < nv; i += T) {  // remaining vectors: per key (a warp may be partial here)
     const uint4 q = __ldcs(v + i);
     if constexpr (sizeof(U) == 4) {
-      add(U(q.x)); add(U(q.y)); add(U(q.z)); add(U(q.w));
+      const U kv[4] = {U(q.x), U(q.y), U(q.z), U(q.w)};
+      add(kv[0]); add(kv[1]); add(kv[2]); add(kv[3]);
+      order_vec(kv, i);
     } else {
-      add(U(q.x) | (U(q.y) << 32));
-      add(U(q.z) | (U(q.w) << 32));
+      const U kv[2] = {U(q.x) | (U(q.y) << 32), U(q.z) | (U(q.w) << 32)};
+      add(kv[0]); add(kv[1]);
+      order_vec(kv, i);
     }
   }
-  for (uint64_t j = head + nv * PER_VEC + gt; j < n; j += T) add(keys[j]);
+  for (uint64_t j = head + nv * PER_VEC + gt; j < n; j += T) {
+    add(keys[j]);
+    check1(j, key_encode<KIND, DESC>(keys[j]));
+  }
+  of.flush(order);
   __syncthreads();
   for (int w = threadIdx.x; w < 32768; w += HIST_THREADS) {
     const uint32_t c = hj[w];
@@ -348,7 +440,8 @@ static __global__ void __launch_bounds__(256)
 static __global__ void __launch_bounds__(256)
     k_plan(unsigned long long* __restrict__ ghist, uint64_t n, int P, unsigned long long* __restrict__ bases,
            PassPlan* __restrict__ plan, uint32_t* __restrict__ tile_counters,
-           unsigned long long* __restrict__ gcount, const unsigned long long* __restrict__ gjoint) {
+           unsigned long long* __restrict__ gcount, const unsigned long long* __restrict__ gjoint,
+           const uint32_t* __restrict__ order = nullptr) {
   __shared__ unsigned long long wt[256 / 32 + 1];
   __shared__ uint32_t skip_s[8];
   if (gjoint != nullptr) {  // marginals of digits 1 (row sums) and 0 (column sums) of J[d1][d0]
@@ -387,6 +480,18 @@ static __global__ void __launch_bounds__(256)
     plan->final_copy = alt;
     plan->executed = executed;
     plan->j01 = 0;  // k_plan_joint (if launched) may enable the look-back-free pass 1
+    plan->reverse = 0;
+    const bool in_order = order != nullptr && order[0] == 0;
+    const bool reversed = order != nullptr && !in_order && order[1] == 0;
+    if (in_order || reversed) {  // presorted input: no pass; reversed input is reversed in place
+      for (int p = 0; p < 8; ++p) {
+        plan->skip[p] = 1;
+        plan->src_alt[p] = 0;
+      }
+      plan->final_copy = 0;
+      plan->executed = 0;
+      plan->reverse = reversed;
+    }
   }
   if (threadIdx.x < 16) tile_counters[threadIdx.x] = 0;  // 8 passes + the J01 pass
   if (gcount != nullptr)
@@ -886,8 +991,31 @@ __global__ void __launch_bounds__(THREADS, MINB)
 template <typename U>
 __global__ void __launch_bounds__(256) k_copy_back(U* __restrict__ a, const U* __restrict__ b, uint64_t n,
                                                    const PassPlan* __restrict__ plan) {
-  if (!plan->final_copy) return;
   const uint64_t T = (uint64_t)gridDim.x * blockDim.x;
+  if (plan->reverse) {  // input was in the opposite order (no pass ran): reverse in place
+    const uint64_t h = n / 2;
+    uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    for (; i + 3 * T < h; i += 4 * T) {  // four independent swaps in flight per thread
+      U x[4], y[4];
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        x[k] = a[i + k * T];
+        y[k] = a[n - 1 - (i + k * T)];
+      }
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        a[i + k * T] = y[k];
+        a[n - 1 - (i + k * T)] = x[k];
+      }
+    }
+    for (; i < h; i += T) {
+      const U x = a[i], y = a[n - 1 - i];
+      a[i] = y;
+      a[n - 1 - i] = x;
+    }
+    return;
+  }
+  if (!plan->final_copy) return;
   for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += T) a[i] = b[i];
 }
 

@@ -328,3 +328,35 @@ def test_warp_specialised_sizes(B, dtype, descending):
     v = vals.cpu().numpy()
     assert np.array_equal(np.sort(v), np.arange(v.size))
     assert orig[v].tobytes() == ref.tobytes()  # every value followed its key
+
+
+@pytest.mark.parametrize("dtype", [torch.int32, torch.float32, torch.uint64, torch.float64],
+                         ids=lambda d: str(d).split(".")[-1])
+def test_presorted_fast_path(B, dtype):
+    """The histogram sweep detects input already in the requested order (no pass runs) or in the
+    opposite order (reversed in place): sorted, reversed, sorted-but-one-swap (must NOT take the
+    fast path), duplicates, key-value payloads, small and >= 2^24 sizes."""
+    for n in (3, 5000, 100_003, (1 << 24) + 77):
+        x = gen(dtype, n, 900 + n % 97)
+        srt_np = oracle.sort_native(host(x))
+        asc = torch.from_numpy(srt_np.view({4: np.int32, 8: np.int64}[srt_np.itemsize]).copy()).to("cuda").view(dtype)
+        for desc in (False, True):
+            check_equal(B, asc.clone(), desc, f"sorted asc input, desc={desc}")
+        swapped = asc.clone()
+        if n > 3:
+            iv = {4: torch.int32, 8: torch.int64}[asc.element_size()]
+            swapped.view(iv)[n - 2:n] = asc.view(iv)[n - 2:n].flip(0)
+            check_equal(B, swapped, False, "one swap at the end")
+    # duplicates in reverse order
+    base = gen(dtype, 64, 5)
+    srt = oracle.sort_native(host(base), descending=True)
+    rev = np.repeat(srt, 70_001)
+    t = torch.from_numpy(rev.view({4: np.int32, 8: np.int64}[rev.itemsize])).to("cuda").view(dtype)
+    check_equal(B, t, False, "reversed with duplicates")
+    # key-value: reversed keys -> values reversed with them
+    keys = torch.from_numpy(srt.view({4: np.int32, 8: np.int64}[srt.itemsize]).copy()).to("cuda").view(dtype)
+    vals = torch.arange(keys.numel(), dtype=torch.int32, device="cuda")
+    B.sort_pairs_(keys, vals)
+    torch.cuda.synchronize()
+    assert host(keys).tobytes() == oracle.sort_native(srt).tobytes()
+    assert np.array_equal(vals.cpu().numpy(), np.arange(keys.numel())[::-1])

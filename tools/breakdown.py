@@ -19,9 +19,10 @@ ap.add_argument("--dtype", default="")
 ap.add_argument("--reps", type=int, default=20)
 ap.add_argument("--inplace", action="store_true")
 ap.add_argument("--chunk", type=int, default=0)
+ap.add_argument("--layout", default="")
 a = ap.parse_args()
 dt = getattr(torch, a.dtype) if a.dtype else None
-x = W.make(a.cfg, "cuda", n=a.n or None, dtype=dt)
+x = W.make(a.cfg, "cuda", n=a.n or None, dtype=dt, layout=a.layout or None)
 w = torch.empty_like(x)
 s = B.Sorter(x.dtype, x.numel(), "cuda")
 run = (lambda: B.sort_inplace_(w, chunk=a.chunk)) if a.inplace else (lambda: s(w))
@@ -44,7 +45,7 @@ with B.profile() as prof:
         w.copy_(x)
         run()
     torch.cuda.synchronize()
-print(json.dumps({"cfg": a.cfg, "n": x.numel(), "dtype": str(x.dtype), "inplace": a.inplace,
+print(json.dumps({"cfg": a.cfg, "layout": a.layout, "n": x.numel(), "dtype": str(x.dtype), "inplace": a.inplace,
                   "median_ms": ms[len(ms) // 2], "min_ms": ms[0],
                   "per_sort": {k: {"ms": v["ms"] / a.reps, "launches": v["launches"] / a.reps}
                                for k, v in prof.items()}}))
