@@ -176,7 +176,7 @@ void suite(uint64_t n) {
   CK(cudaEventCreate(&a));
   CK(cudaEventCreate(&b));
   CK(cudaEventRecord(a));
-  hk<<<148, HIST_THREADS, P * 256 * LANES * 4>>>(in, n, ghist);
+  hk<<<148, HIST_THREADS, P * 256 * LANES * 4>>>(in, n, ghist, nullptr);
   CK(cudaEventRecord(b));
   CK(cudaEventSynchronize(b));
   float hms;
@@ -195,6 +195,8 @@ void suite(uint64_t n) {
     run_ws<U, 512, 16, RANK_RUN2>(in, out, n, bases, lookback, counter, ref, dbg);
     run_ws<U, 512, 20, RANK_STABLE>(in, out, n, bases, lookback, counter, ref, dbg);
     run_ws<U, 512, 20, RANK_RUN2>(in, out, n, bases, lookback, counter, ref, dbg);
+    run_ws<U, 640, 16, RANK_STABLE>(in, out, n, bases, lookback, counter, ref, dbg);
+    run_ws<U, 640, 16, RANK_RUN2>(in, out, n, bases, lookback, counter, ref, dbg);
     run_ws<U, 512, 24, RANK_STABLE>(in, out, n, bases, lookback, counter, ref, dbg);
     run_ws<U, 512, 24, RANK_RUN2>(in, out, n, bases, lookback, counter, ref, dbg);
     run_ws<U, 512, 20, RANK_UNSTABLE>(in, out, n, bases, lookback, counter, ref, dbg, gcount);
