@@ -55,7 +55,10 @@ __host__ __device__ __forceinline__ U key_decode(U k) {
   } else if constexpr (KIND == KIND_I) {
     return U(k ^ SIGN);
   } else {
-    return (k & SIGN) ? U(k ^ SIGN) : U(~k);
+    // (k & SIGN) ? k ^ SIGN : ~k, branch-free: t is all-ones when the sign bit is set
+    using S = typename Bits<sizeof(U)>::S;
+    const U t = U(S(k) >> (W - 1));
+    return U(k ^ (U(~t) | SIGN));
   }
 }
 

@@ -12,6 +12,7 @@
 
 #include "onesweep.cuh"
 #include "onesweep_ws.cuh"
+#include "pass2.cuh"
 #include "paths.cuh"
 
 namespace bsort {
@@ -177,6 +178,37 @@ bsort_status_t launch_pass_ws(const U* a, U* b, uint64_t n, DigitF digit, const 
   return BSORT_SUCCESS;
 }
 
+// Round-2 look-back pass (pass2.cuh) for 32-bit keys: ranking by lane-ordered warp atomics,
+// separate input / staging buffers, vectorised look-back.  Keys stay raw in the buffers (P2_RAW):
+// the passes before it are round-1 kernels.  640 rankers x 16 keys + 256 writers
+// (tools/exp/tune2.cu: 3.45 ms per 2^30-key pass on cfg3 vs 3.65 / 4.16 ms for round 1's RUN2 /
+// stable passes).  Needs n <= 2^30 (30-bit look-back counts).
+struct P2Cfg {
+  static constexpr int RT = 640, WT = 256, ITEMS = 16;
+};
+constexpr uint64_t P2_MAX_N = 1ull << 30;
+inline bool p2_enabled() {
+  static const bool on = [] {
+    const char* e = getenv("BSORT_P2");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
+template <int KIND, bool DESC, int SHIFT, typename U>
+bsort_status_t launch_pass2_stable(const U* a, U* b, uint64_t n, const unsigned long long* bases, uint32_t* lookback,
+                                   uint32_t* counter, const PassPlan* plan, int pass, cudaStream_t s) {
+  using L = Pass2Smem<P2Cfg::RT, P2Cfg::WT, P2Cfg::ITEMS, U, R2_STABLE>;
+  auto kern = k_pass2<U, KIND, DESC, SHIFT, P2Cfg::RT, P2Cfg::WT, P2Cfg::ITEMS, R2_STABLE, false, 2>;
+  BSORT_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L::bytes));
+  const uint64_t tiles = (n + L::TILE - 1) / L::TILE;
+  const uint64_t grid = min64(tiles, (uint64_t)num_sms());  // one CTA per SM, all resident
+  BSORT_LAUNCH(PROF_PASS, s,
+               kern<<<(unsigned)grid, P2Cfg::RT + P2Cfg::WT, L::bytes, s>>>(
+                   a, b, n, bases, lookback, nullptr, counter, (uint32_t)tiles, plan, pass, P2_RAW | P2_ENC | P2_DEC,
+                   ChunkMap{}));
+  return BSORT_SUCCESS;
+}
+
 inline bsort_status_t memset_async(void* p, size_t bytes, cudaStream_t s) {
   BSORT_LAUNCH(PROF_MEMSET, s, cudaMemsetAsync(p, 0, bytes, s));
   return BSORT_SUCCESS;
@@ -260,8 +292,15 @@ bsort_status_t lsd_run(U* keys, uint32_t* vals, uint64_t n, unsigned char* ws, c
                                                       lookback, gcount, counters, plan, p, s, kvp);
     } else {
       bool done = false;
+      if constexpr (sizeof(U) == 4 && !KV) {
+        if (n >= WS_MIN_N && n <= P2_MAX_N && p2_enabled() && (uintptr_t)keys % sizeof(U) == 0) {
+          st = launch_pass2_stable<KIND, DESC, SH>(keys, scratch, n, bases + p * 256,
+                                                   reinterpret_cast<uint32_t*>(lookback), counters + p, plan, p, s);
+          done = true;
+        }
+      }
       // TMA on both buffers (the scratch buffers are aligned)
-      if (n >= WS_MIN_N && ws_enabled() && (uintptr_t)keys % 16 == 0 && (!KV || (uintptr_t)vals % 16 == 0)) {
+      if (!done && n >= WS_MIN_N && ws_enabled() && (uintptr_t)keys % 16 == 0 && (!KV || (uintptr_t)vals % 16 == 0)) {
         st = launch_pass_ws<U, DescT, KV>(keys, scratch, n, RadixDigit<KIND, DESC, U, SH>{}, bases + p * 256,
                                           lookback, counters + p, plan, p, s, kvp);
         done = true;

@@ -108,7 +108,9 @@ struct PassPlan {
   uint32_t executed;    // number of executed passes
   uint32_t j01;         // pass 1 runs as RANK_J01 (every nonzero digit-0 bucket >= one tile)
   uint32_t reverse;     // input already in the opposite order: no pass, k_copy_back reverses
-  uint32_t pad[12];
+  uint32_t first;       // first executed pass (8: none) -- k_pass2 encodes keys as it loads them
+  uint32_t last;        // last executed pass (8: none) -- k_pass2 decodes keys as it writes them
+  uint32_t pad[10];
 };
 
 // Presorted-input check (§8 a3 "sortedness test"), folded into the histogram sweep: for every
@@ -467,7 +469,7 @@ static __global__ void __launch_bounds__(256)
   }
   __syncthreads();
   if (threadIdx.x == 0) {
-    uint32_t alt = 0, executed = 0;
+    uint32_t alt = 0, executed = 0, first = 8, last = 8;
     for (int p = 0; p < 8; ++p) {
       const uint32_t sk = (p < P) ? skip_s[p] : 1u;
       plan->skip[p] = sk;
@@ -475,8 +477,12 @@ static __global__ void __launch_bounds__(256)
       if (!sk) {
         alt ^= 1u;
         ++executed;
+        if (first == 8) first = p;
+        last = p;
       }
     }
+    plan->first = first;
+    plan->last = last;
     plan->final_copy = alt;
     plan->executed = executed;
     plan->j01 = 0;  // k_plan_joint (if launched) may enable the look-back-free pass 1
@@ -490,6 +496,7 @@ static __global__ void __launch_bounds__(256)
       }
       plan->final_copy = 0;
       plan->executed = 0;
+      plan->first = plan->last = 8;
       plan->reverse = reversed;
     }
   }

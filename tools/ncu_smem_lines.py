@@ -1,0 +1,37 @@
+"""Per-source-line shared-memory wavefronts (actual / ideal) of an ncu report (needs -lineinfo)."""
+import csv
+import io
+import subprocess
+import sys
+
+
+def main(rep, top=30, keys=None):
+    out = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "cuda,sass"],
+                         capture_output=True, text=True).stdout
+    rows = list(csv.reader(io.StringIO(out)))
+    fname, hdr, res = None, None, []
+    for r in rows:
+        if len(r) == 2 and r[0] == "File Path":
+            fname = r[1].split("/")[-1]
+            continue
+        if r and r[0] == "Line No":
+            hdr = r
+            continue
+        if hdr is None or len(r) < 8 or not r[0]:
+            continue
+        try:
+            wf = int(r[hdr.index("L1 Wavefronts Shared")])
+            ideal = int(r[hdr.index("L1 Wavefronts Shared Ideal")])
+        except ValueError:
+            continue
+        if wf:
+            res.append((wf, ideal, fname, r[0], r[1][:90]))
+    tot = sum(x[0] for x in res)
+    print(f"total shared wavefronts {tot:.4g}" + (f" = {tot * 32 / keys:.2f} per 32 keys" if keys else ""))
+    for wf, ideal, f, ln, src in sorted(res, key=lambda x: -x[0])[:top]:
+        per = f" {wf * 32 / keys:5.2f}/32k (ideal {ideal * 32 / keys:5.2f})" if keys else ""
+        print(f"{100*wf/tot:5.1f}%{per} {f}:{ln:5s} {src}")
+
+
+if __name__ == "__main__":
+    main(sys.argv[1], int(sys.argv[2]) if len(sys.argv) > 2 else 30, float(sys.argv[3]) if len(sys.argv) > 3 else None)
