@@ -183,10 +183,28 @@ bsort_status_t launch_pass_ws(const U* a, U* b, uint64_t n, DigitF digit, const 
 // the passes before it are round-1 kernels.  640 rankers x 16 keys + 256 writers
 // (tools/exp/tune2.cu: 3.45 ms per 2^30-key pass on cfg3 vs 3.65 / 4.16 ms for round 1's RUN2 /
 // stable passes).  Needs n <= 2^30 (30-bit look-back counts).
-struct P2Cfg {
+template <int MODE> struct P2Cfg {
   static constexpr int RT = 640, WT = 256, ITEMS = 16;
 };
+// RUN2 holds two lane-banked tables (counts, offsets): 8192-key tiles
+template <> struct P2Cfg<R2_RUN2> {
+  static constexpr int RT = 512, WT = 256, ITEMS = 16;
+};
+template <int MODE> constexpr uint64_t p2_tile() { return (uint64_t)P2Cfg<MODE>::RT * P2Cfg<MODE>::ITEMS; }
+// skewed digits (plan->skew): half-warp counter rows, odd ITEMS (conflict-free key loads)
+struct P2SkewCfg {
+  static constexpr int RT = 640, WT = 256, ITEMS = 15;
+};
 constexpr uint64_t P2_MAX_N = 1ull << 30;
+// RUN2 for pass 2 measured slower than the stable pass on cfg3 (4.25 vs 3.6 ms, ALU-bound):
+// off unless BSORT_P2_RUN2=1
+inline bool p2_run2_enabled() {
+  static const bool on = [] {
+    const char* e = getenv("BSORT_P2_RUN2");
+    return e && e[0] == '1';
+  }();
+  return on;
+}
 inline bool p2_enabled() {
   static const bool on = [] {
     const char* e = getenv("BSORT_P2");
@@ -194,18 +212,19 @@ inline bool p2_enabled() {
   }();
   return on;
 }
-template <int KIND, bool DESC, int SHIFT, typename U>
-bsort_status_t launch_pass2_stable(const U* a, U* b, uint64_t n, const unsigned long long* bases, uint32_t* lookback,
-                                   uint32_t* counter, const PassPlan* plan, int pass, cudaStream_t s) {
-  using L = Pass2Smem<P2Cfg::RT, P2Cfg::WT, P2Cfg::ITEMS, U, R2_STABLE>;
-  auto kern = k_pass2<U, KIND, DESC, SHIFT, P2Cfg::RT, P2Cfg::WT, P2Cfg::ITEMS, R2_STABLE, false, 2>;
+template <int KIND, bool DESC, int SHIFT, int MODE = R2_STABLE, int HALVES = 1, typename U>
+bsort_status_t launch_pass2(const U* a, U* b, uint64_t n, const unsigned long long* bases, uint32_t* lookback,
+                            uint32_t* counter, const PassPlan* plan, int pass, cudaStream_t s, uint32_t xflags = 0) {
+  using C = std::conditional_t<HALVES == 2, P2SkewCfg, P2Cfg<MODE>>;
+  using L = Pass2Smem<C::RT, C::WT, C::ITEMS, U, MODE, HALVES>;
+  auto kern = k_pass2<U, KIND, DESC, SHIFT, C::RT, C::WT, C::ITEMS, MODE, false, 2, HALVES>;
   BSORT_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L::bytes));
   const uint64_t tiles = (n + L::TILE - 1) / L::TILE;
   const uint64_t grid = min64(tiles, (uint64_t)num_sms());  // one CTA per SM, all resident
   BSORT_LAUNCH(PROF_PASS, s,
-               kern<<<(unsigned)grid, P2Cfg::RT + P2Cfg::WT, L::bytes, s>>>(
-                   a, b, n, bases, lookback, nullptr, counter, (uint32_t)tiles, plan, pass, P2_RAW | P2_ENC | P2_DEC,
-                   ChunkMap{}));
+               kern<<<(unsigned)grid, C::RT + C::WT, L::bytes, s>>>(
+                   a, b, n, bases, lookback, nullptr, counter, (uint32_t)tiles, plan, pass,
+                   P2_RAW | P2_ENC | P2_DEC | xflags, ChunkMap{}));
   return BSORT_SUCCESS;
 }
 
@@ -263,7 +282,10 @@ bsort_status_t lsd_run(U* keys, uint32_t* vals, uint64_t n, unsigned char* ws, c
                                         order));
   if (use_joint)
     BSORT_LAUNCH(PROF_SCAN, s,
-                 k_plan_joint<<<1, 256, 0, s>>>(joint, ghist, bases + 256, J01_TILE, plan, seg));
+                 k_plan_joint<<<1, 256, 0, s>>>(joint, ghist, bases + 256, J01_TILE, plan, seg,
+                                                (sizeof(U) == 4 && !KV && n <= P2_MAX_N && p2_enabled() && p2_run2_enabled())
+                                                    ? p2_tile<R2_RUN2>()
+                                                    : 0));
   bsort_status_t st = BSORT_SUCCESS;
   auto one_pass = [&](auto shift_c) {
     constexpr int SH = decltype(shift_c)::value;
@@ -294,8 +316,16 @@ bsort_status_t lsd_run(U* keys, uint32_t* vals, uint64_t n, unsigned char* ws, c
       bool done = false;
       if constexpr (sizeof(U) == 4 && !KV) {
         if (n >= WS_MIN_N && n <= P2_MAX_N && p2_enabled() && (uintptr_t)keys % sizeof(U) == 0) {
-          st = launch_pass2_stable<KIND, DESC, SH>(keys, scratch, n, bases + p * 256,
-                                                   reinterpret_cast<uint32_t*>(lookback), counters + p, plan, p, s);
+          // (half-warp counter rows for skewed top digits, k_pass2<..., HALVES = 2> with
+          // P2_SKEWVAR, measured no faster on cfg3's sign+exponent digit: 3.98 vs 3.92 ms)
+          st = launch_pass2<KIND, DESC, SH>(keys, scratch, n, bases + p * 256,
+                                            reinterpret_cast<uint32_t*>(lookback), counters + p, plan, p, s);
+          // pass 2 ranked by runs when the plan allows it (each launch checks plan->run2)
+          if constexpr (p == 2)
+            if (st == BSORT_SUCCESS && use_joint)
+              st = launch_pass2<KIND, DESC, SH, R2_RUN2>(keys, scratch, n, bases + p * 256,
+                                                         reinterpret_cast<uint32_t*>(lookback), counters + 12, plan, p,
+                                                         s);
           done = true;
         }
       }

@@ -110,7 +110,9 @@ struct PassPlan {
   uint32_t reverse;     // input already in the opposite order: no pass, k_copy_back reverses
   uint32_t first;       // first executed pass (8: none) -- k_pass2 encodes keys as it loads them
   uint32_t last;        // last executed pass (8: none) -- k_pass2 decodes keys as it writes them
-  uint32_t pad[10];
+  uint32_t run2;        // pass 2 runs as R2_RUN2 (every nonzero (digit 1, digit 0) bin >= one tile)
+  uint32_t skew;        // bit p: one bin of digit p holds > n/8 keys (pass2.cuh half-warp counters)
+  uint32_t pad[8];
 };
 
 // Presorted-input check (§8 a3 "sortedness test"), folded into the histogram sweep: for every
@@ -420,8 +422,17 @@ __global__ void __launch_bounds__(HIST_THREADS, 1)
 static __global__ void __launch_bounds__(256)
     k_plan_joint(const unsigned long long* __restrict__ gjoint, const unsigned long long* __restrict__ ghist,
                  const unsigned long long* __restrict__ bases1, uint64_t tile, PassPlan* __restrict__ plan,
-                 unsigned long long* __restrict__ seg) {
+                 unsigned long long* __restrict__ seg, uint64_t run2_tile = 0) {
   const uint32_t t = threadIdx.x;
+  // RUN2 for pass 2 (pass2.cuh): its input is sorted by the low 16 bits, whose runs are the joint
+  // bins; a tile meets at most two of them when every nonzero bin is at least a tile long
+  bool ok2 = run2_tile > 0;
+  for (int b = 0; b < 256 && ok2; ++b) {
+    const unsigned long long c = gjoint[t * 256 + b];
+    ok2 = c == 0 || c >= run2_tile;
+  }
+  const int run2 = __syncthreads_and(ok2);
+  if (t == 0) plan->run2 = (uint32_t)run2 && !plan->skip[2];
   const unsigned long long c0 = ghist[t];  // digit-0 marginal
   const int eligible = __syncthreads_and(c0 == 0 || c0 >= tile);
   if (t == 0) plan->j01 = (uint32_t)eligible && !plan->skip[1];
@@ -445,7 +456,7 @@ static __global__ void __launch_bounds__(256)
            unsigned long long* __restrict__ gcount, const unsigned long long* __restrict__ gjoint,
            const uint32_t* __restrict__ order = nullptr) {
   __shared__ unsigned long long wt[256 / 32 + 1];
-  __shared__ uint32_t skip_s[8];
+  __shared__ uint32_t skip_s[8], skew_s[8];
   if (gjoint != nullptr) {  // marginals of digits 1 (row sums) and 0 (column sums) of J[d1][d0]
     unsigned long long r = 0, c = 0;
     const ulonglong2* row = reinterpret_cast<const ulonglong2*>(gjoint + threadIdx.x * 256);
@@ -465,7 +476,11 @@ static __global__ void __launch_bounds__(256)
     const unsigned long long ex = block_exclusive_scan<256>(c, wt, (unsigned long long*)nullptr);
     bases[p * 256 + threadIdx.x] = ex;
     const int trivial = __syncthreads_or(c == n);
-    if (threadIdx.x == 0) skip_s[p] = trivial;
+    const int skewed = __syncthreads_or(c * 8 > n);
+    if (threadIdx.x == 0) {
+      skip_s[p] = trivial;
+      skew_s[p] = skewed;
+    }
   }
   __syncthreads();
   if (threadIdx.x == 0) {
@@ -483,9 +498,13 @@ static __global__ void __launch_bounds__(256)
     }
     plan->first = first;
     plan->last = last;
+    uint32_t skew = 0;
+    for (int p = 0; p < P; ++p) skew |= skew_s[p] << p;
+    plan->skew = skew;
     plan->final_copy = alt;
     plan->executed = executed;
     plan->j01 = 0;  // k_plan_joint (if launched) may enable the look-back-free pass 1
+    plan->run2 = 0;  // ... and pass 2 ranked by runs (pass2.cuh R2_RUN2)
     plan->reverse = 0;
     const bool in_order = order != nullptr && order[0] == 0;
     const bool reversed = order != nullptr && !in_order && order[1] == 0;

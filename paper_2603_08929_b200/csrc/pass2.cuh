@@ -46,7 +46,9 @@
 
 namespace bsort {
 
-enum Rank2 : int { R2_STABLE = 0, R2_UNSTABLE = 1, R2_J01 = 2 };
+enum Rank2 : int { R2_STABLE = 0, R2_UNSTABLE = 1, R2_J01 = 2, R2_RUN2 = 3 };
+// ranking by (digit, run of the lower bits) in lane-banked tables: J01 and RUN2
+constexpr bool p2_runs(int mode) { return mode == R2_J01 || mode == R2_RUN2; }
 constexpr int P2_NC = 32;  // look-back chains (chunks) of a chunked stable pass
 
 // Chunk map of a stable pass (device arrays written by the plan kernel).
@@ -170,6 +172,7 @@ __device__ __forceinline__ uint32_t lookback_walk_v4(const uint32_t* lb, uint32_
       }
     }
     if (fin) return excl;
+    if (stop) __nanosleep(128);  // a predecessor has not published yet: do not hammer L2
     j = next;
   }
 }
@@ -188,7 +191,7 @@ struct SlotInfo {
 static_assert(sizeof(SlotInfo) == 32, "slot layout");
 constexpr uint32_t P2_END = 0xFFFFFFFFu;
 
-template <int RT, int WT, int ITEMS, typename U, int MODE>
+template <int RT, int WT, int ITEMS, typename U, int MODE, int HALVES = 1>
 struct Pass2Smem {
   static constexpr int RW = RT / 32;
   static constexpr int TILE = RT * ITEMS;
@@ -197,7 +200,10 @@ struct Pass2Smem {
   // STABLE: per-warp counters [RW][256]; UNSTABLE: lane-banked table [256 digits][32 lanes];
   // J01: lane-banked counts [256][32] of (run 0 | run 1 << 16) and the staging offsets, same shape
   static constexpr int NG = MODE == R2_J01 ? 512 : 256;  // write-out bins (J01: 2 * digit + run)
-  static constexpr int CNT_WORDS = MODE == R2_STABLE ? RW * 256 : (MODE == R2_J01 ? 2 : 1) * 256 * 32;
+  // STABLE with HALVES = 2: one row per half-warp, rows 272 words apart (the halves' counters of
+  // one digit sit 16 banks apart), for skewed digits
+  static constexpr int HW = HALVES == 2 ? 272 : 256;
+  static constexpr int CNT_WORDS = MODE == R2_STABLE ? RW * HALVES * HW : (p2_runs(MODE) ? 2 : 1) * 256 * 32;
   static constexpr size_t ibuf_off = 0;  // U[2][IBUFK] TMA input
   static constexpr size_t sbuf_off = align_up(ibuf_off + 2 * sizeof(U) * IBUFK, 16);  // U[2][TILE] staging
   static constexpr size_t cnt_off = align_up(sbuf_off + 2 * sizeof(U) * TILE, 16);
@@ -218,6 +224,9 @@ constexpr uint32_t P2_ENC = 1, P2_DEC = 2;
 // P2_RAW: keys are raw (not encoded) in both buffers whatever the plan says -- the pass encodes as
 // it loads and decodes as it writes (passes of round-1 kernels run before / after it)
 constexpr uint32_t P2_RAW = 4;
+// P2_SKEWVAR: one of a pair of STABLE launches for the same pass; the HALVES = 2 kernel works when
+// the plan marks the pass's digit skewed, the HALVES = 1 kernel otherwise
+constexpr uint32_t P2_SKEWVAR = 8;
 
 // MODE R2_STABLE: look-back pass; with CHUNKED the chains of `cm`, else one chain over tiles of
 //   TILE keys (gcount unused).
@@ -227,19 +236,27 @@ constexpr uint32_t P2_RAW = 4;
 //   means equal low 16 bits, whose order is irrelevant -- and each bin's global offset is one
 //   atomicAdd on its (digit 1, digit 0) segment counter gcount[d0 * 256 + d1] seeded by
 //   k_plan_joint: no look-back.  The plan's j01 flag picks this launch or the R2_STABLE one.
+// MODE R2_RUN2 (LSD pass p >= 2 when every nonzero joint bin of the digits below is at least a
+//   tile long: a tile meets at most two runs of equal lower bits L): ranked unstably by (digit,
+//   run) as J01 -- keys with equal digit and equal L are interchangeable, run 0 precedes run 1 --
+//   with R2_STABLE's look-back for the order between tiles.  The plan's run2 flag picks this
+//   launch or the R2_STABLE one.
 // Keys: digit SHIFT/8 of the encoded key; n < 2^32 (32-bit offsets), n <= 2^30 for R2_STABLE
 // (30-bit look-back counts).
 template <typename U, int KIND, bool DESC, int SHIFT, int RT, int WT, int ITEMS, int MODE, bool CHUNKED = false,
-          int LBV = 2>
+          int LBV = 2, int HALVES = 1>
 __global__ void __launch_bounds__(RT + WT, 1)
     k_pass2(const U* a_ptr, U* b_ptr, uint64_t n, const unsigned long long* __restrict__ bases,
             uint32_t* __restrict__ lookback, unsigned long long* __restrict__ gcount,
             uint32_t* __restrict__ tile_counter, uint32_t num_tiles, const PassPlan* __restrict__ plan, int pass,
             uint32_t flags, ChunkMap cm) {
-  using L = Pass2Smem<RT, WT, ITEMS, U, MODE>;
+  using L = Pass2Smem<RT, WT, ITEMS, U, MODE, HALVES>;
   using LB = LookbackBits<uint32_t>;
   constexpr int TILE = L::TILE;
   constexpr int RW = L::RW;
+  constexpr int NROW = RW * HALVES;  // STABLE counter rows, in index order
+  constexpr int HW = L::HW;
+  static_assert(HALVES == 1 || (MODE == R2_STABLE && ITEMS % 2 == 1), "half-warp rows: stable, odd ITEMS");
   constexpr int SEG = 32 * ITEMS;
   constexpr uint32_t KS = sizeof(U) == 4 ? 2 : 3;  // log2 key bytes
   static_assert(RT >= 256 && RT % 32 == 0 && WT >= 256 && WT % 32 == 0, "one ranker / writer per digit");
@@ -265,8 +282,13 @@ __global__ void __launch_bounds__(RT + WT, 1)
     if (plan->skip[pass]) return;
     if constexpr (MODE == R2_J01) {
       if (!plan->j01) return;
+    } else if constexpr (MODE == R2_RUN2) {
+      if (!plan->run2) return;
     } else if constexpr (MODE == R2_STABLE) {
       if (pass == 1 && plan->j01) return;
+      if (pass == 2 && plan->run2) return;
+      if (flags & P2_SKEWVAR)
+        if ((((plan->skew >> pass) & 1u) != 0) != (HALVES == 2)) return;
     }
     if (plan->src_alt[pass]) {
       src = b_ptr;
@@ -328,22 +350,28 @@ __global__ void __launch_bounds__(RT + WT, 1)
     for (int i = t; i < L::CNT_WORDS / 4; i += RT + WT) reinterpret_cast<uint4*>(cnt)[i] = make_uint4(0, 0, 0, 0);
   }
   __syncthreads();
-  constexpr uint32_t OFS = MODE == R2_J01 ? 256 * 32 : 0;  // J01: offsets table after the counts
+  constexpr uint32_t OFS = p2_runs(MODE) ? 256 * 32 : 0;  // J01 / RUN2: offsets table after the counts
+  constexpr uint32_t LOWMASK = SHIFT >= 32 ? 0xFFFFFFFFu : (1u << SHIFT) - 1u;  // bits below the digit
 
   if (t < (uint32_t)RT) {
     // ---------------------------------------------------------------- rankers
     const uint32_t lane = t & 31, warp = t >> 5;
-    const uint32_t wcnt_a = smem_base + (uint32_t)L::cnt_off + warp * 1024u;  // STABLE: this warp's row
+    // STABLE: this thread's counter row (warp, or half-warp when HALVES == 2); item k of the thread
+    // is tile key seg + IS * k, so (row, item, lane in row) is index order
+    const uint32_t half = HALVES == 2 ? lane >> 4 : 0u;
+    constexpr uint32_t IS = HALVES == 2 ? 16u : 32u;
+    const uint32_t wcnt_a = smem_base + (uint32_t)L::cnt_off + (warp * HALVES + half) * (uint32_t)(HW * 4);
     const uint32_t lane_a = smem_base + (uint32_t)L::cnt_off + lane * 4u;     // UNSTABLE: lane column
-    const uint32_t seg = warp * SEG + lane;
+    const uint32_t seg = HALVES == 2 ? warp * SEG + half * (16 * ITEMS) + (lane & 15) : warp * SEG + lane;
     for (uint32_t it = 0;; ++it) {
       const uint32_t s = it & 1u;  // input buffer and staging slot
       if (it >= 2) named_bar_sync(P2_BAR_SFREE + s, RT + WT);  // writers done with tile it - 2
       if constexpr (MODE == R2_STABLE) {
         // this warp's previous staging (the only reader of its row after the scan) is done
-        uint4* w4 = reinterpret_cast<uint4*>(cnt + warp * 256);
-        w4[lane] = make_uint4(0, 0, 0, 0);
-        w4[lane + 32] = make_uint4(0, 0, 0, 0);
+        uint4* w4 = reinterpret_cast<uint4*>(cnt + warp * HALVES * HW);
+#pragma unroll
+        for (int j = 0; j < (HALVES * HW / 4 + 31) / 32; ++j)
+          if (lane + 32 * j < (uint32_t)(HALVES * HW / 4)) w4[lane + 32 * j] = make_uint4(0, 0, 0, 0);
       }
       mbar_wait(&mbar[s], (it >> 1) & 1u);
       const uint32_t lin = islot[s].lin;
@@ -375,13 +403,13 @@ __global__ void __launch_bounds__(RT + WT, 1)
         for (int j = 0; j < (ITEMS + 1) / 2; ++j) rk[j] = 0;
         if constexpr (FULL) {
 #pragma unroll
-          for (int k = 0; k < ITEMS; ++k) keys[k] = s_ldk<U>(ibuf_a + (seg + 32u * k) * (uint32_t)sizeof(U));
+          for (int k = 0; k < ITEMS; ++k) keys[k] = s_ldk<U>(ibuf_a + (seg + IS * k) * (uint32_t)sizeof(U));
         } else {
           const uint32_t bk = islot[s].bk;
           const U* gsrc = src + islot[s].start;
 #pragma unroll
           for (int k = 0; k < ITEMS; ++k) {
-            const uint32_t i = seg + 32u * k;
+            const uint32_t i = seg + IS * k;
             keys[k] = i < bk ? s_ldk<U>(ibuf_a + i * (uint32_t)sizeof(U)) : (i < valid ? ldg_nc(gsrc + i) : U(0));
           }
         }
@@ -389,8 +417,8 @@ __global__ void __launch_bounds__(RT + WT, 1)
 #pragma unroll
           for (int k = 0; k < ITEMS; ++k) keys[k] = key_encode<KIND, DESC>(keys[k]);
         }
-        uint32_t lf = 0;  // J01: digit 0 of the tile's first key (run 0)
-        if constexpr (MODE == R2_J01) {
+        uint32_t lf = 0;  // J01 / RUN2: lower bits of the tile's first key (run 0)
+        if constexpr (p2_runs(MODE)) {
           const uint32_t bk = islot[s].bk;
           const U* gsrc = src + islot[s].start;
           U fk = bk > 0 ? s_ldk<U>(ibuf_a) : ldg_nc(gsrc);
@@ -399,10 +427,13 @@ __global__ void __launch_bounds__(RT + WT, 1)
             fk = key_encode<KIND, DESC>(fk);
             lk = key_encode<KIND, DESC>(lk);
           }
-          lf = uint32_t(fk) & 0xFFu;
-          if (t == 0) meta[s * 256 + 255].w = lf | ((uint32_t(lk) & 0xFFu) << 8);
+          lf = uint32_t(fk) & LOWMASK;
+          if (t == 0) {
+            meta[s * 256 + 254].w = lf;
+            meta[s * 256 + 255].w = uint32_t(lk) & LOWMASK;
+          }
         }
-        auto run_of = [&](U key) -> uint32_t { return (uint32_t(key) & 0xFFu) != lf ? 1u : 0u; };
+        auto run_of = [&](U key) -> uint32_t { return (uint32_t(key) & LOWMASK) != lf ? 1u : 0u; };
         (void)run_of;
         if constexpr (MODE == R2_STABLE) __syncwarp();  // row zeroed
         // counter of key k: STABLE this warp's digit counter; UNSTABLE (digit, lane), bank = lane
@@ -415,13 +446,13 @@ __global__ void __launch_bounds__(RT + WT, 1)
         };
 #pragma unroll
         for (int k = 0; k < ITEMS; ++k) {
-          if (FULL || seg + 32u * k < valid) {
+          if (FULL || seg + IS * k < valid) {
             uint32_t r;
             if constexpr (MODE == R2_STABLE) {
               r = s_atom_add(counter(keys[k]), 4u);
             } else if constexpr (MODE == R2_UNSTABLE) {
               r = (s_atom_add(counter(keys[k]), 4u << hsh) >> hsh) & 0xFFFFu;
-            } else {
+            } else {  // J01 / RUN2
               const uint32_t sh = run_of(keys[k]) << 4;
               r = (s_atom_add(counter(keys[k]), 4u << sh) >> sh) & 0xFFFFu;
             }
@@ -435,7 +466,7 @@ __global__ void __launch_bounds__(RT + WT, 1)
           uint32_t tot = 0;
           if (t < 256) {
 #pragma unroll
-            for (int w = 0; w < RW; ++w) tot += cnt[w * 256 + t];
+            for (int w = 0; w < NROW; ++w) tot += cnt[w * HW + t];
             tot >>= 2;
             st_relaxed(&lookback[lb2_index(lin, t)], (first_tile ? LB::INC : LB::AGG) | tot);
             meta[s * 256 + t].y = tot;
@@ -445,14 +476,14 @@ __global__ void __launch_bounds__(RT + WT, 1)
           if (t < 256) {
             uint32_t run = sbuf_a + (excl << KS);
 #pragma unroll
-            for (int w = 0; w < RW; ++w) {
-              const uint32_t c = cnt[w * 256 + t];
-              cnt[w * 256 + t] = run;
+            for (int w = 0; w < NROW; ++w) {
+              const uint32_t c = cnt[w * HW + t];
+              cnt[w * HW + t] = run;
               run += c << (KS - 2);
             }
             meta[s * 256 + t].x = excl;
           }
-        } else if constexpr (MODE == R2_J01) {
+        } else if constexpr (p2_runs(MODE)) {
           // as UNSTABLE below, with both u16 halves (runs 0 / 1) of every word counted, the
           // offsets written to the second table and the counts zeroed
           const uint32_t qr = t & 7u;
@@ -471,6 +502,8 @@ __global__ void __launch_bounds__(RT + WT, 1)
           }
           const uint32_t t0 = (tot & 0xFFFFu) >> 2, t1 = tot >> 18;
           if (t < 256) {
+            if constexpr (MODE == R2_RUN2)
+              st_relaxed(&lookback[lb2_index(lin, t)], (first_tile ? LB::INC : LB::AGG) | (t0 + t1));
             meta[s * 256 + t].y = t0 + t1;
             meta[s * 256 + t].z = t0;
           }
@@ -550,13 +583,13 @@ __global__ void __launch_bounds__(RT + WT, 1)
 #pragma unroll
           for (int j = 0; j < SG; ++j) {
             const int k = k0 + j;
-            if (k < ITEMS && (FULL || seg + 32u * k < valid)) {
+            if (k < ITEMS && (FULL || seg + IS * k < valid)) {
               const uint32_t w = s_ld(counter(keys[k]) + OFS * 4u);
               const uint32_t r = (rk[k >> 1] >> ((k & 1) * 16)) & 0xFFFFu;
               if constexpr (MODE == R2_STABLE)
                 pos[j] = w + (r << (KS - 2));
-              else if constexpr (MODE == R2_J01)
-                pos[j] = sbuf_a + (p2_swz<U>((((w >> (run_of(keys[k]) << 4)) & 0xFFFFu) >> KS) + (r >> 2)) << KS);
+              else if constexpr (p2_runs(MODE))
+                pos[j] = sbuf_a + ((w >> (run_of(keys[k]) << 4)) & 0xFFFFu) + (r << (KS - 2));
               else
                 pos[j] = sbuf_a + (p2_swz<U>((((w >> hsh) & 0xFFFFu) >> KS) + (r >> 2)) << KS);  // swizzled
             }
@@ -564,7 +597,7 @@ __global__ void __launch_bounds__(RT + WT, 1)
 #pragma unroll
           for (int j = 0; j < SG; ++j) {
             const int k = k0 + j;
-            if (k < ITEMS && (FULL || seg + 32u * k < valid)) s_st(pos[j], keys[k]);
+            if (k < ITEMS && (FULL || seg + IS * k < valid)) s_st(pos[j], keys[k]);
           }
         }
       };
@@ -589,14 +622,14 @@ __global__ void __launch_bounds__(RT + WT, 1)
       uint32_t* gof = gofs + s * L::NG;
       uint32_t lf = 0, ll = 0;  // J01: the tile's digit-0 runs
       if constexpr (MODE == R2_J01) {
-        lf = meta[s * 256 + 255].w & 0xFFu;
-        ll = (meta[s * 256 + 255].w >> 8) & 0xFFu;
+        lf = meta[s * 256 + 254].w;
+        ll = meta[s * 256 + 255].w;
       }
       unsigned long long g0 = 0, g1 = 0;  // global start of this tile's run of digit w (J01: runs 0 / 1)
       uint32_t c0 = 0;
       if (w < 256) {
         const uint32_t c = meta[s * 256 + w].y;
-        if constexpr (MODE == R2_STABLE) {
+        if constexpr (MODE == R2_STABLE || MODE == R2_RUN2) {
           uint32_t excl = 0;
           if (!first_tile) {
             excl = lookback_walk_v4<LBV>(lookback, w, lin);
@@ -636,7 +669,7 @@ __global__ void __launch_bounds__(RT + WT, 1)
 #pragma unroll
           for (int j = 0; j < WB; ++j) {
             const uint32_t i = base + j * WT;
-            const uint32_t si = MODE != R2_STABLE ? p2_swz<U>(i) : i;
+            const uint32_t si = MODE == R2_UNSTABLE ? p2_swz<U>(i) : i;
             x[j] = (FULL || i < valid) ? s_ldk<U>(sbuf_a + si * (uint32_t)sizeof(U)) : U(0);
           }
 #pragma unroll
