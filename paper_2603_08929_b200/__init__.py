@@ -82,9 +82,10 @@ def sort_(t: torch.Tensor, descending: bool = False) -> torch.Tensor:
         return t
     wsb = int(lib.bsort_workspace_bytes(code, n))
     ws = _workspace(wsb, t.device)
-    check(lib.bsort_sort_ws(code, ctypes.c_void_p(t.data_ptr()), n, int(bool(descending)),
-                            ctypes.c_void_p(ws.data_ptr()), wsb, _stream_ptr(t.device)),
-          "bsort_sort_ws")
+    with torch.cuda.device(t.device):  # launches and allocations on the tensor's GPU
+        check(lib.bsort_sort_ws(code, ctypes.c_void_p(t.data_ptr()), n, int(bool(descending)),
+                                ctypes.c_void_p(ws.data_ptr()), wsb, _stream_ptr(t.device)),
+              "bsort_sort_ws")
     return t
 
 
@@ -107,9 +108,10 @@ def sort_inplace_(t: torch.Tensor, descending: bool = False, chunk: int = 0) -> 
         return t
     wsb = int(lib.bsort_inplace_workspace_bytes(code, n, chunk))
     ws = _workspace(wsb, t.device)
-    check(lib.bsort_sort_inplace_ws(code, ctypes.c_void_p(t.data_ptr()), n, int(bool(descending)), chunk,
-                                    ctypes.c_void_p(ws.data_ptr()), wsb, _stream_ptr(t.device)),
-          "bsort_sort_inplace_ws")
+    with torch.cuda.device(t.device):  # launches and allocations on the tensor's GPU
+        check(lib.bsort_sort_inplace_ws(code, ctypes.c_void_p(t.data_ptr()), n, int(bool(descending)), chunk,
+                                        ctypes.c_void_p(ws.data_ptr()), wsb, _stream_ptr(t.device)),
+              "bsort_sort_inplace_ws")
     return t
 
 
@@ -126,9 +128,10 @@ def sort_pairs_(keys: torch.Tensor, values: torch.Tensor, descending: bool = Fal
         return keys, values
     wsb = int(lib.bsort_pairs_workspace_bytes(code, n))
     ws = _workspace(wsb, keys.device)
-    check(lib.bsort_sort_pairs_ws(code, ctypes.c_void_p(keys.data_ptr()), ctypes.c_void_p(values.data_ptr()),
-                                  n, int(bool(descending)), ctypes.c_void_p(ws.data_ptr()), wsb,
-                                  _stream_ptr(keys.device)), "bsort_sort_pairs_ws")
+    with torch.cuda.device(keys.device):  # launches and allocations on the tensor's GPU
+        check(lib.bsort_sort_pairs_ws(code, ctypes.c_void_p(keys.data_ptr()), ctypes.c_void_p(values.data_ptr()),
+                                      n, int(bool(descending)), ctypes.c_void_p(ws.data_ptr()), wsb,
+                                      _stream_ptr(keys.device)), "bsort_sort_pairs_ws")
     return keys, values
 
 
@@ -154,9 +157,10 @@ class Sorter:
         _check_tensor(t)
         if t.dtype != self.dtype or t.numel() > self.n:
             raise ValueError("Sorter: dtype mismatch or tensor larger than the workspace")
-        check(lib.bsort_sort_ws(self.code, ctypes.c_void_p(t.data_ptr()), t.numel(),
-                                int(bool(descending)), ctypes.c_void_p(self.ws.data_ptr()),
-                                self.ws_bytes, _stream_ptr(t.device)), "bsort_sort_ws")
+        with torch.cuda.device(t.device):  # launches and allocations on the tensor's GPU
+            check(lib.bsort_sort_ws(self.code, ctypes.c_void_p(t.data_ptr()), t.numel(),
+                                    int(bool(descending)), ctypes.c_void_p(self.ws.data_ptr()),
+                                    self.ws_bytes, _stream_ptr(t.device)), "bsort_sort_ws")
         return t
 
     def graph(self, t: torch.Tensor, descending: bool = False) -> "torch.cuda.CUDAGraph":
@@ -177,10 +181,11 @@ class Sorter:
         _check_tensor(dev_buf)
         if dev_buf.numel() < host.numel() or host.numel() > self.n:
             raise ValueError("sort_host: device buffer / workspace too small")
-        check(lib.bsort_sort_host(self.code, ctypes.c_void_p(host.data_ptr()), host.numel(),
-                                  int(bool(descending)), ctypes.c_void_p(dev_buf.data_ptr()),
-                                  ctypes.c_void_p(self.ws.data_ptr()), self.ws_bytes,
-                                  _stream_ptr(dev_buf.device)), "bsort_sort_host")
+        with torch.cuda.device(dev_buf.device):  # launches and allocations on the tensor's GPU
+            check(lib.bsort_sort_host(self.code, ctypes.c_void_p(host.data_ptr()), host.numel(),
+                                      int(bool(descending)), ctypes.c_void_p(dev_buf.data_ptr()),
+                                      ctypes.c_void_p(self.ws.data_ptr()), self.ws_bytes,
+                                      _stream_ptr(dev_buf.device)), "bsort_sort_host")
         return host
 
 
@@ -199,9 +204,10 @@ def top_hist(t: torch.Tensor, descending: bool = False) -> torch.Tensor:
     """uint64[65536] device histogram of the top 16 bits of the transformed keys."""
     _check_tensor(t)
     h = torch.empty(_lib.DIST_BINS, dtype=torch.uint64, device=t.device)
-    check(lib.bsort_dist_top_hist(dtype_code(t.dtype), ctypes.c_void_p(t.data_ptr()), t.numel(),
-                                  int(bool(descending)), ctypes.c_void_p(h.data_ptr()),
-                                  _stream_ptr(t.device)), "bsort_dist_top_hist")
+    with torch.cuda.device(t.device):  # launches and allocations on the tensor's GPU
+        check(lib.bsort_dist_top_hist(dtype_code(t.dtype), ctypes.c_void_p(t.data_ptr()), t.numel(),
+                                      int(bool(descending)), ctypes.c_void_p(h.data_ptr()),
+                                      _stream_ptr(t.device)), "bsort_dist_top_hist")
     return h
 
 
@@ -243,10 +249,11 @@ def partition(t: torch.Tensor, cuts: np.ndarray, counts: np.ndarray,
     out = torch.empty_like(t)
     wsb = int(lib.bsort_dist_partition_workspace_bytes(code, t.numel(), nranks))
     ws = _workspace(wsb, t.device)
-    check(lib.bsort_dist_partition(code, ctypes.c_void_p(t.data_ptr()), t.numel(),
-                                   int(bool(descending)), _u32p(c), _u64p(sc), nranks,
-                                   ctypes.c_void_p(out.data_ptr()), ctypes.c_void_p(ws.data_ptr()),
-                                   wsb, _stream_ptr(t.device)), "bsort_dist_partition")
+    with torch.cuda.device(t.device):  # launches and allocations on the tensor's GPU
+        check(lib.bsort_dist_partition(code, ctypes.c_void_p(t.data_ptr()), t.numel(),
+                                       int(bool(descending)), _u32p(c), _u64p(sc), nranks,
+                                       ctypes.c_void_p(out.data_ptr()), ctypes.c_void_p(ws.data_ptr()),
+                                       wsb, _stream_ptr(t.device)), "bsort_dist_partition")
     return out
 
 
@@ -263,10 +270,11 @@ def partition_remote(t: torch.Tensor, cuts: np.ndarray, counts: np.ndarray, dst_
     nranks = c.size - 1
     wsb = int(lib.bsort_dist_partition_workspace_bytes(code, t.numel(), nranks))
     ws = _workspace(wsb, t.device)
-    check(lib.bsort_dist_partition_remote(code, ctypes.c_void_p(t.data_ptr()), t.numel(),
-                                          int(bool(descending)), _u32p(c), _u64p(sc), nranks,
-                                          _u64p(da), ctypes.c_void_p(ws.data_ptr()), wsb,
-                                          _stream_ptr(t.device)), "bsort_dist_partition_remote")
+    with torch.cuda.device(t.device):  # launches and allocations on the tensor's GPU
+        check(lib.bsort_dist_partition_remote(code, ctypes.c_void_p(t.data_ptr()), t.numel(),
+                                              int(bool(descending)), _u32p(c), _u64p(sc), nranks,
+                                              _u64p(da), ctypes.c_void_p(ws.data_ptr()), wsb,
+                                              _stream_ptr(t.device)), "bsort_dist_partition_remote")
 
 
 def refine_hist(t: torch.Tensor, prefixes, prefix_bits: int, descending: bool = False) -> torch.Tensor:
@@ -275,9 +283,10 @@ def refine_hist(t: torch.Tensor, prefixes, prefix_bits: int, descending: bool = 
     _check_tensor(t)
     pre = np.ascontiguousarray(np.asarray(prefixes, dtype=np.uint64))
     h = torch.empty(pre.size * _lib.DIST_BINS, dtype=torch.uint64, device=t.device)
-    check(lib.bsort_dist_refine_hist(dtype_code(t.dtype), ctypes.c_void_p(t.data_ptr()), t.numel(),
-                                     int(bool(descending)), _u64p(pre), pre.size, int(prefix_bits),
-                                     ctypes.c_void_p(h.data_ptr()), _stream_ptr(t.device)), "bsort_dist_refine_hist")
+    with torch.cuda.device(t.device):  # launches and allocations on the tensor's GPU
+        check(lib.bsort_dist_refine_hist(dtype_code(t.dtype), ctypes.c_void_p(t.data_ptr()), t.numel(),
+                                         int(bool(descending)), _u64p(pre), pre.size, int(prefix_bits),
+                                         ctypes.c_void_p(h.data_ptr()), _stream_ptr(t.device)), "bsort_dist_refine_hist")
     return h.view(pre.size, _lib.DIST_BINS)
 
 
@@ -286,9 +295,10 @@ def class_hist(t: torch.Tensor, values, descending: bool = False) -> torch.Tenso
     _check_tensor(t)
     v = np.ascontiguousarray(np.asarray(values, dtype=np.uint64))
     c = torch.empty(2 * v.size + 1, dtype=torch.uint64, device=t.device)
-    check(lib.bsort_dist_class_hist(dtype_code(t.dtype), ctypes.c_void_p(t.data_ptr()), t.numel(),
-                                    int(bool(descending)), _u64p(v), v.size, ctypes.c_void_p(c.data_ptr()),
-                                    _stream_ptr(t.device)), "bsort_dist_class_hist")
+    with torch.cuda.device(t.device):  # launches and allocations on the tensor's GPU
+        check(lib.bsort_dist_class_hist(dtype_code(t.dtype), ctypes.c_void_p(t.data_ptr()), t.numel(),
+                                        int(bool(descending)), _u64p(v), v.size, ctypes.c_void_p(c.data_ptr()),
+                                        _stream_ptr(t.device)), "bsort_dist_class_hist")
     return c
 
 
@@ -302,10 +312,11 @@ def partition_classes(t: torch.Tensor, values, class_counts, descending: bool = 
         return out
     wsb = int(lib.bsort_dist_class_partition_workspace_bytes())
     ws = _workspace(wsb, t.device)
-    check(lib.bsort_dist_partition_classes(dtype_code(t.dtype), ctypes.c_void_p(t.data_ptr()), t.numel(),
-                                           int(bool(descending)), _u64p(v), v.size, _u64p(cc),
-                                           ctypes.c_void_p(out.data_ptr()), ctypes.c_void_p(ws.data_ptr()), wsb,
-                                           _stream_ptr(t.device)), "bsort_dist_partition_classes")
+    with torch.cuda.device(t.device):  # launches and allocations on the tensor's GPU
+        check(lib.bsort_dist_partition_classes(dtype_code(t.dtype), ctypes.c_void_p(t.data_ptr()), t.numel(),
+                                               int(bool(descending)), _u64p(v), v.size, _u64p(cc),
+                                               ctypes.c_void_p(out.data_ptr()), ctypes.c_void_p(ws.data_ptr()), wsb,
+                                               _stream_ptr(t.device)), "bsort_dist_partition_classes")
     return out
 
 
@@ -365,10 +376,11 @@ def sort_dist_native(t: torch.Tensor, comm: Comm, descending: bool = False,
     for attempt in range(2):
         out = torch.empty(cap, dtype=t.dtype, device=t.device)
         n_out = ctypes.c_uint64(0)
-        st = lib.bsort_sort_dist_ex(dtype_code(t.dtype), ctypes.c_void_p(t.data_ptr()), n,
-                                    ctypes.c_void_p(out.data_ptr()), cap, ctypes.byref(n_out),
-                                    int(bool(descending)), _lib.DIST_EXACT if exact else 0, comm._h,
-                                    _stream_ptr(t.device))
+        with torch.cuda.device(t.device):  # launches and allocations on the tensor's GPU
+            st = lib.bsort_sort_dist_ex(dtype_code(t.dtype), ctypes.c_void_p(t.data_ptr()), n,
+                                        ctypes.c_void_p(out.data_ptr()), cap, ctypes.byref(n_out),
+                                        int(bool(descending)), _lib.DIST_EXACT if exact else 0, comm._h,
+                                        _stream_ptr(t.device))
         if st == _lib.ERROR_CAPACITY and attempt == 0:
             cap = int(n_out.value)
             continue

@@ -15,6 +15,12 @@ static thread_local int t_last_err = 0;
 void count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
 void set_last_cuda_error(cudaError_t e) { t_last_err = (int)e; }
 
+int current_device() {
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return 0;
+  return dev;
+}
+
 int num_sms() {
   static int cached[64] = {0};
   int dev = 0;

@@ -92,6 +92,19 @@ enum ProfKind : int {
 static_assert(BSORT_PROF_KINDS == 12, "keep ProfKind in sync with the header");
 
 void prof_begin(int kind, cudaStream_t s);
+int current_device();  // cudaGetDevice, clamped to [0, 64)
+
+// Per-device state of the one-time launch set-up (cudaFuncSetAttribute and the occupancy query
+// act on the CURRENT device only, so a cache keyed by nothing would skip a second GPU).
+struct DeviceOnce {
+  bool done[64] = {};
+  bool pending() const { return !done[current_device()]; }
+  void mark() { done[current_device()] = true; }
+};
+struct DeviceInt {
+  int v[64] = {};
+  int& get() { return v[current_device()]; }
+};
 void prof_end(int kind, cudaStream_t s);
 void count_launch();
 int num_sms();

@@ -358,10 +358,10 @@ bsort_status_t run16(uint16_t* keys, uint64_t n, void* ws, cudaStream_t s) {
   auto* tot = reinterpret_cast<unsigned long long*>(w + l.tot);
   auto* partial = reinterpret_cast<uint16_t*>(w + l.partial);
   const int smem = (BINS16 / 2) * sizeof(uint32_t);
-  static bool attr_set = false;  // idempotent; benign race
-  if (!attr_set) {
+  static DeviceOnce attr;  // per device; idempotent, benign race
+  if (attr.pending()) {
     BSORT_CUDA(cudaFuncSetAttribute(k_count_hist16<TR>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-    attr_set = true;
+    attr.mark();
   }
   const int rows = num_sms();
   BSORT_LAUNCH(PROF_MEMSET, s, cudaMemsetAsync(ovf, 0, BINS16 * sizeof(unsigned long long), s));

@@ -40,10 +40,10 @@ bsort_status_t tophist_run(const U* keys, uint64_t n, uint64_t* hist, cudaStream
   if (n == 0) return BSORT_SUCCESS;
   auto k = k_dist_tophist<KIND, DESC, U>;
   constexpr int smem = TOP_BINS / 2 * 4;
-  static bool attr = false;
-  if (!attr) {
+  static DeviceOnce attr;
+  if (attr.pending()) {
     BSORT_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-    attr = true;
+    attr.mark();
   }
   const int pairs = max(1, num_sms() / 2);
   BSORT_LAUNCH(PROF_DIST_HIST, s, k<<<2 * pairs, 1024, smem, s>>>(keys, n, h));

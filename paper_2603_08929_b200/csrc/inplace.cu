@@ -355,12 +355,12 @@ bsort_status_t ip_partition(U* a, uint64_t n, int shift, char* ws, const IpLayou
   BSORT_LAUNCH(PROF_MEMSET, s, cudaMemsetAsync(ws + l.count, 0, l.bk - l.count, s));
   const uint64_t stripe_len = align_up((n + l.stripes - 1) / l.stripes, IP_TILE);
   const uint64_t grid = (n + stripe_len - 1) / stripe_len;
-  static bool attr = false;
+  static DeviceOnce attr;
   auto k1 = k_ip_classify<KIND, DESC, U>;
   const int smem = 256 * IP_BLOCK_BYTES + IP_TILE * (int)sizeof(U);
-  if (!attr) {
+  if (attr.pending()) {
     BSORT_CUDA(cudaFuncSetAttribute(k1, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-    attr = true;
+    attr.mark();
   }
   BSORT_LAUNCH(PROF_PASS, s,
                k1<<<(unsigned)grid, IP_THREADS, smem, s>>>(a, n, shift, stripe_len, reinterpret_cast<U*>(ws + l.ovf),

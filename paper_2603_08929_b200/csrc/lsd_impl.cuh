@@ -104,7 +104,8 @@ bsort_status_t launch_pass_t(const U* a, U* b, uint64_t n, DigitF digit, const u
   using C = PassCfg<U, RANK, KV>;
   using L = PassSmem<C::THREADS, C::ITEMS, U, RANK, KV>;
   auto kern = k_onesweep_pass<U, C::THREADS, C::ITEMS, C::MINB, BULK, DescT, DigitF, RANK, C::LBG, KV>;
-  static int occ = 0;  // per instantiation; benign race (idempotent)
+  static DeviceInt occ_d;  // per instantiation and device; benign race (idempotent)
+  int& occ = occ_d.get();
   if (occ == 0) {
     BSORT_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L::bytes));
     int o = 0;
@@ -163,7 +164,8 @@ bsort_status_t launch_pass_ws(const U* a, U* b, uint64_t n, DigitF digit, const 
   using L = PassSmemWS<WS_RT, WsCfg<U, KV>::ITEMS, U, KV>;
   static_assert(L::bytes <= 227 * 1024, "fits one CTA per SM");
   auto kern = k_onesweep_pass_ws<U, WS_RT, WsCfg<U, KV>::ITEMS, DescT, DigitF, MODE, 8, 1, KV>;
-  static int occ = 0;
+  static DeviceInt occ_d;
+  int& occ = occ_d.get();
   if (occ == 0) {
     BSORT_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L::bytes));
     int o = 0;
@@ -260,20 +262,20 @@ bsort_status_t lsd_run(U* keys, uint32_t* vals, uint64_t n, unsigned char* ws, c
     constexpr int JL = sizeof(U) == 4 ? 32 : 16;  // lanes of the digit >= 2 counters (224 KB for u64)
     auto hk = k_onesweep_hist_joint<KIND, DESC, U, JL>;
     constexpr int hsmem = (32768 + (P - 2) * 256 * JL) * 4;
-    static bool hattr = false;
-    if (!hattr) {
+    static DeviceOnce hattr;
+    if (hattr.pending()) {
       BSORT_CUDA(cudaFuncSetAttribute(hk, cudaFuncAttributeMaxDynamicSharedMemorySize, hsmem));
-      hattr = true;
+      hattr.mark();
     }
     BSORT_LAUNCH(PROF_MEMSET, s, cudaMemsetAsync(joint, 0, 65536 * 8, s));
     BSORT_LAUNCH(PROF_HIST, s, hk<<<num_sms(), HIST_THREADS, hsmem, s>>>(keys, n, ghist, joint, order));
   } else {
     auto hk = k_onesweep_hist<KIND, DESC, U, LANES>;
     constexpr int hsmem = P * 256 * LANES * 4;
-    static bool hattr = false;
-    if (!hattr) {
+    static DeviceOnce hattr;
+    if (hattr.pending()) {
       BSORT_CUDA(cudaFuncSetAttribute(hk, cudaFuncAttributeMaxDynamicSharedMemorySize, hsmem));
-      hattr = true;
+      hattr.mark();
     }
     BSORT_LAUNCH(PROF_HIST, s, hk<<<num_sms(), HIST_THREADS, hsmem, s>>>(keys, n, ghist, order));
   }
