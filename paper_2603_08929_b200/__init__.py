@@ -25,7 +25,8 @@ from ._lib import BsortError, check, lib
 
 __all__ = ["sort_", "sort", "sort_inplace_", "inplace_workspace_bytes", "sort_pairs_", "argsort", "Sorter", "sort_host", "sort_dist", "dtype_code", "workspace_bytes",
            "top_hist", "splitters", "send_counts", "partition", "partition_remote", "refine_hist",
-           "class_hist", "partition_classes", "Comm", "sort_dist_native", "profile",
+           "class_hist", "partition_classes", "exact_boundaries", "exact_send_counts", "Comm",
+           "sort_dist_native", "profile",
            "launch_count",
            "BsortError", "version"]
 
@@ -387,6 +388,58 @@ def sort_dist_native(t: torch.Tensor, comm: Comm, descending: bool = False,
         check(st, "bsort_sort_dist_ex")
         return out[:int(n_out.value)]
     raise AssertionError("unreachable")
+
+
+def exact_boundaries(hg: np.ndarray, nranks: int, key_bits: int, refine):
+    """§8 N2 host planning, libbsort's bsort_dist_exact_boundaries (marshalling only): for the
+    GLOBAL top-16-bit histogram ``hg`` of keys of ``key_bits`` (32/64) bits, the transformed key
+    K_r of global rank floor(r N / nranks) and its quota for every boundary r.  ``refine(prefixes,
+    bits)`` returns the GLOBAL uint64[m, 65536] next-16-bit histograms below the prefixes.
+    Returns (values np.uint64[m], idx np.int64[nranks-1], quota np.int64[nranks-1], levels)."""
+    hg = np.ascontiguousarray(np.asarray(hg, dtype=np.uint64))
+    err = []
+
+    @_lib.REFINE_FN
+    def _cb(ctx, prefixes, m, bits, out):
+        try:
+            pre = np.array([int(prefixes[j]) for j in range(m)], dtype=np.uint64)
+            h = np.ascontiguousarray(np.asarray(refine(pre, int(bits)), dtype=np.uint64).reshape(-1))
+            if h.size != m * _lib.DIST_BINS:
+                raise ValueError("refine returned a wrong-sized histogram")
+            ctypes.memmove(out, h.ctypes.data, h.nbytes)
+            return 0
+        except Exception as e:  # reported after the C call returns
+            err.append(e)
+            return 1
+
+    R = max(nranks - 1, 1)
+    values = (ctypes.c_uint64 * R)()
+    idx = (ctypes.c_int * R)()
+    quota = (ctypes.c_uint64 * R)()
+    m = ctypes.c_int(0)
+    levels = ctypes.c_int(0)
+    st = lib.bsort_dist_exact_boundaries(_u64p(hg), nranks, key_bits, _cb, None, values, ctypes.byref(m), idx,
+                                         quota, ctypes.byref(levels))
+    if err:
+        raise err[0]
+    check(st, "bsort_dist_exact_boundaries")
+    return (np.array(values[:m.value], dtype=np.uint64), np.array(idx[:nranks - 1], dtype=np.int64),
+            np.array(quota[:nranks - 1], dtype=np.int64), int(levels.value))
+
+
+def exact_send_counts(class_counts_all: np.ndarray, me: int, idx: np.ndarray, quota: np.ndarray) -> np.ndarray:
+    """§8 N2: this rank's per-destination send counts over its class-ordered keys, libbsort's
+    bsort_dist_exact_send_counts (marshalling only).  ``class_counts_all[q]`` = rank q's 2m+1
+    class counts."""
+    C = np.ascontiguousarray(np.asarray(class_counts_all, dtype=np.uint64))
+    P, ncls = C.shape
+    m = (ncls - 1) // 2
+    idx_c = (ctypes.c_int * max(P - 1, 1))(*[int(x) for x in idx])
+    quo_c = (ctypes.c_uint64 * max(P - 1, 1))(*[int(x) for x in quota])
+    out = np.zeros(P, dtype=np.uint64)
+    check(lib.bsort_dist_exact_send_counts(_u64p(C), P, m, int(me), idx_c, quo_c, _u64p(out)),
+          "bsort_dist_exact_send_counts")
+    return out
 
 
 from .dist import sort_dist  # noqa: E402  (needs the helpers above)

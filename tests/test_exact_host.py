@@ -9,7 +9,7 @@ unsigned keys, so no kernel and no oracle arithmetic is involved: the check is s
 import numpy as np
 import pytest
 
-from paper_2603_08929_b200.dist import exact_boundaries, exact_send_counts
+from _exact_ref import exact_boundaries, exact_send_counts
 
 
 def _hist(keys, width, bits, prefix=None, pbits=0):

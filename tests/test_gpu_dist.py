@@ -275,7 +275,7 @@ def test_refine_and_class_hist(B, dtype, descending):
 
 def simulated_exact(B, parts, descending):
     """sort_dist(exact=True) on one GPU: kernels per virtual rank, collectives as tensor ops."""
-    from paper_2603_08929_b200.dist import exact_boundaries, exact_send_counts
+    from paper_2603_08929_b200 import exact_boundaries, exact_send_counts  # libbsort planning
     P = len(parts)
     w = parts[0].element_size() * 8
     hg = sum(B.top_hist(p, descending).view(torch.int64).cpu().numpy() for p in parts).view(np.uint64)

@@ -360,3 +360,60 @@ def test_presorted_fast_path(B, dtype):
     torch.cuda.synchronize()
     assert host(keys).tobytes() == oracle.sort_native(srt).tobytes()
     assert np.array_equal(vals.cpu().numpy(), np.arange(keys.numel())[::-1])
+
+
+# ---- BASELINE.json's own signature: bsort_sort(dtype, dev_ptr, n, direction, stream), which
+# allocates its workspace itself (stream-ordered cudaMallocAsync / cudaFreeAsync)
+
+@pytest.mark.parametrize("dtype", ALL)
+@pytest.mark.parametrize("desc", [False, True])
+def test_bsort_sort_bj_signature(B, dtype, desc):
+    import ctypes
+    n = (1 << 22) + 13 if torch.empty(0, dtype=dtype).element_size() >= 4 else (1 << 20) + 13
+    t = gen(dtype, n, 901 + ALL.index(dtype))
+    ref = oracle.sort_native(host(t), descending=desc)
+    stream = ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
+    st = B.lib.bsort_sort(B.dtype_code(dtype), ctypes.c_void_p(t.data_ptr()), n, int(desc), stream)
+    assert st == 0, B.lib.bsort_status_string(st)
+    torch.cuda.synchronize()
+    assert host(t).tobytes() == ref.tobytes()
+
+
+def test_second_device_after_first(B):
+    """Launch set-up is per device: a sort on cuda:1 after one on cuda:0 works."""
+    if torch.cuda.device_count() < 2:
+        pytest.skip("needs two GPUs")
+    for d in (0, 1):
+        x = gen(torch.float32, (1 << 22) + 5, 77 + d).to(f"cuda:{d}")
+        ref = oracle.sort_native(host(x), descending=False)
+        B.sort_(x)
+        torch.cuda.synchronize(d)
+        assert host(x).tobytes() == ref.tobytes()
+
+
+# ---- presorted fast path (ADVICE r1): the histogram sweep's adjacent-pair check must catch a
+# single out-of-order pair wherever it sits -- inside a 16-byte vector, across vectors (taken
+# from the next lane by a shuffle), across lane 31 / warps (read from memory) and across the
+# grid-stride boundary -- for inputs in the requested order and in the opposite order.
+
+@pytest.mark.parametrize("dtype", [torch.int32, torch.int64])
+@pytest.mark.parametrize("n", [(1 << 22) + 7, (1 << 24) + 11])
+@pytest.mark.parametrize("desc", [False, True])
+def test_presorted_one_swap_interior(B, dtype, n, desc):
+    import paper_2603_08929_b200 as b
+    per_vec = 16 // torch.empty(0, dtype=dtype).element_size()
+    base, _ = torch.sort(W.uniform_int(dtype, n, 4242, "cuda"))
+    want = base.flip(0) if desc else base
+    sms = torch.cuda.get_device_properties(0).multi_processor_count
+    spots = {"in-vector": 4 * per_vec + 1, "vector-boundary": 5 * per_vec - 1,
+             "lane31": 32 * per_vec - 1, "warp": 3 * 32 * per_vec - 1,
+             "grid-stride": sms * 1024 * per_vec - 1}
+    for name, p in spots.items():
+        for src in (want, want.flip(0)):  # requested order / opposite order, one swap each
+            x = src.clone()
+            x[p], x[p + 1] = src[p + 1].item(), src[p].item()
+            if bool((x == src).all()):
+                continue  # equal neighbours: nothing swapped
+            b.sort_(x, descending=desc)
+            torch.cuda.synchronize()
+            assert bool((x == want).all()), f"{name} at {p} (n={n}, desc={desc})"
