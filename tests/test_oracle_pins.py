@@ -307,3 +307,35 @@ def test_bfloat16_matches_float32_order():
     widened = (got.astype(np.uint32) << 16).view(np.float32)
     ref = oracle.sort_native((w.astype(np.uint32) << 16).view(np.float32))
     assert np.array_equal(widened.view(np.uint32), ref.view(np.uint32))
+
+
+def test_fullsize_order_key_matches_oracle_total_order():
+    """tests/test_gpu_fullsize.py checks 2^30-key outputs with a torch restatement of the order
+    (order_key); pin it to the oracle's own total-order key on every f32 pattern class: +-0,
+    +-subnormals, +-normals of every exponent, +-inf, NaNs of both signs with assorted payloads,
+    plus random bit patterns -- sorting by either key must give the same sequence."""
+    import torch
+    from test_gpu_fullsize import order_key
+    rng = np.random.default_rng(20260)
+    cls = [np.array([0x00000000, 0x80000000, 0x7F800000, 0xFF800000, 0x00000001, 0x80000001,
+                     0x007FFFFF, 0x807FFFFF, 0x7F800001, 0xFF800001, 0x7FC00000, 0xFFC00000,
+                     0x7FFFFFFF, 0xFFFFFFFF, 0x00800000, 0x80800000], dtype=np.uint32)]
+    for e in range(256):  # every exponent, both signs, a few mantissas
+        m = rng.integers(0, 1 << 23, 4, dtype=np.uint32)
+        for s in (0, 1):
+            cls.append((np.uint32(s << 31) | np.uint32(e << 23) | m).astype(np.uint32))
+    cls.append(rng.integers(0, 1 << 32, 1 << 20, dtype=np.uint64).astype(np.uint32))
+    x = np.unique(np.concatenate(cls))
+    rng.shuffle(x)
+    k_test = order_key(torch.from_numpy(x.view(np.float32))).numpy()
+    k_orc = oracle.total_order_keys(x.astype(np.uint64), oracle.NATIVE_SCHEMES[np.dtype(np.float32)])
+    a = x[np.argsort(k_test, kind="stable")]
+    b = x[np.argsort(k_orc, kind="stable")]
+    assert np.array_equal(a, b)
+    for dt, bits in ((np.float64, 64),):
+        y = rng.integers(0, 1 << 63, 1 << 18, dtype=np.uint64) | (rng.integers(0, 2, 1 << 18, dtype=np.uint64) << 63)
+        y = np.unique(np.concatenate([y, np.array([0, 1 << 63, 0x7FF0000000000000, 0xFFF0000000000000,
+                                                   0x7FF8000000000000, 0xFFF8000000000000], dtype=np.uint64)]))
+        kt = order_key(torch.from_numpy(y.view(np.int64)).view(torch.float64)).numpy()
+        ko = oracle.total_order_keys(y, oracle.NATIVE_SCHEMES[np.dtype(dt)])
+        assert np.array_equal(y[np.argsort(kt, kind="stable")], y[np.argsort(ko, kind="stable")])
