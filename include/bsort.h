@@ -231,9 +231,15 @@ bsort_status_t bsort_dist_partition_classes(bsort_dtype_t dtype, const void* dev
  * the concatenation of the shards over ranks 0..P-1 is the global order.  Shard boundaries are
  * bin-granular (reading Q16).  *n_out (host, nullable) = this rank's shard size.
  * If any rank's shard exceeds its out_capacity, EVERY rank returns BSORT_ERROR_CAPACITY after
- * the counts exchange with nothing written to dev_out (n_out still set).  Blocks the host twice
- * (after the histogram all-reduce and after the counts all-gather); scratch is
- * cudaMallocAsync'ed on `stream` (n_local keys + partition/sort workspace). */
+ * the counts exchange with nothing written to dev_out (n_out still set).  Blocks the host three
+ * times (after the histogram all-reduce, after the counts all-gather, after the keys exchange);
+ * scratch is cudaMallocAsync'ed on `stream` (n_local keys + partition workspace; the local
+ * sort's workspace is sized from the received count and reuses that block when it fits).
+ * Failure detection: while it waits, the call polls ncclCommGetAsyncError; on an asynchronous
+ * NCCL error, or when a wait exceeds BSORT_NCCL_TIMEOUT_S seconds (environment, default 300,
+ * 0 = no limit: a dead peer), it calls ncclCommAbort and returns BSORT_ERROR_NCCL
+ * (bsort_last_nccl_error: the NCCL code, ncclInternalError for a timeout); the communicator is
+ * then unusable (later calls return BSORT_ERROR_NCCL; bsort_comm_destroy still frees it). */
 typedef struct bsort_comm* bsort_comm_t;
 bsort_status_t bsort_get_unique_id(uint8_t id[128]);
 bsort_status_t bsort_comm_init(bsort_comm_t* out, const uint8_t id[128], int nranks, int rank);

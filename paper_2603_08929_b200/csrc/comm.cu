@@ -19,8 +19,11 @@
 #include <nccl.h>
 
 #include <algorithm>
+#include <chrono>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
+#include <thread>
 #include <vector>
 
 #include "bsort.h"
@@ -40,6 +43,9 @@ struct NcclApi {
   ncclResult_t (*Recv)(void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
   ncclResult_t (*GroupStart)() = nullptr;
   ncclResult_t (*GroupEnd)() = nullptr;
+  // failure detection (optional symbols: without them waits are plain stream syncs)
+  ncclResult_t (*CommGetAsyncError)(ncclComm_t, ncclResult_t*) = nullptr;
+  ncclResult_t (*CommAbort)(ncclComm_t) = nullptr;
 };
 
 NcclApi& nccl() {
@@ -64,6 +70,9 @@ NcclApi& nccl() {
     get(api.GroupStart, "ncclGroupStart");
     get(api.GroupEnd, "ncclGroupEnd");
     api.ok = all;
+    api.CommGetAsyncError =
+        reinterpret_cast<decltype(api.CommGetAsyncError)>(dlsym(h, "ncclCommGetAsyncError"));
+    api.CommAbort = reinterpret_cast<decltype(api.CommAbort)>(dlsym(h, "ncclCommAbort"));
   });
   return api;
 }
@@ -116,7 +125,52 @@ struct bsort_comm {
   int nranks = 0;
   int rank = 0;
   int device = 0;
+  bool aborted = false;  // ncclCommAbort was called (peer failure / timeout): unusable
 };
+
+namespace {
+
+// Wait for the stream while watching the communicator (SURVEY §8 failure detection): a peer that
+// dies mid-collective leaves the stream pending forever, so poll cudaStreamQuery and
+// ncclCommGetAsyncError; on an asynchronous NCCL error, or after BSORT_NCCL_TIMEOUT_S seconds
+// (default 300; 0 = no limit), abort the communicator (its pending collectives are cancelled and
+// the stream drains) and return BSORT_ERROR_NCCL (bsort_last_nccl_error holds the NCCL code,
+// ncclInternalError for a timeout).  Every later call on the communicator fails.
+double nccl_timeout_s() {
+  static const double v = [] {
+    const char* e = getenv("BSORT_NCCL_TIMEOUT_S");
+    return e ? atof(e) : 300.0;
+  }();
+  return v;
+}
+
+bsort_status_t abort_comm(bsort_comm* c, ncclResult_t why) {
+  NcclApi& N = nccl();
+  if (N.CommAbort && c->comm && !c->aborted) N.CommAbort(c->comm);
+  c->aborted = true;
+  return nccl_status(why == ncclSuccess ? ncclInternalError : why);
+}
+
+bsort_status_t wait_watching(cudaStream_t s, bsort_comm* c) {
+  NcclApi& N = nccl();
+  if (!N.CommGetAsyncError) return cuda_status(cudaStreamSynchronize(s));
+  const double limit = nccl_timeout_s();
+  const auto t0 = std::chrono::steady_clock::now();
+  unsigned spins = 0;
+  for (;;) {
+    const cudaError_t q = cudaStreamQuery(s);
+    if (q == cudaSuccess) return BSORT_SUCCESS;
+    if (q != cudaErrorNotReady) return cuda_status(q);
+    ncclResult_t ae = ncclSuccess;
+    if (N.CommGetAsyncError(c->comm, &ae) == ncclSuccess && ae != ncclSuccess && ae != ncclInProgress)
+      return abort_comm(c, ae);
+    if (limit > 0 && std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count() > limit)
+      return abort_comm(c, ncclInternalError);
+    if (++spins > 64) std::this_thread::sleep_for(std::chrono::microseconds(20));
+  }
+}
+
+}  // namespace
 
 namespace {
 
@@ -149,12 +203,13 @@ int refine_cb(void* p, const uint64_t* prefixes, int m, int prefix_bits, uint64_
   const size_t cnt = (size_t)m * BSORT_DIST_BINS;
   if (r->N->AllReduce(r->dev_hist, r->dev_hist, cnt, ncclUint64, ncclSum, r->c->comm, r->s) != ncclSuccess) return 2;
   if (cudaMemcpyAsync(hist, r->dev_hist, cnt * 8, cudaMemcpyDeviceToHost, r->s) != cudaSuccess) return 3;
-  return cudaStreamSynchronize(r->s) == cudaSuccess ? 0 : 4;
+  return wait_watching(r->s, r->c) == BSORT_SUCCESS ? 0 : 4;
 }
 
 bsort_status_t sort_dist_impl(bsort_dtype_t dtype, const void* dev_in, uint64_t n, void* dev_out, uint64_t cap,
                               uint64_t* n_out, bsort_direction_t dir, bool exact, bsort_comm* c, cudaStream_t s) {
   NcclApi& N = nccl();
+  if (c->aborted) return nccl_status(ncclInvalidUsage);
   const int P = c->nranks, me = c->rank;
   const int es = key_bytes(dtype);
   exact = exact && P > 1;  // one rank: every key stays, both modes coincide
@@ -173,9 +228,9 @@ bsort_status_t sort_dist_impl(bsort_dtype_t dtype, const void* dev_in, uint64_t 
   const size_t head = 2 * hist_b + cnt_b + ref_b;
   StreamBlock blk;
   blk.s = s;
-  // the tail must hold the partition phase and, later, the local sort of up to `cap` keys
-  const size_t sort_ws_cap = bsort_workspace_bytes(dtype, cap);
-  const size_t tail = std::max(bucket_b + part_ws, sort_ws_cap);
+  // the tail holds the partition phase; the local sort reuses it when its workspace fits (its
+  // size is known only after the counts all-gather), else takes a second stream-ordered block
+  const size_t tail = bucket_b + part_ws;
   if (cudaMallocAsync(&blk.p, head + tail, s) != cudaSuccess) {
     cudaGetLastError();
     blk.p = nullptr;
@@ -193,7 +248,7 @@ bsort_status_t sort_dist_impl(bsort_dtype_t dtype, const void* dev_in, uint64_t 
   NCCL_TRY(N.AllReduce(l_hist, g_hist, BSORT_DIST_BINS, ncclUint64, ncclSum, c->comm, s));
   std::vector<uint64_t> hist(2 * (size_t)BSORT_DIST_BINS);
   CUDA_TRY(cudaMemcpyAsync(hist.data(), g_hist, 2 * hist_b, cudaMemcpyDeviceToHost, s));
-  CUDA_TRY(cudaStreamSynchronize(s));
+  BS_TRY(wait_watching(s, c));
 
   // a8: per-destination counts of every rank, all-gathered with every rank's capacity.
   // sendm[src * P + dst] = keys src sends to dst; caps[q] = rank q's out_capacity.
@@ -211,7 +266,7 @@ bsort_status_t sort_dist_impl(bsort_dtype_t dtype, const void* dev_in, uint64_t 
     NCCL_TRY(N.AllGather(d_cnt + (size_t)me * CW, d_cnt, CW, ncclUint64, c->comm, s));
     std::vector<uint64_t> all((size_t)P * CW);
     CUDA_TRY(cudaMemcpyAsync(all.data(), d_cnt, all.size() * 8, cudaMemcpyDeviceToHost, s));
-    CUDA_TRY(cudaStreamSynchronize(s));
+    BS_TRY(wait_watching(s, c));
     for (int q = 0; q < P; ++q) {
       for (int d = 0; d < P; ++d) sendm[(size_t)q * P + d] = all[(size_t)q * CW + d];
       caps[q] = all[(size_t)q * CW + P];
@@ -230,7 +285,7 @@ bsort_status_t sort_dist_impl(bsort_dtype_t dtype, const void* dev_in, uint64_t 
       NCCL_TRY(N.AllGather(d_cnt + (size_t)me * CW, d_cnt, CW, ncclUint64, c->comm, s));
       std::vector<uint64_t> all((size_t)P * CW);
       CUDA_TRY(cudaMemcpyAsync(all.data(), d_cnt, all.size() * 8, cudaMemcpyDeviceToHost, s));
-      CUDA_TRY(cudaStreamSynchronize(s));
+      BS_TRY(wait_watching(s, c));
       std::vector<uint64_t> cc((size_t)P * C);
       for (int q = 0; q < P; ++q) {
         for (int k = 0; k < C; ++k) cc[(size_t)q * C + k] = all[(size_t)q * CW + k];
@@ -284,11 +339,25 @@ bsort_status_t sort_dist_impl(bsort_dtype_t dtype, const void* dev_in, uint64_t 
   const ncclResult_t ge = N.GroupEnd();
   NCCL_TRY(first);
   NCCL_TRY(ge);
+  // the exchange is where a dead peer would hang every rank: wait for it watching the comm
+  BS_TRY(wait_watching(s, c));
 
-  // a11: local sort of the received keys (workspace reuses the bucketed region, now dead)
+  // a11: local sort of the received keys; workspace = the bucketed region (dead now) when it is
+  // large enough for recv_total keys, else a second stream-ordered block of exactly that size
   if (recv_total > 1) {
     const size_t wsb = bsort_workspace_bytes(dtype, recv_total);
-    BS_TRY(bsort_sort_ws(dtype, dev_out, recv_total, dir, bucket, wsb, s));
+    StreamBlock more;
+    more.s = s;
+    void* sws = bucket;
+    if (wsb > tail) {
+      if (cudaMallocAsync(&more.p, wsb, s) != cudaSuccess) {
+        cudaGetLastError();
+        more.p = nullptr;
+        return BSORT_ERROR_OUT_OF_MEMORY;
+      }
+      sws = more.p;
+    }
+    BS_TRY(bsort_sort_ws(dtype, dev_out, recv_total, dir, sws, wsb, s));
   }
   return BSORT_SUCCESS;
 }
@@ -331,7 +400,8 @@ bsort_status_t bsort_comm_init(bsort_comm_t* out, const uint8_t id[128], int nra
 bsort_status_t bsort_comm_destroy(bsort_comm_t c) {
   if (!c) return BSORT_ERROR_INVALID_ARGUMENT;
   NcclApi& N = nccl();
-  ncclResult_t r = N.ok && c->comm ? N.CommDestroy(c->comm) : ncclSuccess;
+  // an aborted communicator was already released by ncclCommAbort
+  ncclResult_t r = N.ok && c->comm && !c->aborted ? N.CommDestroy(c->comm) : ncclSuccess;
   delete c;
   return nccl_status(r);
 }
