@@ -10,27 +10,65 @@ using namespace lsd_detail;
 namespace {
 constexpr int TOP_BINS = BSORT_DIST_BINS;
 
-// Top-16-bit histogram of the transformed keys: 65536 u32 bins do not fit next to a useful
-// occupancy, so each CTA counts into a 16-bit-index smem table of 32768 u32 for its half of
-// the bins (CTA pairs, as in the 16-bit counting path) and flushes with global atomics.
+// Top-16-bit histogram of the transformed keys (a7), one read of the keys: one CTA of 1024
+// threads per SM holds all 65536 bins as u16 halves of 32768 smem words (128 KB); a half that
+// reaches 0x8000 is drained into the global count (as the 16-bit counting path does), so the
+// table never overflows.  Keys are read with 128-bit streaming loads, grid-stride; each CTA adds
+// its nonzero bins to the global histogram at the end.  (Round 1: CTA pairs each read ALL keys
+// and kept half of the bins -- 2x the algorithmic bytes.)
+__device__ __forceinline__ uint4 ldg_stream16(const void* p) {
+  uint4 r;
+  asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+               : "l"(p));
+  return r;
+}
+
 template <int KIND, bool DESC, typename U>
 __global__ void __launch_bounds__(1024, 1)
     k_dist_tophist(const U* __restrict__ keys, uint64_t n, unsigned long long* __restrict__ hist) {
-  extern __shared__ uint32_t th[];
-  const uint32_t half = blockIdx.x & 1;
-  const uint32_t chunk = blockIdx.x >> 1;
-  const uint32_t pairs = gridDim.x >> 1;
+  extern __shared__ uint32_t th[];  // bin 2w in the low half of word w, 2w + 1 in the high half
   for (int i = threadIdx.x; i < TOP_BINS / 2; i += 1024) th[i] = 0;
   __syncthreads();
-  const uint64_t per = (n + pairs - 1) / pairs;
-  const uint64_t s0 = min64(n, (uint64_t)chunk * per), s1 = min64(n, s0 + per);
-  for (uint64_t i = s0 + threadIdx.x; i < s1; i += 1024) {
-    const uint32_t b = uint32_t(key_encode<KIND, DESC>(keys[i]) >> (sizeof(U) * 8 - 16));
-    if ((b >> 15) == half) atomicAdd(&th[b & 0x7FFF], 1u);
+  constexpr int SH = (int)sizeof(U) * 8 - 16;
+  auto add = [&](U x) {
+    const uint32_t b = uint32_t(key_encode<KIND, DESC>(x) >> SH);
+    const uint32_t sh = (b & 1u) << 4;
+    const uint32_t old = atomicAdd(&th[b >> 1], 1u << sh);
+    if (((old >> sh) & 0xFFFFu) == 0x7FFFu) {  // this add made the half 0x8000: drain it
+      atomicAdd(&th[b >> 1], 0u - (0x8000u << sh));
+      atomicAdd(&hist[b], 0x8000ull);
+    }
+  };
+  constexpr int PER_VEC = 16 / (int)sizeof(U);
+  const uint64_t T = (uint64_t)gridDim.x * 1024;
+  const uint64_t gt = (uint64_t)blockIdx.x * 1024 + threadIdx.x;
+  const uint64_t head = min64(n, ((16 - ((uintptr_t)keys & 15)) & 15) / sizeof(U));
+  for (uint64_t i = gt; i < head; i += T) add(keys[i]);
+  const U* vbase = keys + head;
+  const uint64_t nv = (n - head) / PER_VEC;
+  auto vec = [&](uint4 q) {
+    if constexpr (sizeof(U) == 4) {
+      add(U(q.x)); add(U(q.y)); add(U(q.z)); add(U(q.w));
+    } else {
+      add(U(q.x) | (U(q.y) << 32));
+      add(U(q.z) | (U(q.w) << 32));
+    }
+  };
+  uint64_t i = gt;
+  for (; i + 3 * T < nv; i += 4 * T) {
+    const uint4 q0 = ldg_stream16(vbase + i * PER_VEC), q1 = ldg_stream16(vbase + (i + T) * PER_VEC);
+    const uint4 q2 = ldg_stream16(vbase + (i + 2 * T) * PER_VEC), q3 = ldg_stream16(vbase + (i + 3 * T) * PER_VEC);
+    vec(q0); vec(q1); vec(q2); vec(q3);
   }
+  for (; i < nv; i += T) vec(ldg_stream16(vbase + i * PER_VEC));
+  for (uint64_t j = head + nv * PER_VEC + gt; j < n; j += T) add(keys[j]);
   __syncthreads();
-  for (int b = threadIdx.x; b < TOP_BINS / 2; b += 1024)
-    if (th[b]) atomicAdd(&hist[half * (TOP_BINS / 2) + b], (unsigned long long)th[b]);
+  for (int w = threadIdx.x; w < TOP_BINS / 2; w += 1024) {
+    const uint32_t c = th[w];
+    if (c & 0xFFFFu) atomicAdd(&hist[2 * w], (unsigned long long)(c & 0xFFFFu));
+    if (c >> 16) atomicAdd(&hist[2 * w + 1], (unsigned long long)(c >> 16));
+  }
 }
 
 template <int KIND, bool DESC, typename U>
@@ -45,8 +83,7 @@ bsort_status_t tophist_run(const U* keys, uint64_t n, uint64_t* hist, cudaStream
     BSORT_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
     attr.mark();
   }
-  const int pairs = max(1, num_sms() / 2);
-  BSORT_LAUNCH(PROF_DIST_HIST, s, k<<<2 * pairs, 1024, smem, s>>>(keys, n, h));
+  BSORT_LAUNCH(PROF_DIST_HIST, s, k<<<num_sms(), 1024, smem, s>>>(keys, n, h));
   return BSORT_SUCCESS;
 }
 

@@ -66,6 +66,23 @@ def test_top_hist(B, dtype, descending):
         assert np.array_equal(h, ref)
 
 
+@pytest.mark.parametrize("dtype", [torch.int32, torch.float32, torch.int64])
+def test_top_hist_skewed(B, dtype):
+    """Bins past 0x8000 keys per CTA (the u16 halves drain into the global counts), misaligned
+    start, and a few-value input (32-way same-bin atomics)."""
+    n = (1 << 22) + 5
+    x = torch.full((n,), 3, dtype=dtype, device="cuda")
+    x[::7] = 5
+    x[1::13] = -2 if dtype.is_signed else 9
+    for t in (x, x[1:]):
+        h = B.top_hist(t, False).view(torch.int64).cpu().numpy()
+        ref = np.bincount(top16_oracle(host(t), False), minlength=65536)
+        assert np.array_equal(h, ref)
+    y = gen(dtype, (1 << 24) + 3, 99)  # several grid-stride rounds
+    h = B.top_hist(y, True).view(torch.int64).cpu().numpy()
+    assert np.array_equal(h, np.bincount(top16_oracle(host(y), True), minlength=65536))
+
+
 @pytest.mark.parametrize("dtype", [torch.int32, torch.float64])
 @pytest.mark.parametrize("P", [2, 3, 8])
 def test_partition_buckets(B, dtype, P):
