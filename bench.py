@@ -5,11 +5,13 @@
 
 N=1 (default): one step = one full sort of BASELINE.json cfg3 (2^30 f32 keys, mixed
 distribution, ascending) already resident in HBM.  N>1 (torchrun, one rank per GPU, NCCL):
-one step = sort_dist of 2^30 cfg3-distributed f32 keys PER RANK (weak scaling): MSD
-histogram + all-reduce + partition + all-to-all + local sort.  Rank 0 prints ONE JSON line.
+one step = one bsort_sort_dist call (C-ABI) on BASELINE.json cfg5 -- 2^33 int64 keys in total,
+2^33/N per rank (strong scaling; float64 and 2^30 keys per rank weak scaling measured too):
+MSD histogram + all-reduce + partition + grouped send/recv + local sort.  --force-dist runs
+that path on one GPU (weak shape).  Rank 0 prints ONE JSON line.
 
-Timing: CUDA events on the sorting stream around each step (device time); the input is
-restored by a device copy between steps, outside the events.  Inputs are 4 GiB per buffer,
+Timing: CUDA events on the sorting stream around each step (device time); the N=1 input is
+restored by a device copy between steps, outside the events.  Inputs are >= 4 GiB per buffer,
 far larger than the 126 MB L2, so no flush is needed.  The per-kernel roofline comes from
 libbsort's own CUDA events recorded around every kernel during the same timed steps.
 --impl reference times the CPU oracle (the reference arm for this tier) on a bounded sample.
@@ -391,109 +393,199 @@ def emit(text: str):
         os.write(_JSON_FD, (text + "\n").encode())
 
 
+CFG5_TOTAL = 1 << 33   # BASELINE.json cfg5: 2^33 keys in total (strong scaling over 2/4/8 GPUs)
+CFG5_WEAK = 1 << 30    # weak-scaling companion: 2^30 keys per rank
+
+
+def multi_shapes(world: int, force_weak: bool = False):
+    """The N > 1 measurements: [(name, mode, dtype, n_per_rank)], the headline first.
+    At world size 1 (--force-dist) the 2^33-key strong shape does not fit one GPU (64 GiB of keys
+    + a shard + the workspace), so the headline is the weak shape."""
+    shapes = []
+    if world > 1 and not force_weak:
+        shapes += [("strong_i64", "strong", "i64", CFG5_TOTAL // world),
+                   ("strong_f64", "strong", "f64", CFG5_TOTAL // world)]
+    shapes += [("weak_i64", "weak", "i64", CFG5_WEAK), ("weak_f64", "weak", "f64", CFG5_WEAK)]
+    return shapes
+
+
+def multi_line(world, steps, warmup, head, results, e2e, a2a_ref, launches, clocks, exact=False):
+    """The N > 1 JSON line (pure: tested on CPU by tests/test_bench_contract.py).
+    head = the headline (name, mode, dtype, n_per_rank); results[name] = {"ms", "a2a_ms",
+    "a2a_bytes", "pass_ms", "pass_bytes", "n_out"} (max-over-ranks ms); e2e = {"ms", "h2d", "d2h"}
+    or {"error": ...}; a2a_ref = NCCL all_to_all_single per-rank egress GB/s at 1 GiB per pair."""
+    name, mode, dt, n_loc = head
+    r = results[name]
+    total = n_loc * world
+    hbm_peak, peak_src = load_peaks()
+    achieved = r["pass_bytes"] / (r["pass_ms"] / 1e3) / 1e9 if r.get("pass_ms") else None
+    a2a_gbs = r["a2a_bytes"] / (r["a2a_ms"] / 1e3) / 1e9 if r.get("a2a_ms") else None
+    others = {}
+    for k, v in results.items():
+        nl = v["n_per_rank"]
+        others[k] = {"keys_per_s": nl * world / (v["ms"] / 1e3), "ms": v["ms"], "n_per_rank": nl,
+                     "dtype": v["dtype"], "mode": v["mode"], "a2a_ms": v.get("a2a_ms"),
+                     "a2a_GBps_egress_rank0": (v["a2a_bytes"] / (v["a2a_ms"] / 1e3) / 1e9
+                                               if v.get("a2a_ms") else None)}
+    e2e_rec = None
+    if e2e is not None:
+        if "error" in e2e:
+            e2e_rec = {"value": None, "unit": UNIT, "h2d_bytes_per_step": None, "d2h_bytes_per_step": None,
+                       "error": e2e["error"]}
+        else:
+            e2e_rec = {"value": total / (e2e["ms"] / 1e3), "unit": UNIT, "h2d_bytes_per_step": e2e["h2d"],
+                       "d2h_bytes_per_step": e2e["d2h"], "ms_per_step": e2e["ms"],
+                       "note": "per rank: pinned host keys -> H2D -> bsort_sort_dist (C-ABI) -> D2H of the "
+                               "shard; CUDA events, max over ranks; bytes are rank 0's"}
+    return {
+        "metric": METRIC, "value": total / (r["ms"] / 1e3), "unit": UNIT, "n_gpus": world,
+        "steps": steps, "warmup": warmup, "ms_per_step": r["ms"], "higher_is_better": True,
+        "scaling": mode, "vs_baseline": None, "dtype": dt, "data": "synthetic",
+        "config": {"workload": f"cfg5: {total} {dt} keys uniform over all "
+                               f"{'bit patterns' if dt == 'i64' else 'finite bit patterns'}, "
+                               f"{n_loc} per rank x {world} ranks, globally sorted shards",
+                   "n_per_rank": n_loc, "n_total": total, "key": dt, "direction": "ascending",
+                   "path": "bsort_sort_dist (C-ABI): a7 top-16-bit histogram + NCCL all-reduce + splitters "
+                           "+ counts all-gather + a9 partition + grouped NCCL send/recv + local one-sweep LSD",
+                   "parallelism": f"msd-a2a x{world}" + (" exact-split" if exact else ""),
+                   "l2": f"inputs {n_loc * 8} B per rank >> 126 MB L2 (no flush); the input is const "
+                         "(bsort_sort_dist reads dev_in, writes dev_out)"},
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
+                     "frac": (achieved / hbm_peak) if achieved else None, "traffic": None,
+                     "kernel": "local LSD scatter pass of 64-bit keys (8 passes per step)",
+                     "algorithmic_bytes_per_launch": r.get("pass_bytes"), "avg_launch_ms": r.get("pass_ms"),
+                     "peak_source": peak_src,
+                     "a2a": {"ms_per_step": r.get("a2a_ms"), "bytes_per_step_rank0": r.get("a2a_bytes"),
+                             "GBps_egress_rank0": a2a_gbs, "nccl_all_to_all_1GiB_pair_GBps": a2a_ref,
+                             "frac_of_nccl_a2a": (a2a_gbs / a2a_ref) if (a2a_gbs and a2a_ref) else None,
+                             "note": "exchange = grouped ncclSend/ncclRecv inside bsort_sort_dist, timed by "
+                                     "libbsort's dist_a2a profile events (a separate profiled run)"}},
+        "cpu_baseline": None,
+        "e2e": e2e_rec,
+        "gpu_launches": launches,
+        "clocks": clocks,
+        "configs": others,
+    }
+
+
 def bench_multi(args, B):
-    """N > 1: one step = sort_dist of 2^30 cfg3-distributed f32 keys per rank (weak scaling)."""
+    """N > 1 (torchrun, one rank per GPU) or --force-dist: BASELINE.json cfg5 through the C-ABI
+    bsort_sort_dist (B.Comm + B.sort_dist_native).  Headline: 2^33 int64 keys in total (strong
+    scaling); float64 and the 2^30-per-rank weak shape are measured too (under "configs").
+    A step = one bsort_sort_dist call (input const, shard written to a separate buffer)."""
     import torch.distributed as dist
+    import workloads as W
     rank, world = dist.get_rank(), dist.get_world_size()
     local = int(os.environ.get("LOCAL_RANK", rank))
     dev = torch.device("cuda", local)
     torch.cuda.set_device(dev)
     stream = torch.cuda.current_stream(dev)
-    n = args.n or N_CFG3
-    pristine = cfg3_input(n, dev, rank)
-    work = torch.empty_like(pristine)
-    restore = lambda: work.copy_(pristine)  # noqa: E731
-    for _ in range(args.warmup):
-        restore()
-        B.sort_dist(work, exact=args.exact)
-    torch.cuda.synchronize()
-    dist.barrier()
-    launches0 = B.launch_count()
-    a2a = []
-    with ClockSampler(local) as clk:
-        restore()
-        torch.cuda.synchronize()
-        dist.barrier()
-        a = torch.cuda.Event(enable_timing=True)
-        b = torch.cuda.Event(enable_timing=True)
-        step_ev = []
-        a.record(stream)
-        for i in range(args.steps):
-            # the restore copy is outside the step events but inside the bracket (input >> L2)
-            if i:
-                restore()
-            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            e0.record(stream)
-            B.sort_dist(work, a2a_events=a2a, exact=args.exact)
-            e1.record(stream)
-            step_ev.append((e0, e1))
-        b.record(stream)
-        torch.cuda.synchronize()
-        dist.barrier()
-    launches = B.launch_count() - launches0
-    step_ms = sum(e0.elapsed_time(e1) for e0, e1 in step_ev)
-    a2a_ms = sum(ev[0].elapsed_time(ev[1]) for ev, _ in a2a)
-    a2a_bytes = sum(nb for _, nb in a2a)
-    t = torch.tensor([step_ms, a2a_ms], dtype=torch.float64, device=dev)
-    dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    ms = t[0].item() / args.steps
-    a2a_max_ms = t[1].item() / args.steps
+    comm = B.Comm()
+    shapes = multi_shapes(world)
+    if args.n:
+        shapes = [("weak_i64", "weak", "i64", args.n)]
+    if args.quick:
+        shapes = shapes[:1]
+    head = shapes[0]
+    tdt = {"i64": torch.int64, "f64": torch.float64}
 
-    # end to end through the public API: pinned host keys -> H2D -> sort_dist -> D2H of the shard
-    host = pristine.cpu().pin_memory()
-    host_out = torch.empty(2 * n, dtype=pristine.dtype).pin_memory()  # shard ~ n keys per rank
-    e_times, out_bytes = [], 0
-    for i in range(2):
+    def maxr(v):
+        t = torch.tensor([float(v)], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return t.item()
+
+    results, e2e, launches, clocks = {}, None, None, None
+    for name, mode, dt, n_loc in shapes:
+        x = W.make("cfg5", dev, n=n_loc * world, dtype=tdt[dt], rank=rank, world=world)
+        cap = n_loc + n_loc // 16 + (1 << 16)
+        run = lambda: B.sort_dist_native(x, comm, capacity=cap, exact=args.exact)  # noqa: E731
+        for _ in range(args.warmup):
+            out = run()
+            del out
+        torch.cuda.synchronize()
+        dist.barrier()
+        l0 = B.launch_count()
+        sampler = ClockSampler(local) if name == head[0] else None
+        if sampler:
+            sampler.__enter__()
+        ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+              for _ in range(args.steps)]
+        for i in range(args.steps):
+            ev[i][0].record(stream)
+            out = run()
+            ev[i][1].record(stream)
+            del out
+        torch.cuda.synchronize()
+        if sampler:
+            sampler.__exit__(None, None, None)
+            clocks = sampler.summary()
+            launches = B.launch_count() - l0
+        dist.barrier()
+        ms = maxr(sum(a.elapsed_time(b) for a, b in ev) / args.steps)
+        # a separate profiled run: the exchange (dist_a2a events) and the local LSD passes
+        with B.profile() as prof:
+            out = run()
+        n_out = out.numel()
+        del out
+        pk = prof.get("onesweep_pass", {"ms": 0.0})
+        a2 = prof.get("dist_a2a", {"ms": 0.0})
+        res = {"ms": ms, "mode": mode, "dtype": dt, "n_per_rank": n_loc,
+               "a2a_ms": maxr(a2["ms"]), "a2a_bytes": None, "n_out": n_out,
+               "pass_ms": maxr(pk["ms"] / 8) if pk["ms"] else None, "pass_bytes": 2 * n_out * 8}
+        # rank 0's egress bytes (keys to the other ranks): n_loc minus what it keeps
+        res["a2a_bytes"] = _egress_bytes(B, x, comm, world, rank) if world > 1 else 0
+        results[name] = res
+        if name == head[0] and not (args.quick and not args.e2e):
+            e2e = _e2e_dist(B, x, comm, cap, args, dev, stream, maxr)
+        del x
+        torch.cuda.empty_cache()
+    a2a_ref = a2a_microbench(dev, bytes_per_pair=1 << 30) if world > 1 else None
+    comm.close()
+    if rank == 0:
+        emit(json.dumps(multi_line(world, args.steps, args.warmup, head, results, e2e, a2a_ref, launches,
+                                   clocks, exact=args.exact)))
+
+
+def _egress_bytes(B, x, comm, world, rank):
+    """Bytes this rank sends to other ranks in one bsort_sort_dist of x (bin-granular split):
+    from the same top-16-bit histograms libbsort computes (B.top_hist + all-reduce)."""
+    import torch.distributed as dist
+    hl = B.top_hist(x)
+    hg = hl.clone()
+    dist.all_reduce(hg.view(torch.int64), op=dist.ReduceOp.SUM)
+    cuts = B.splitters(hg.view(torch.int64).cpu().numpy().view(np.uint64), world)
+    sc = B.send_counts(hl.view(torch.int64).cpu().numpy().view(np.uint64), cuts)
+    return int((int(sc.sum()) - int(sc[rank])) * x.element_size())
+
+
+def _e2e_dist(B, x, comm, cap, args, dev, stream, maxr):
+    """End to end through the public API: pinned host keys -> H2D -> bsort_sort_dist -> D2H."""
+    try:
+        host = x.cpu().pin_memory()
+        host_out = torch.empty(cap, dtype=x.dtype).pin_memory()
+    except RuntimeError as e:
+        return {"error": f"pinned host buffers: {str(e).splitlines()[0]}"}
+    work = torch.empty_like(x)
+    times, out_bytes = [], 0
+    for i in range(3):
+        import torch.distributed as dist
         dist.barrier()
         torch.cuda.synchronize()
-        ea, eb = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        ea.record(stream)
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
         work.copy_(host, non_blocking=True)
-        shard = B.sort_dist(work, exact=args.exact)
-        if shard.numel() > host_out.numel():
-            host_out = torch.empty(shard.numel(), dtype=shard.dtype).pin_memory()
+        shard = B.sort_dist_native(work, comm, capacity=cap, exact=args.exact)
         res = host_out[:shard.numel()]
         res.copy_(shard, non_blocking=True)
-        eb.record(stream)
+        b.record(stream)
         torch.cuda.synchronize()
         out_bytes = res.numel() * res.element_size()
+        del shard
         if i:
-            e_times.append(ea.elapsed_time(eb))
-    te = torch.tensor([max(e_times)], dtype=torch.float64, device=dev)
-    dist.all_reduce(te, op=dist.ReduceOp.MAX)
-    del host, host_out
-    a2a_gbs = a2a_microbench(dev)  # collective; None at world size 1
-    total = n * world
-    if rank == 0:
-        nv_peak, nv_src = nvlink_peak()
-        if a2a_gbs is not None:
-            nv_peak, nv_src = a2a_gbs, ("measured here: NCCL all_to_all_single, 256 MiB per rank pair, "
-                                        "per-rank egress, max over ranks")
-        per_rank_bytes = a2a_bytes / max(1, args.steps)
-        achieved = per_rank_bytes / (a2a_max_ms / 1e3) / 1e9 if a2a_max_ms > 0 else None
-        line = {
-            "metric": METRIC, "value": total / (ms / 1e3), "unit": UNIT, "n_gpus": world,
-            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "u32", "data": "synthetic",
-            "config": {"workload": f"cfg3 distribution, {n} f32 keys per rank x {world} ranks, "
-                                   "globally sorted shards (MSD top-16-bit split + NCCL all-to-all "
-                                   "+ local one-sweep LSD)", "n_per_rank": n,
-                       "parallelism": f"msd-a2a x{world}" + (" exact-split" if args.exact else ""),
-                       "l2": "inputs of n*4 B per rank (4 GiB at the default n) >> L2; restored by D2D copy between steps"},
-            "roofline": {"bound": "nvlink", "achieved": achieved, "peak": nv_peak, "unit": "GB/s",
-                         "frac": (achieved / nv_peak) if achieved else None, "traffic": None,
-                         "kernel": "keys all-to-all (NCCL, rank 0's egress bytes / max-over-ranks time)",
-                         "a2a_ms_per_step": a2a_max_ms, "a2a_bytes_per_step_rank0": per_rank_bytes,
-                         "peak_source": nv_src},
-            "cpu_baseline": None,
-            "e2e": {"value": total / (te.item() / 1e3), "unit": UNIT,
-                    "h2d_bytes_per_step": n * 4, "d2h_bytes_per_step": out_bytes,
-                    "ms_per_step": te.item(),
-                    "note": "per rank: pinned host keys -> H2D -> sort_dist -> D2H of the shard; max over ranks"},
-            "gpu_launches": launches,
-            "clocks": clk.summary(),
-        }
-        emit(json.dumps(line))
+            times.append(a.elapsed_time(b))
+    ms = maxr(max(times))
+    del host, host_out, work
+    return {"ms": ms, "h2d": x.numel() * x.element_size(), "d2h": out_bytes}
 
 
 # ------------------------------------------------------------------------ reference arm

@@ -294,8 +294,9 @@ uint64_t bsort_launch_count(void);
  * kernel this library launches.  bsort_profile_enable(1) clears and starts recording,
  * bsort_profile_enable(0) stops.  bsort_profile_read() synchronises the recorded events and
  * fills, per kernel kind (BSORT_PROF_KINDS entries), the summed milliseconds and launch count;
- * returns the number of kinds.  Kind names: bsort_profile_kind_name(). */
-#define BSORT_PROF_KINDS 12
+ * returns the number of kinds.  Kind names: bsort_profile_kind_name().  Kind 12 ("dist_a2a") is
+ * not a kernel: it brackets bsort_sort_dist's grouped NCCL send/recv (the key exchange). */
+#define BSORT_PROF_KINDS 13
 void bsort_profile_enable(int on);
 int bsort_profile_read(double* ms_per_kind, uint64_t* launches_per_kind);
 const char* bsort_profile_kind_name(int kind);

@@ -19,7 +19,7 @@ DTYPE_BYTES = [1, 1, 2, 2, 4, 4, 4, 8, 8, 8, 2, 2]
 ASCENDING, DESCENDING = 0, 1
 DIST_BINS = 65536
 DIST_MAX_RANKS = 64
-PROF_KINDS = 12
+PROF_KINDS = 13
 
 SUCCESS = 0
 ERROR_NCCL = 6

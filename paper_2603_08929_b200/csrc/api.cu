@@ -541,7 +541,7 @@ int bsort_profile_read(double* ms, uint64_t* launches) {
 const char* bsort_profile_kind_name(int k) {
   static const char* names[BSORT_PROF_KINDS] = {"memset", "onesweep_hist", "plan_scan", "onesweep_pass",
                                                 "copy_back", "count_hist", "count_scan", "count_fill",
-                                                "dist_tophist", "dist_partition", "h2d", "d2h"};
+                                                "dist_tophist", "dist_partition", "h2d", "d2h", "dist_a2a"};
   return (k >= 0 && k < BSORT_PROF_KINDS) ? names[k] : "?";
 }
 

@@ -28,6 +28,7 @@
 
 #include "bsort.h"
 #include "common.cuh"
+#include "common.cuh"
 
 namespace {
 
@@ -126,6 +127,12 @@ struct bsort_comm {
   int rank = 0;
   int device = 0;
   bool aborted = false;  // ncclCommAbort was called (peer failure / timeout): unusable
+  // Grow-only device workspace reused by every bsort_sort_dist call on this communicator (a
+  // fresh multi-GiB cudaMallocAsync per call would remap pages whenever the pool trims).
+  // ws_done is recorded after each call's last use; the next call's stream waits on it.
+  void* ws = nullptr;
+  size_t ws_bytes = 0;
+  cudaEvent_t ws_done = nullptr;
 };
 
 namespace {
@@ -174,12 +181,36 @@ bsort_status_t wait_watching(cudaStream_t s, bsort_comm* c) {
 
 namespace {
 
-// RAII for the call's single cudaMallocAsync block (freed stream-ordered on every exit path).
-struct StreamBlock {
-  void* p = nullptr;
-  cudaStream_t s = nullptr;
-  ~StreamBlock() {
-    if (p) cudaFreeAsync(p, s);
+// The communicator's cached workspace, at least `bytes`, ordered after its previous use on
+// whatever stream that was.  Growing frees the old block stream-ordered (its contents are dead:
+// callers grow only between phases).  nullptr on allocation failure.
+void* comm_ws(bsort_comm* c, size_t bytes, cudaStream_t s) {
+  if (c->ws_done) cudaStreamWaitEvent(s, c->ws_done, 0);
+  if (bytes <= c->ws_bytes && c->ws) return c->ws;
+  if (c->ws) cudaFreeAsync(c->ws, s);
+  c->ws = nullptr;
+  c->ws_bytes = 0;
+  if (cudaMallocAsync(&c->ws, bytes, s) != cudaSuccess) {
+    cudaGetLastError();
+    c->ws = nullptr;
+    return nullptr;
+  }
+  c->ws_bytes = bytes;
+  return c->ws;
+}
+
+// Marks the end of a call's use of the cached workspace (on every exit path).
+struct WsUse {
+  bsort_comm* c;
+  cudaStream_t s;
+  ~WsUse() {
+    if (!c->ws_done && cudaEventCreateWithFlags(&c->ws_done, cudaEventDisableTiming) != cudaSuccess) {
+      cudaGetLastError();
+      c->ws_done = nullptr;
+      cudaStreamSynchronize(s);  // no event: order the next call by draining this one
+      return;
+    }
+    cudaEventRecord(c->ws_done, s);
   }
 };
 
@@ -226,17 +257,13 @@ bsort_status_t sort_dist_impl(bsort_dtype_t dtype, const void* dev_in, uint64_t 
   const size_t part_ws = exact ? bsort_dist_class_partition_workspace_bytes()
                                : bsort_dist_partition_workspace_bytes(dtype, n, P);
   const size_t head = 2 * hist_b + cnt_b + ref_b;
-  StreamBlock blk;
-  blk.s = s;
-  // the tail holds the partition phase; the local sort reuses it when its workspace fits (its
-  // size is known only after the counts all-gather), else takes a second stream-ordered block
+  // the communicator's cached workspace: [head | tail], the tail holding the partition phase;
+  // the local sort's workspace (size known only after the counts all-gather) reuses the whole
+  // block, grown if needed once the partition phase is dead
   const size_t tail = bucket_b + part_ws;
-  if (cudaMallocAsync(&blk.p, head + tail, s) != cudaSuccess) {
-    cudaGetLastError();
-    blk.p = nullptr;
-    return BSORT_ERROR_OUT_OF_MEMORY;
-  }
-  char* base = static_cast<char*>(blk.p);
+  WsUse use{c, s};
+  char* base = static_cast<char*>(comm_ws(c, head + tail, s));
+  if (!base) return BSORT_ERROR_OUT_OF_MEMORY;
   uint64_t* g_hist = reinterpret_cast<uint64_t*>(base);
   uint64_t* l_hist = reinterpret_cast<uint64_t*>(base + hist_b);
   uint64_t* d_cnt = reinterpret_cast<uint64_t*>(base + 2 * hist_b);
@@ -323,6 +350,7 @@ bsort_status_t sort_dist_impl(bsort_dtype_t dtype, const void* dev_in, uint64_t 
   }
 
   // a10: grouped send/recv; rank r's keys land at sum_{r'<r} sent(r', me) in dev_out
+  bsort::prof_begin(bsort::PROF_DIST_A2A, s);
   NCCL_TRY(N.GroupStart());
   ncclResult_t first = ncclSuccess;
   uint64_t soff = 0, roff = 0;
@@ -337,26 +365,18 @@ bsort_status_t sort_dist_impl(bsort_dtype_t dtype, const void* dev_in, uint64_t 
     roff += rc;
   }
   const ncclResult_t ge = N.GroupEnd();
+  bsort::prof_end(bsort::PROF_DIST_A2A, s);
   NCCL_TRY(first);
   NCCL_TRY(ge);
   // the exchange is where a dead peer would hang every rank: wait for it watching the comm
   BS_TRY(wait_watching(s, c));
 
-  // a11: local sort of the received keys; workspace = the bucketed region (dead now) when it is
-  // large enough for recv_total keys, else a second stream-ordered block of exactly that size
+  // a11: local sort of the received keys in the cached workspace (everything in it is dead
+  // now), grown to the local sort's size for recv_total keys if that exceeds it
   if (recv_total > 1) {
     const size_t wsb = bsort_workspace_bytes(dtype, recv_total);
-    StreamBlock more;
-    more.s = s;
-    void* sws = bucket;
-    if (wsb > tail) {
-      if (cudaMallocAsync(&more.p, wsb, s) != cudaSuccess) {
-        cudaGetLastError();
-        more.p = nullptr;
-        return BSORT_ERROR_OUT_OF_MEMORY;
-      }
-      sws = more.p;
-    }
+    void* sws = comm_ws(c, wsb, s);
+    if (!sws) return BSORT_ERROR_OUT_OF_MEMORY;
     BS_TRY(bsort_sort_ws(dtype, dev_out, recv_total, dir, sws, wsb, s));
   }
   return BSORT_SUCCESS;
@@ -402,6 +422,11 @@ bsort_status_t bsort_comm_destroy(bsort_comm_t c) {
   NcclApi& N = nccl();
   // an aborted communicator was already released by ncclCommAbort
   ncclResult_t r = N.ok && c->comm && !c->aborted ? N.CommDestroy(c->comm) : ncclSuccess;
+  if (c->ws_done) {
+    cudaEventSynchronize(c->ws_done);
+    cudaEventDestroy(c->ws_done);
+  }
+  if (c->ws) cudaFree(c->ws);
   delete c;
   return nccl_status(r);
 }

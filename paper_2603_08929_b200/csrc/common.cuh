@@ -88,8 +88,9 @@ enum ProfKind : int {
   PROF_DIST_PART = 9,
   PROF_H2D = 10,
   PROF_D2H = 11,
+  PROF_DIST_A2A = 12,  // bsort_sort_dist's grouped NCCL send/recv (not a libbsort kernel)
 };
-static_assert(BSORT_PROF_KINDS == 12, "keep ProfKind in sync with the header");
+static_assert(BSORT_PROF_KINDS == 13, "keep ProfKind in sync with the header");
 
 void prof_begin(int kind, cudaStream_t s);
 int current_device();  // cudaGetDevice, clamped to [0, 64)

@@ -182,3 +182,15 @@ def test_beyond_2_32_keys_u8(B):
     assert int(x[:3].to(torch.int32).sum()) == 21 and int(x[3].item()) == 200
     assert int(x[-3].item()) == 200 and int(x[-2:].to(torch.int32).sum()) == 510
     assert bool((x[3:-2] == 200).all())
+
+
+def test_cfg5_strong_p2_local_i64(B):
+    """The local sort of cfg5's strong-scaling shape at 2 ranks: 2^32 + 12,345 int64 keys on one
+    GPU (more than 2^32 keys: 64-bit counts and tile indices past 2^32 / 7168 tiles)."""
+    n = (1 << 32) + 12345
+    x = W.make("cfg5", "cuda", n=n, dtype=torch.int64)
+    fp = fingerprint(x)
+    y = sort_like_bench(B, x, False)
+    del x
+    check_sorted(y, False)
+    assert fingerprint(y) == fp
