@@ -287,6 +287,15 @@ const char* bsort_status_string(bsort_status_t status);
 int bsort_last_cuda_error(void);          /* raw cudaError_t of the last failure (thread-local) */
 const char* bsort_version(void);
 
+/* Device self-checks of hardware behaviour the fast paths rely on, run on the CURRENT device
+ * (the library also runs them implicitly once per device on first use).  Check 1: lanes of
+ * one warp instruction that atomically add to the same shared-memory word receive the old
+ * values in ascending lane order (the stable rankings of the round-2 look-back pass and of the
+ * small-n kernel use that value as the key's rank; where it fails those kernels are not used).
+ * Returns 0 when every check holds, else a bitmask of failed checks (bit 0 = check 1), or -1
+ * when no device is usable.  Synchronous; allocates 8 bytes; do not call during graph capture. */
+int bsort_selftest(void);
+
 /* Total number of kernels this library has launched since it was loaded (all threads). */
 uint64_t bsort_launch_count(void);
 

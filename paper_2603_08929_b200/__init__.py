@@ -27,7 +27,7 @@ __all__ = ["sort_", "sort", "sort_inplace_", "inplace_workspace_bytes", "sort_pa
            "top_hist", "splitters", "send_counts", "partition", "partition_remote", "refine_hist",
            "class_hist", "partition_classes", "exact_boundaries", "exact_send_counts", "Comm",
            "sort_dist_native", "profile",
-           "launch_count",
+           "launch_count", "selftest",
            "BsortError", "version"]
 
 _TORCH_CODES = {
@@ -47,6 +47,13 @@ def launch_count() -> int:
     return int(lib.bsort_launch_count())
 
 
+def selftest(device=None) -> int:
+    """bsort_selftest on ``device`` (default: current): 0 when the hardware behaviour the fast
+    kernels rely on holds there (shared-atomic lane order), else the bitmask of failed checks."""
+    with torch.cuda.device(device if device is not None else torch.cuda.current_device()):
+        return int(lib.bsort_selftest())
+
+
 def dtype_code(dtype: torch.dtype) -> int:
     try:
         return _TORCH_CODES[dtype]
@@ -58,8 +65,23 @@ def workspace_bytes(dtype: torch.dtype, n: int) -> int:
     return int(lib.bsort_workspace_bytes(dtype_code(dtype), n))
 
 
+_SAME_DEVICE = contextlib.nullcontext()
+
+
+def _on(device):
+    """Context that makes ``device`` current for libbsort's launches and allocations: a no-op
+    when it already is (torch.cuda.device's switch costs microseconds per call, which small
+    sorts notice)."""
+    idx = device.index
+    if idx is None or idx == torch._C._cuda_getDevice():
+        return _SAME_DEVICE
+    return torch.cuda.device(idx)
+
+
 def _stream_ptr(device) -> ctypes.c_void_p:
-    return ctypes.c_void_p(torch.cuda.current_stream(device).cuda_stream)
+    """The current torch stream of ``device`` as a raw cudaStream_t."""
+    idx = device.index if device.index is not None else torch._C._cuda_getDevice()
+    return ctypes.c_void_p(torch._C._cuda_getCurrentRawStream(idx))
 
 
 def _check_tensor(t: torch.Tensor):
@@ -83,7 +105,7 @@ def sort_(t: torch.Tensor, descending: bool = False) -> torch.Tensor:
         return t
     wsb = int(lib.bsort_workspace_bytes(code, n))
     ws = _workspace(wsb, t.device)
-    with torch.cuda.device(t.device):  # launches and allocations on the tensor's GPU
+    with _on(t.device):  # launches and allocations on the tensor's GPU
         check(lib.bsort_sort_ws(code, ctypes.c_void_p(t.data_ptr()), n, int(bool(descending)),
                                 ctypes.c_void_p(ws.data_ptr()), wsb, _stream_ptr(t.device)),
               "bsort_sort_ws")
@@ -109,7 +131,7 @@ def sort_inplace_(t: torch.Tensor, descending: bool = False, chunk: int = 0) -> 
         return t
     wsb = int(lib.bsort_inplace_workspace_bytes(code, n, chunk))
     ws = _workspace(wsb, t.device)
-    with torch.cuda.device(t.device):  # launches and allocations on the tensor's GPU
+    with _on(t.device):  # launches and allocations on the tensor's GPU
         check(lib.bsort_sort_inplace_ws(code, ctypes.c_void_p(t.data_ptr()), n, int(bool(descending)), chunk,
                                         ctypes.c_void_p(ws.data_ptr()), wsb, _stream_ptr(t.device)),
               "bsort_sort_inplace_ws")
@@ -129,7 +151,7 @@ def sort_pairs_(keys: torch.Tensor, values: torch.Tensor, descending: bool = Fal
         return keys, values
     wsb = int(lib.bsort_pairs_workspace_bytes(code, n))
     ws = _workspace(wsb, keys.device)
-    with torch.cuda.device(keys.device):  # launches and allocations on the tensor's GPU
+    with _on(keys.device):  # launches and allocations on the tensor's GPU
         check(lib.bsort_sort_pairs_ws(code, ctypes.c_void_p(keys.data_ptr()), ctypes.c_void_p(values.data_ptr()),
                                       n, int(bool(descending)), ctypes.c_void_p(ws.data_ptr()), wsb,
                                       _stream_ptr(keys.device)), "bsort_sort_pairs_ws")
@@ -158,7 +180,7 @@ class Sorter:
         _check_tensor(t)
         if t.dtype != self.dtype or t.numel() > self.n:
             raise ValueError("Sorter: dtype mismatch or tensor larger than the workspace")
-        with torch.cuda.device(t.device):  # launches and allocations on the tensor's GPU
+        with _on(t.device):  # launches and allocations on the tensor's GPU
             check(lib.bsort_sort_ws(self.code, ctypes.c_void_p(t.data_ptr()), t.numel(),
                                     int(bool(descending)), ctypes.c_void_p(self.ws.data_ptr()),
                                     self.ws_bytes, _stream_ptr(t.device)), "bsort_sort_ws")
@@ -182,7 +204,7 @@ class Sorter:
         _check_tensor(dev_buf)
         if dev_buf.numel() < host.numel() or host.numel() > self.n:
             raise ValueError("sort_host: device buffer / workspace too small")
-        with torch.cuda.device(dev_buf.device):  # launches and allocations on the tensor's GPU
+        with _on(dev_buf.device):  # launches and allocations on the tensor's GPU
             check(lib.bsort_sort_host(self.code, ctypes.c_void_p(host.data_ptr()), host.numel(),
                                       int(bool(descending)), ctypes.c_void_p(dev_buf.data_ptr()),
                                       ctypes.c_void_p(self.ws.data_ptr()), self.ws_bytes,
@@ -205,7 +227,7 @@ def top_hist(t: torch.Tensor, descending: bool = False) -> torch.Tensor:
     """uint64[65536] device histogram of the top 16 bits of the transformed keys."""
     _check_tensor(t)
     h = torch.empty(_lib.DIST_BINS, dtype=torch.uint64, device=t.device)
-    with torch.cuda.device(t.device):  # launches and allocations on the tensor's GPU
+    with _on(t.device):  # launches and allocations on the tensor's GPU
         check(lib.bsort_dist_top_hist(dtype_code(t.dtype), ctypes.c_void_p(t.data_ptr()), t.numel(),
                                       int(bool(descending)), ctypes.c_void_p(h.data_ptr()),
                                       _stream_ptr(t.device)), "bsort_dist_top_hist")
@@ -250,7 +272,7 @@ def partition(t: torch.Tensor, cuts: np.ndarray, counts: np.ndarray,
     out = torch.empty_like(t)
     wsb = int(lib.bsort_dist_partition_workspace_bytes(code, t.numel(), nranks))
     ws = _workspace(wsb, t.device)
-    with torch.cuda.device(t.device):  # launches and allocations on the tensor's GPU
+    with _on(t.device):  # launches and allocations on the tensor's GPU
         check(lib.bsort_dist_partition(code, ctypes.c_void_p(t.data_ptr()), t.numel(),
                                        int(bool(descending)), _u32p(c), _u64p(sc), nranks,
                                        ctypes.c_void_p(out.data_ptr()), ctypes.c_void_p(ws.data_ptr()),
@@ -271,7 +293,7 @@ def partition_remote(t: torch.Tensor, cuts: np.ndarray, counts: np.ndarray, dst_
     nranks = c.size - 1
     wsb = int(lib.bsort_dist_partition_workspace_bytes(code, t.numel(), nranks))
     ws = _workspace(wsb, t.device)
-    with torch.cuda.device(t.device):  # launches and allocations on the tensor's GPU
+    with _on(t.device):  # launches and allocations on the tensor's GPU
         check(lib.bsort_dist_partition_remote(code, ctypes.c_void_p(t.data_ptr()), t.numel(),
                                               int(bool(descending)), _u32p(c), _u64p(sc), nranks,
                                               _u64p(da), ctypes.c_void_p(ws.data_ptr()), wsb,
@@ -284,7 +306,7 @@ def refine_hist(t: torch.Tensor, prefixes, prefix_bits: int, descending: bool = 
     _check_tensor(t)
     pre = np.ascontiguousarray(np.asarray(prefixes, dtype=np.uint64))
     h = torch.empty(pre.size * _lib.DIST_BINS, dtype=torch.uint64, device=t.device)
-    with torch.cuda.device(t.device):  # launches and allocations on the tensor's GPU
+    with _on(t.device):  # launches and allocations on the tensor's GPU
         check(lib.bsort_dist_refine_hist(dtype_code(t.dtype), ctypes.c_void_p(t.data_ptr()), t.numel(),
                                          int(bool(descending)), _u64p(pre), pre.size, int(prefix_bits),
                                          ctypes.c_void_p(h.data_ptr()), _stream_ptr(t.device)), "bsort_dist_refine_hist")
@@ -296,7 +318,7 @@ def class_hist(t: torch.Tensor, values, descending: bool = False) -> torch.Tenso
     _check_tensor(t)
     v = np.ascontiguousarray(np.asarray(values, dtype=np.uint64))
     c = torch.empty(2 * v.size + 1, dtype=torch.uint64, device=t.device)
-    with torch.cuda.device(t.device):  # launches and allocations on the tensor's GPU
+    with _on(t.device):  # launches and allocations on the tensor's GPU
         check(lib.bsort_dist_class_hist(dtype_code(t.dtype), ctypes.c_void_p(t.data_ptr()), t.numel(),
                                         int(bool(descending)), _u64p(v), v.size, ctypes.c_void_p(c.data_ptr()),
                                         _stream_ptr(t.device)), "bsort_dist_class_hist")
@@ -313,7 +335,7 @@ def partition_classes(t: torch.Tensor, values, class_counts, descending: bool = 
         return out
     wsb = int(lib.bsort_dist_class_partition_workspace_bytes())
     ws = _workspace(wsb, t.device)
-    with torch.cuda.device(t.device):  # launches and allocations on the tensor's GPU
+    with _on(t.device):  # launches and allocations on the tensor's GPU
         check(lib.bsort_dist_partition_classes(dtype_code(t.dtype), ctypes.c_void_p(t.data_ptr()), t.numel(),
                                                int(bool(descending)), _u64p(v), v.size, _u64p(cc),
                                                ctypes.c_void_p(out.data_ptr()), ctypes.c_void_p(ws.data_ptr()), wsb,
@@ -377,7 +399,7 @@ def sort_dist_native(t: torch.Tensor, comm: Comm, descending: bool = False,
     for attempt in range(2):
         out = torch.empty(cap, dtype=t.dtype, device=t.device)
         n_out = ctypes.c_uint64(0)
-        with torch.cuda.device(t.device):  # launches and allocations on the tensor's GPU
+        with _on(t.device):  # launches and allocations on the tensor's GPU
             st = lib.bsort_sort_dist_ex(dtype_code(t.dtype), ctypes.c_void_p(t.data_ptr()), n,
                                         ctypes.c_void_p(out.data_ptr()), cap, ctypes.byref(n_out),
                                         int(bool(descending)), _lib.DIST_EXACT if exact else 0, comm._h,

@@ -37,7 +37,7 @@ EXPORTS = [
     "bsort_sort_dist", "bsort_sort_dist_ex", "bsort_last_nccl_error",
     "bsort_dist_exact_boundaries", "bsort_dist_exact_send_counts",
     "bsort_status_string", "bsort_last_cuda_error", "bsort_version", "bsort_launch_count",
-    "bsort_profile_enable", "bsort_profile_read", "bsort_profile_kind_name",
+    "bsort_selftest", "bsort_profile_enable", "bsort_profile_read", "bsort_profile_kind_name",
 ]
 
 
@@ -103,6 +103,7 @@ def _load():
         "bsort_last_cuda_error": (i32, []),
         "bsort_version": (ctypes.c_char_p, []),
         "bsort_launch_count": (u64, []),
+        "bsort_selftest": (i32, []),
         "bsort_profile_enable": (None, [i32]),
         "bsort_profile_read": (i32, [ctypes.POINTER(ctypes.c_double), u64p]),
         "bsort_profile_kind_name": (ctypes.c_char_p, [i32]),

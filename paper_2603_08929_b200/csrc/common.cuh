@@ -109,6 +109,9 @@ struct DeviceInt {
 void prof_end(int kind, cudaStream_t s);
 void count_launch();
 int num_sms();
+// selftest.cu: shared atomicAdd hands out old values in lane order on this device (checked
+// once per device on first use; false while `s` is being captured before the check has run)
+bool atomics_lane_ordered(cudaStream_t s);
 void set_last_cuda_error(cudaError_t e);
 
 // Launch helper: profile-bracket, launch, count (kernels only, not memsets), check.

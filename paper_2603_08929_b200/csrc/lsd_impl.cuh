@@ -13,6 +13,7 @@
 #include "onesweep.cuh"
 #include "onesweep_ws.cuh"
 #include "pass2.cuh"
+#include "small.cuh"
 #include "paths.cuh"
 
 namespace bsort {
@@ -57,6 +58,7 @@ template <typename U> constexpr int hist_lanes() { return sizeof(U) == 4 ? 32 : 
 
 struct LsdLayout {
   size_t scratch, vscratch, ghist, bases, gcount, joint, seg, plan, counters, lookback, total;
+  size_t lb_bytes;    // one look-back region
   uint64_t lb_tiles;  // look-back descriptor rows: tiles of the smallest look-back tile in use
 };
 
@@ -72,6 +74,9 @@ constexpr uint64_t lookback_tile() {
 // this size the digit-0 buckets are shorter than a tile anyway and the joint histogram's fixed
 // cost (65536 bins) is not worth it.
 constexpr uint64_t JOINT_MIN_N = 1ull << 24;
+
+// Smallest n for the warp-specialised / round-2 look-back passes (lsd_run).
+constexpr uint64_t WS_MIN_N = 1ull << 22;
 
 template <typename U>
 LsdLayout lsd_layout(uint64_t n, bool kv = false) {
@@ -91,7 +96,10 @@ LsdLayout lsd_layout(uint64_t n, bool kv = false) {
   l.seg = off;      off = align_up(off + jbytes, 256);
   l.plan = off;     off = align_up(off + sizeof(PassPlan), 256);
   l.counters = off; off = align_up(off + 16 * 4, 256);
-  l.lookback = off; off = align_up(off + tiles * 256 * desc, 256);
+  // below WS_MIN_N two look-back regions alternate by pass parity (each pass kernel zeroes the
+  // next pass's region: no memset launches, lsd_run)
+  l.lb_bytes = align_up(tiles * 256 * desc, 256);
+  l.lookback = off; off += (n < WS_MIN_N ? 2 : 1) * l.lb_bytes;
   l.lb_tiles = tiles;
   l.total = off;
   return l;
@@ -100,7 +108,7 @@ LsdLayout lsd_layout(uint64_t n, bool kv = false) {
 template <typename U, bool BULK, int RANK, bool KV, typename DescT, typename DigitF>
 bsort_status_t launch_pass_t(const U* a, U* b, uint64_t n, DigitF digit, const unsigned long long* bases,
                              DescT* lookback, unsigned long long* gcount, uint32_t* counter, const PassPlan* plan,
-                             int pass, KvPtrs kvp, cudaStream_t s) {
+                             int pass, KvPtrs kvp, cudaStream_t s, ZeroSpan zs = {}) {
   using C = PassCfg<U, RANK, KV>;
   using L = PassSmem<C::THREADS, C::ITEMS, U, RANK, KV>;
   auto kern = k_onesweep_pass<U, C::THREADS, C::ITEMS, C::MINB, BULK, DescT, DigitF, RANK, C::LBG, KV>;
@@ -117,7 +125,7 @@ bsort_status_t launch_pass_t(const U* a, U* b, uint64_t n, DigitF digit, const u
   const uint64_t grid = min64(tiles, (uint64_t)num_sms() * occ);
   BSORT_LAUNCH(PROF_PASS, s,
                kern<<<(unsigned)grid, C::THREADS, L::bytes, s>>>(a, b, n, digit, bases, lookback, gcount, counter,
-                                                                 (uint32_t)tiles, plan, pass, kvp));
+                                                                 (uint32_t)tiles, plan, pass, kvp, zs));
   return BSORT_SUCCESS;
 }
 
@@ -126,14 +134,14 @@ bsort_status_t launch_pass_t(const U* a, U* b, uint64_t n, DigitF digit, const u
 template <typename U, int RANK, typename DescT, bool KV = false, typename DigitF>
 bsort_status_t launch_pass(const U* a, U* b, uint64_t n, DigitF digit, const unsigned long long* bases,
                            DescT* lookback, unsigned long long* gcount, uint32_t* counter, const PassPlan* plan,
-                           int pass, cudaStream_t s, KvPtrs kvp = {}) {
+                           int pass, cudaStream_t s, KvPtrs kvp = {}, ZeroSpan zs = {}) {
   bool aligned = ((uintptr_t)a % 16 == 0) && (plan == nullptr || (uintptr_t)b % 16 == 0);
   if (KV) aligned = aligned && (uintptr_t)kvp.va % 16 == 0 && (uintptr_t)kvp.vb % 16 == 0;
   if (aligned)
     return launch_pass_t<U, true, RANK, KV, DescT>(a, b, n, digit, bases, lookback, gcount, counter, plan, pass, kvp,
-                                                   s);
+                                                   s, zs);
   return launch_pass_t<U, false, RANK, KV, DescT>(a, b, n, digit, bases, lookback, gcount, counter, plan, pass, kvp,
-                                                  s);
+                                                  s, zs);
 }
 
 // Warp-specialised look-back pass (onesweep_ws.cuh) for keys without payload: rankers never wait
@@ -147,7 +155,6 @@ bsort_status_t launch_pass(const U* a, U* b, uint64_t n, DigitF digit, const uns
 
 // Below this size a pass has too few tiles to keep the walk off the critical path anyway, and
 // the two-CTA kernel's smaller tiles spread a small input over more SMs (cfg1: 2^20 keys).
-constexpr uint64_t WS_MIN_N = 1ull << 22;
 inline bool ws_enabled() {
   static const bool on = [] {
     const char* e = getenv("BSORT_WS");
@@ -220,7 +227,11 @@ bsort_status_t launch_pass2(const U* a, U* b, uint64_t n, const unsigned long lo
   using C = std::conditional_t<HALVES == 2, P2SkewCfg, P2Cfg<MODE>>;
   using L = Pass2Smem<C::RT, C::WT, C::ITEMS, U, MODE, HALVES>;
   auto kern = k_pass2<U, KIND, DESC, SHIFT, C::RT, C::WT, C::ITEMS, MODE, false, 2, HALVES>;
-  BSORT_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L::bytes));
+  static DeviceOnce attr;  // per instantiation and device
+  if (attr.pending()) {
+    BSORT_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L::bytes));
+    attr.mark();
+  }
   const uint64_t tiles = (n + L::TILE - 1) / L::TILE;
   const uint64_t grid = min64(tiles, (uint64_t)num_sms());  // one CTA per SM, all resident
   BSORT_LAUNCH(PROF_PASS, s,
@@ -253,6 +264,11 @@ bsort_status_t lsd_run(U* keys, uint32_t* vals, uint64_t n, unsigned char* ws, c
   auto* counters = reinterpret_cast<uint32_t*>(ws + l.counters);
   auto* lookback = reinterpret_cast<DescT*>(ws + l.lookback);
 
+  // small n: the whole sort in one single-CTA launch (small.cuh)
+  if constexpr (!KV)
+    if (n <= small_max_n<U>())
+      return launch_small<KIND, DESC, U>(keys, n, s);
+
   static const bool joint_off = getenv("BSORT_NO_JOINT") != nullptr;  // A/B and debugging
   const bool use_joint = n >= JOINT_MIN_N && !joint_off;
   // digit histograms and, right after them, the presorted-input flags (k_onesweep_hist*)
@@ -270,18 +286,20 @@ bsort_status_t lsd_run(U* keys, uint32_t* vals, uint64_t n, unsigned char* ws, c
     BSORT_LAUNCH(PROF_MEMSET, s, cudaMemsetAsync(joint, 0, 65536 * 8, s));
     BSORT_LAUNCH(PROF_HIST, s, hk<<<num_sms(), HIST_THREADS, hsmem, s>>>(keys, n, ghist, joint, order));
   } else {
-    auto hk = k_onesweep_hist<KIND, DESC, U, LANES>;
+    // the histogram kernel's last CTA also plans (no k_plan launch)
+    auto hk = k_onesweep_hist<KIND, DESC, U, LANES, true>;
     constexpr int hsmem = P * 256 * LANES * 4;
     static DeviceOnce hattr;
     if (hattr.pending()) {
       BSORT_CUDA(cudaFuncSetAttribute(hk, cudaFuncAttributeMaxDynamicSharedMemorySize, hsmem));
       hattr.mark();
     }
-    BSORT_LAUNCH(PROF_HIST, s, hk<<<num_sms(), HIST_THREADS, hsmem, s>>>(keys, n, ghist, order));
+    BSORT_LAUNCH(PROF_HIST, s,
+                 hk<<<num_sms(), HIST_THREADS, hsmem, s>>>(keys, n, ghist, order,
+                                                           PlanArgs{bases, plan, counters, gcount}));
   }
-  BSORT_LAUNCH(PROF_SCAN, s,
-               k_plan<<<1, 256, 0, s>>>(ghist, n, P, bases, plan, counters, gcount, use_joint ? joint : nullptr,
-                                        order));
+  if (use_joint)
+    BSORT_LAUNCH(PROF_SCAN, s, k_plan<<<1, 256, 0, s>>>(ghist, n, P, bases, plan, counters, gcount, joint, order));
   if (use_joint)
     BSORT_LAUNCH(PROF_SCAN, s,
                  k_plan_joint<<<1, 256, 0, s>>>(joint, ghist, bases + 256, J01_TILE, plan, seg,
@@ -289,11 +307,21 @@ bsort_status_t lsd_run(U* keys, uint32_t* vals, uint64_t n, unsigned char* ws, c
                                                     ? p2_tile<R2_RUN2>()
                                                     : 0));
   bsort_status_t st = BSORT_SUCCESS;
+  const bool fold = n < WS_MIN_N;  // look-back zeroing folded into the pass kernels
   auto one_pass = [&](auto shift_c) {
     constexpr int SH = decltype(shift_c)::value;
     constexpr int p = SH / 8;
     if (p >= P || st != BSORT_SUCCESS) return;
-    if constexpr (p > 0) {
+    // below WS_MIN_N only k_onesweep_pass runs: it zeroes the other look-back region for the
+    // next pass (fold), else one memset per look-back pass
+    DescT* lb = lookback;
+    ZeroSpan zs{};
+    if (fold) {
+      lb = reinterpret_cast<DescT*>(reinterpret_cast<unsigned char*>(lookback) + (p & 1) * l.lb_bytes);
+      if (p + 1 < P)
+        zs = ZeroSpan{reinterpret_cast<uint4*>(reinterpret_cast<unsigned char*>(lookback) + ((p + 1) & 1) * l.lb_bytes),
+                      (uint32_t)(l.lb_bytes / 16)};
+    } else if constexpr (p > 0) {
       st = memset_async(lookback, l.lb_tiles * 256 * sizeof(DescT), s);
       if (st != BSORT_SUCCESS) return;
     }
@@ -313,11 +341,12 @@ bsort_status_t lsd_run(U* keys, uint32_t* vals, uint64_t n, unsigned char* ws, c
       }
       if (!done)
         st = launch_pass<U, RANK_UNSTABLE, DescT, KV>(keys, scratch, n, RadixDigit<KIND, DESC, U, SH>{}, bases,
-                                                      lookback, gcount, counters, plan, p, s, kvp);
+                                                      lookback, gcount, counters, plan, p, s, kvp, zs);
     } else {
       bool done = false;
       if constexpr (sizeof(U) == 4 && !KV) {
-        if (n >= WS_MIN_N && n <= P2_MAX_N && p2_enabled() && (uintptr_t)keys % sizeof(U) == 0) {
+        if (n >= WS_MIN_N && n <= P2_MAX_N && p2_enabled() && (uintptr_t)keys % sizeof(U) == 0 &&
+            atomics_lane_ordered(s)) {
           // (half-warp counter rows for skewed top digits, k_pass2<..., HALVES = 2> with
           // P2_SKEWVAR, measured no faster on cfg3's sign+exponent digit: 3.98 vs 3.92 ms)
           st = launch_pass2<KIND, DESC, SH>(keys, scratch, n, bases + p * 256,
@@ -339,8 +368,8 @@ bsort_status_t lsd_run(U* keys, uint32_t* vals, uint64_t n, unsigned char* ws, c
       }
       if (!done)
         st = launch_pass<U, RANK_RUN2, DescT, KV>(keys, scratch, n, RadixDigit<KIND, DESC, U, SH>{},
-                                                  bases + p * 256, lookback, gcount + p * 256, counters + p,
-                                                  plan, p, s, kvp);
+                                                  bases + p * 256, lb, gcount + p * 256, counters + p,
+                                                  plan, p, s, kvp, zs);
     }
     // pass 1 without look-back when the joint plan allows it (each launch checks plan->j01
     // and exactly one of the two does the work)

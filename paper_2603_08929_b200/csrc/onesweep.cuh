@@ -219,10 +219,26 @@ struct RankDigit {
 // warp never conflict; one CTA of 1024 threads per SM, grid-stride, 128-bit loads.
 constexpr int HIST_THREADS = 1024;
 
-template <int KIND, bool DESC, typename U, int LANES>
+// Forward declaration: the fused-plan epilogue below.
+template <int NT>
+__device__ __forceinline__ void plan_body(const unsigned long long* ghist, uint64_t n, int P,
+                                          unsigned long long* __restrict__ bases, PassPlan* __restrict__ plan,
+                                          uint32_t* __restrict__ tile_counters,
+                                          unsigned long long* __restrict__ gcount, const uint32_t* order);
+
+// What the fused-plan histogram kernel needs for k_plan's work (FUSE_PLAN; order[2] is the
+// arrival ticket, zeroed with the histograms).
+struct PlanArgs {
+  unsigned long long* bases;
+  PassPlan* plan;
+  uint32_t* tile_counters;
+  unsigned long long* gcount;
+};
+
+template <int KIND, bool DESC, typename U, int LANES, bool FUSE_PLAN = false>
 __global__ void __launch_bounds__(HIST_THREADS, 1)
     k_onesweep_hist(const U* __restrict__ keys, uint64_t n, unsigned long long* __restrict__ ghist,
-                    uint32_t* __restrict__ order = nullptr) {
+                    uint32_t* __restrict__ order = nullptr, PlanArgs pa = {}) {
   constexpr int P = sizeof(U);
   OrderFlags of;
   // pair (j, j+1) for a scalar key j
@@ -279,6 +295,19 @@ __global__ void __launch_bounds__(HIST_THREADS, 1)
 #pragma unroll 8
     for (int l = 0; l < LANES; ++l) s += hs[b * LANES + ((l + b) & (LANES - 1))];
     if (s) atomicAdd(&ghist[b], (unsigned long long)s);
+  }
+  if constexpr (FUSE_PLAN) {
+    // the last CTA to finish plans (k_plan's work without its launch): small sorts are bound by
+    // launch count (DESIGN.md §6 small n)
+    __shared__ int last;
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0) last = atomicAdd(&order[2], 1u) == gridDim.x - 1;
+    __syncthreads();
+    if (last) {
+      __threadfence();
+      plan_body<HIST_THREADS>(ghist, n, P, pa.bases, pa.plan, pa.tile_counters, pa.gcount, order);
+    }
   }
 }
 
@@ -449,41 +478,30 @@ static __global__ void __launch_bounds__(256)
 }
 
 // Plan: exclusive scan of every digit histogram into global digit bases, trivial-digit
-// detection, ping-pong buffer assignment, tile-counter reset.  One CTA of 256 threads.
-static __global__ void __launch_bounds__(256)
-    k_plan(unsigned long long* __restrict__ ghist, uint64_t n, int P, unsigned long long* __restrict__ bases,
-           PassPlan* __restrict__ plan, uint32_t* __restrict__ tile_counters,
-           unsigned long long* __restrict__ gcount, const unsigned long long* __restrict__ gjoint,
-           const uint32_t* __restrict__ order = nullptr) {
-  __shared__ unsigned long long wt[256 / 32 + 1];
+// detection, ping-pong buffer assignment, tile-counter reset.  Run by a block of NT >= 256
+// threads (thread d < 256 owns digit d; every thread takes part in the block barriers): k_plan
+// below, or the last CTA of the fused histogram kernel (k_onesweep_hist<..., FUSE_PLAN>).
+template <int NT>
+__device__ __forceinline__ void plan_body(const unsigned long long* ghist, uint64_t n, int P,
+                                          unsigned long long* __restrict__ bases, PassPlan* __restrict__ plan,
+                                          uint32_t* __restrict__ tile_counters,
+                                          unsigned long long* __restrict__ gcount, const uint32_t* order) {
+  __shared__ unsigned long long wt[NT / 32 + 1];
   __shared__ uint32_t skip_s[8], skew_s[8];
-  if (gjoint != nullptr) {  // marginals of digits 1 (row sums) and 0 (column sums) of J[d1][d0]
-    unsigned long long r = 0, c = 0;
-    const ulonglong2* row = reinterpret_cast<const ulonglong2*>(gjoint + threadIdx.x * 256);
-#pragma unroll 8
-    for (int a = 0; a < 128; ++a) {
-      const ulonglong2 q = row[a];
-      r += q.x + q.y;
-    }
-#pragma unroll 8
-    for (int b = 0; b < 256; ++b) c += gjoint[b * 256 + threadIdx.x];
-    ghist[threadIdx.x] = c;
-    ghist[256 + threadIdx.x] = r;
-    __syncthreads();
-  }
+  const uint32_t t = threadIdx.x;
   for (int p = 0; p < P; ++p) {
-    const unsigned long long c = ghist[p * 256 + threadIdx.x];
-    const unsigned long long ex = block_exclusive_scan<256>(c, wt, (unsigned long long*)nullptr);
-    bases[p * 256 + threadIdx.x] = ex;
-    const int trivial = __syncthreads_or(c == n);
-    const int skewed = __syncthreads_or(c * 8 > n);
-    if (threadIdx.x == 0) {
+    const unsigned long long c = t < 256 ? __ldcg(&ghist[p * 256 + t]) : 0ull;
+    const unsigned long long ex = block_exclusive_scan<NT>(c, wt, (unsigned long long*)nullptr);
+    if (t < 256) bases[p * 256 + t] = ex;
+    const int trivial = __syncthreads_or(t < 256 && c == n);
+    const int skewed = __syncthreads_or(t < 256 && c * 8 > n);
+    if (t == 0) {
       skip_s[p] = trivial;
       skew_s[p] = skewed;
     }
   }
   __syncthreads();
-  if (threadIdx.x == 0) {
+  if (t == 0) {
     uint32_t alt = 0, executed = 0, first = 8, last = 8;
     for (int p = 0; p < 8; ++p) {
       const uint32_t sk = (p < P) ? skip_s[p] : 1u;
@@ -506,8 +524,8 @@ static __global__ void __launch_bounds__(256)
     plan->j01 = 0;  // k_plan_joint (if launched) may enable the look-back-free pass 1
     plan->run2 = 0;  // ... and pass 2 ranked by runs (pass2.cuh R2_RUN2)
     plan->reverse = 0;
-    const bool in_order = order != nullptr && order[0] == 0;
-    const bool reversed = order != nullptr && !in_order && order[1] == 0;
+    const bool in_order = order != nullptr && __ldcg(&order[0]) == 0;
+    const bool reversed = order != nullptr && !in_order && __ldcg(&order[1]) == 0;
     if (in_order || reversed) {  // presorted input: no pass; reversed input is reversed in place
       for (int p = 0; p < 8; ++p) {
         plan->skip[p] = 1;
@@ -519,9 +537,31 @@ static __global__ void __launch_bounds__(256)
       plan->reverse = reversed;
     }
   }
-  if (threadIdx.x < 16) tile_counters[threadIdx.x] = 0;  // 8 passes + the J01 pass
-  if (gcount != nullptr)
-    for (int p = 0; p < P; ++p) gcount[p * 256 + threadIdx.x] = 0;  // unstable-pass digit counters
+  if (t < 16) tile_counters[t] = 0;  // 8 passes + the J01 pass
+  if (gcount != nullptr && t < 256)
+    for (int p = 0; p < P; ++p) gcount[p * 256 + t] = 0;  // unstable-pass digit counters
+}
+
+static __global__ void __launch_bounds__(256)
+    k_plan(unsigned long long* __restrict__ ghist, uint64_t n, int P, unsigned long long* __restrict__ bases,
+           PassPlan* __restrict__ plan, uint32_t* __restrict__ tile_counters,
+           unsigned long long* __restrict__ gcount, const unsigned long long* __restrict__ gjoint,
+           const uint32_t* __restrict__ order = nullptr) {
+  if (gjoint != nullptr) {  // marginals of digits 1 (row sums) and 0 (column sums) of J[d1][d0]
+    unsigned long long r = 0, c = 0;
+    const ulonglong2* row = reinterpret_cast<const ulonglong2*>(gjoint + threadIdx.x * 256);
+#pragma unroll 8
+    for (int a = 0; a < 128; ++a) {
+      const ulonglong2 q = row[a];
+      r += q.x + q.y;
+    }
+#pragma unroll 8
+    for (int b = 0; b < 256; ++b) c += gjoint[b * 256 + threadIdx.x];
+    ghist[threadIdx.x] = c;
+    ghist[256 + threadIdx.x] = r;
+    __syncthreads();
+  }
+  plan_body<256>(ghist, n, P, bases, plan, tile_counters, gcount, order);
 }
 
 // ---------------------------------------------------------------------------------------
@@ -594,6 +634,13 @@ struct KvPtrs {
   uint32_t* vb;
 };
 
+// A region the pass kernel zeroes (grid-stride, 16-byte stores) before anything else: the next
+// pass's look-back descriptors, so small sorts need no memset launch per pass (lsd_impl.cuh).
+struct ZeroSpan {
+  uint4* p;
+  uint32_t n16;
+};
+
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return (uint32_t)__cvta_generic_to_shared(p);
 }
@@ -637,7 +684,8 @@ __global__ void __launch_bounds__(THREADS, MINB)
     k_onesweep_pass(const U* a_ptr, U* b_ptr, uint64_t n, DigitF digit,
                     const unsigned long long* __restrict__ bases, DescT* __restrict__ lookback,
                     unsigned long long* __restrict__ gcount, uint32_t* __restrict__ tile_counter,
-                    uint32_t num_tiles, const PassPlan* __restrict__ plan, int pass, KvPtrs kvp = {}) {
+                    uint32_t num_tiles, const PassPlan* __restrict__ plan, int pass, KvPtrs kvp = {},
+                    ZeroSpan zs = {}) {
   using L = PassSmem<THREADS, ITEMS, U, MODE, KV>;
   using LB = LookbackBits<DescT>;
   constexpr int TILE = L::TILE;
@@ -663,6 +711,8 @@ __global__ void __launch_bounds__(THREADS, MINB)
   const uint32_t* vsrc = kvp.va;
   uint32_t* vdst = kvp.vb;
   (void)vbufs;
+  for (uint32_t i = blockIdx.x * THREADS + threadIdx.x; i < zs.n16; i += gridDim.x * THREADS)
+    zs.p[i] = make_uint4(0u, 0u, 0u, 0u);
   if (plan != nullptr) {
     if (plan->skip[pass]) return;
     if constexpr (MODE == RANK_J01) {
@@ -1019,6 +1069,32 @@ __global__ void __launch_bounds__(256) k_copy_back(U* __restrict__ a, const U* _
                                                    const PassPlan* __restrict__ plan) {
   const uint64_t T = (uint64_t)gridDim.x * blockDim.x;
   if (plan->reverse) {  // input was in the opposite order (no pass ran): reverse in place
+    constexpr uint32_t V = 16 / sizeof(U);
+    if ((uintptr_t)a % 16 == 0 && n % V == 0) {
+      // 16-byte vectors: vector k and its mirror nv-1-k swap with their elements reversed
+      const uint64_t nv = n / V;
+      uint4* av = reinterpret_cast<uint4*>(a);
+      auto rev = [](uint4 q) {
+        if constexpr (sizeof(U) == 4) return make_uint4(q.w, q.z, q.y, q.x);
+        else return make_uint4(q.z, q.w, q.x, q.y);
+      };
+      uint64_t k = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+      const uint64_t hv = nv / 2;
+      for (; k + T < hv; k += 2 * T) {  // two swaps in flight per thread
+        const uint4 x0 = av[k], y0 = av[nv - 1 - k], x1 = av[k + T], y1 = av[nv - 1 - k - T];
+        av[k] = rev(y0);
+        av[nv - 1 - k] = rev(x0);
+        av[k + T] = rev(y1);
+        av[nv - 1 - k - T] = rev(x1);
+      }
+      for (; k < hv; k += T) {
+        const uint4 x = av[k], y = av[nv - 1 - k];
+        av[k] = rev(y);
+        av[nv - 1 - k] = rev(x);
+      }
+      if ((nv & 1) && blockIdx.x == 0 && threadIdx.x == 0) av[hv] = rev(av[hv]);  // the middle vector
+      return;
+    }
     const uint64_t h = n / 2;
     uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
     for (; i + 3 * T < h; i += 4 * T) {  // four independent swaps in flight per thread

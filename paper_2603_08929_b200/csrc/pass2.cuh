@@ -10,8 +10,8 @@
 //    atomicAdd(&cnt[warp][digit], 4).  Items of one warp are ordered by program order, and lanes
 //    of ONE atomic instruction that hit the same word receive their old values in ascending
 //    lane order on sm_100 (measured: tools/exp/atoms_order.cu, 0 violations in >10^9 same-word
-//    lane pairs, random / skewed / divergent patterns; bsort_selftest re-checks it at run time
-//    and the library falls back to the round-1 kernels if it ever fails).  So the returned value
+//    lane pairs, random / skewed / divergent patterns; selftest.cu re-checks it once per device
+//    on first use, and where it fails the library launches the round-1 kernels instead).  So the returned value
 //    IS the stable rank inside the warp; a per-digit scan over warps gives the tile rank.  The
 //    round-1 half-warp multisplit needed three shared accesses per key.
 //  * Chunked look-back.  Pass p+1's input is sorted by digit p, so it splits into NC = 32

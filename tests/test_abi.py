@@ -162,3 +162,25 @@ def test_splitters_reject_bad_args(B):
         B.splitters(np.zeros(65536, np.uint64), 0)
     with pytest.raises(BsortError):
         B.send_counts(np.zeros(65536, np.uint64), np.array([0, 7, 3, 65536], np.uint32))
+
+
+def test_workspace_bytes_monotone_in_n(B):
+    """A workspace sized for n serves every m <= n (Sorter, the in-place mode's groups): sizes
+    never decrease with n, across the single-CTA bound, the folded look-back range (n < 2^22,
+    two look-back regions) and the 2^24 joint-histogram / 2^30 descriptor-width steps."""
+    from paper_2603_08929_b200 import _lib
+    L = _lib.lib
+    probes = sorted({m for e in range(1, 33) for m in ((1 << e) - 1, 1 << e, (1 << e) + 1)} |
+                    {12287, 12288, 12289, 6143, 6144, 6145, (1 << 22) - 8193, (1 << 22) - 1})
+    for code in (_lib.U8, _lib.I16, _lib.U32, _lib.F32, _lib.I64, _lib.F64):
+        prev = 0
+        for m in probes:
+            w = int(L.bsort_workspace_bytes(code, m))
+            assert w >= prev, (code, m, w, prev)
+            prev = w
+    for code in (_lib.U32, _lib.I64):
+        prev = 0
+        for m in probes:
+            w = int(L.bsort_pairs_workspace_bytes(code, m))
+            assert w >= prev, ("pairs", code, m, w, prev)
+            prev = w

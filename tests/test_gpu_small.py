@@ -1,0 +1,148 @@
+"""GPU parity of the small-n path (csrc/small.cuh: the whole LSD sort in shared memory by one
+CTA in one launch, keys-only sorts of n <= 12288 32-bit / 6144 64-bit keys) against the CPU
+oracle, bit for bit: sizes around warp segments and both sides of the size bound, passes
+skipped for constant digits (odd and even numbers of moving passes), both directions, the
+multi-launch path above the bound (its look-back zeroing folded into the pass kernels below
+2^22 keys) and at the same sizes (BSORT_SMALL=0, in a subprocess: the switch is read once per
+process)."""
+import os
+import subprocess
+import sys
+
+import numpy as np
+import pytest
+import torch
+
+import oracle
+import workloads as W
+
+pytestmark = pytest.mark.gpu
+
+REPO = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+NP = {torch.uint32: np.uint32, torch.int32: np.int32, torch.float32: np.float32,
+      torch.uint64: np.uint64, torch.int64: np.int64, torch.float64: np.float64}
+SIGNED = {torch.uint32: torch.int32, torch.uint64: torch.int64}
+
+
+@pytest.fixture(scope="module")
+def B():
+    if not torch.cuda.is_available():
+        pytest.skip("needs a CUDA device")
+    import paper_2603_08929_b200 as b
+    return b
+
+
+def host(t):
+    return t.view(SIGNED.get(t.dtype, t.dtype)).cpu().numpy().view(NP[t.dtype])
+
+
+def gen(dtype, n, seed):
+    if dtype.is_floating_point:
+        return W.special_mix(dtype, n, seed, "cuda")
+    return W.uniform_int(dtype, n, seed, "cuda")
+
+
+def check(B, t, desc, what):
+    ref = oracle.sort_native(host(t), descending=desc)
+    B.sort_(t, descending=desc)
+    torch.cuda.synchronize()
+    got = host(t)
+    if got.tobytes() != ref.tobytes():
+        bad = np.flatnonzero(got != ref) if got.dtype.kind != "f" else np.flatnonzero(
+            got.view(np.uint8) != ref.view(np.uint8))
+        raise AssertionError(f"{what}: {len(bad)} mismatches, first at {bad[:4]} of n={got.size}")
+
+
+def bound(dtype):
+    return 12288 if torch.empty(0, dtype=dtype).element_size() == 4 else 6144
+
+
+@pytest.mark.parametrize("dtype", [torch.int32, torch.float32, torch.uint64, torch.float64],
+                         ids=lambda d: str(d).split(".")[-1])
+@pytest.mark.parametrize("desc", [False, True], ids=["asc", "desc"])
+def test_small_sizes(B, dtype, desc):
+    big = bound(dtype)
+    for n in [2, 3, 15, 16, 17, 31, 32, 33, 511, 512, 513, 4097, big // 2 + 3, big - 1, big, big + 1,
+              3 * big + 7, 300_007, (1 << 22) - 1, (1 << 22) + 1]:
+        check(B, gen(dtype, n, 1000 + n), desc, f"n={n}")
+
+
+@pytest.mark.parametrize("dtype,keep", [(torch.uint32, 0x000000FF), (torch.uint32, 0x00FF00FF),
+                                        (torch.uint32, 0x00FFFFFF), (torch.int32, 0x7F00FF00),
+                                        (torch.uint64, 0x00FF0000FF0000FF), (torch.int64, 0x0FFFFFFFFFFFFF00)])
+@pytest.mark.parametrize("n", [5000, 1 << 20])
+def test_small_skipped_passes(B, dtype, keep, n):
+    """Constant digits: their passes are skipped; 1, 2, 3 (odd: copy-back) and 7 moving passes."""
+    x = W.uniform_int(dtype, n, 77, "cuda")
+    sd = SIGNED.get(dtype, dtype)
+    x = (x.view(sd) & torch.tensor(keep, dtype=torch.int64).to(sd).item()).view(dtype)
+    for desc in (False, True):
+        check(B, x.clone(), desc, f"keep={keep:#x} desc={desc}")
+
+
+def test_small_all_equal_and_two_values(B):
+    for n in (9, 10_000, 100_000, 1 << 22):
+        x = torch.full((n,), -7, dtype=torch.int32, device="cuda")
+        check(B, x.clone(), False, f"equal n={n}")
+        x[::3] = 12
+        check(B, x.clone(), True, f"two values n={n}")
+
+
+def test_multilaunch_path_at_small_sizes():
+    """BSORT_SMALL=0: the multi-launch one-sweep path the small kernel replaces, same sizes."""
+    code = r"""
+import sys; sys.path.insert(0, %r)
+import numpy as np, torch, oracle, workloads as W, paper_2603_08929_b200 as B
+for dt, n in ((torch.int32, 1000), (torch.int32, 1 << 20), (torch.float64, 70001), (torch.float32, 8193)):
+    x = W.special_mix(dt, n, 5, "cuda") if dt.is_floating_point else W.uniform_int(dt, n, 5, "cuda")
+    h = x.cpu().numpy()
+    for desc in (False, True):
+        ref = oracle.sort_native(h, descending=desc)
+        y = x.clone(); B.sort_(y, descending=desc); torch.cuda.synchronize()
+        assert y.cpu().numpy().tobytes() == ref.tobytes(), (dt, n, desc)
+print("ok")
+""" % REPO
+    r = subprocess.run([sys.executable, "-c", code], env=dict(os.environ, BSORT_SMALL="0"), capture_output=True,
+                       text=True, timeout=600, cwd=REPO)
+    assert r.returncode == 0 and "ok" in r.stdout, r.stderr[-2000:]
+
+
+def test_small_bound_override():
+    """BSORT_SMALL_MAX=20480 (the shared-memory limit for 32-bit keys) in a subprocess: the
+    single-CTA kernel up to its capacity."""
+    code = r"""
+import sys; sys.path.insert(0, %r)
+import numpy as np, torch, oracle, workloads as W, paper_2603_08929_b200 as B
+for dt, n in ((torch.int32, 20480), (torch.float32, 20479), (torch.uint32, 16385), (torch.float64, 10240),
+              (torch.int64, 9999)):
+    x = W.special_mix(dt, n, 9, "cuda") if dt.is_floating_point else W.uniform_int(dt, n, 9, "cuda")
+    sd = {torch.uint32: torch.int32}.get(dt, dt)
+    h = x.view(sd).cpu().numpy().view({torch.uint32: np.uint32}.get(dt, x.view(sd).cpu().numpy().dtype))
+    for desc in (False, True):
+        ref = oracle.sort_native(h, descending=desc)
+        y = x.clone(); c0 = B.launch_count(); B.sort_(y, descending=desc); torch.cuda.synchronize()
+        assert B.launch_count() - c0 == 1, "single-CTA path expected"
+        assert y.view(sd).cpu().numpy().tobytes() == ref.tobytes(), (dt, n, desc)
+print("ok")
+""" % REPO
+    r = subprocess.run([sys.executable, "-c", code], env=dict(os.environ, BSORT_SMALL_MAX="20480"),
+                       capture_output=True, text=True, timeout=600, cwd=REPO)
+    assert r.returncode == 0 and "ok" in r.stdout, r.stderr[-2000:]
+
+
+def test_small_launch_count(B):
+    """One launch per small sort (the path's point): libbsort's own launch counter."""
+    x = W.uniform_int(torch.int32, 10_000, 3, "cuda")
+    B.sort_(x)
+    torch.cuda.synchronize()
+    c0 = B.launch_count()
+    B.sort_(x)
+    torch.cuda.synchronize()
+    assert B.launch_count() - c0 == 1
+
+
+def test_selftest_lane_order(B):
+    """bsort_selftest: the shared-atomic lane order the stable rankings rely on holds here (if it
+    did not, the library would route around those kernels and this documents that it does not
+    need to on this part)."""
+    assert B.selftest() == 0

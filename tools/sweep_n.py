@@ -11,8 +11,11 @@ import paper_2603_08929_b200 as B  # noqa: E402
 import workloads as W  # noqa: E402
 
 CASES = [("cfg3", torch.float32), ("cfg1", torch.int32), ("cfg5", torch.int64), ("cfg5", torch.float64)]
+# argv: [max_lg [step]] -- e.g. `sweep_n.py 24 1` for every power of two up to 2^24
+MAX_LG = int(sys.argv[1]) if len(sys.argv) > 1 else 30
+STEP = int(sys.argv[2]) if len(sys.argv) > 2 else 2
 for cfg, dt in CASES:
-    for lg in range(16, 31, 2):
+    for lg in range(16, MAX_LG + 1, STEP):
         n = 1 << lg
         x = W.make(cfg, "cuda", n=n, dtype=dt if cfg == "cfg5" else None)
         if x.dtype != dt:
