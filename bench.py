@@ -427,6 +427,8 @@ def multi_line(world, steps, warmup, head, results, e2e, a2a_ref, launches, cloc
                      "dtype": v["dtype"], "mode": v["mode"], "a2a_ms": v.get("a2a_ms"),
                      "a2a_GBps_egress_rank0": (v["a2a_bytes"] / (v["a2a_ms"] / 1e3) / 1e9
                                                if v.get("a2a_ms") else None)}
+        if v.get("note"):
+            others[k]["note"] = v["note"]
     e2e_rec = None
     if e2e is not None:
         if "error" in e2e:
@@ -535,6 +537,27 @@ def bench_multi(args, B):
         # rank 0's egress bytes (keys to the other ranks): n_loc minus what it keeps
         res["a2a_bytes"] = _egress_bytes(B, x, comm, world, rank) if world > 1 else 0
         results[name] = res
+        if name == head[0] and not args.quick:
+            # §8 N1: the same step with the fused partition + exchange over CUDA IPC peer memory
+            runf = lambda: B.sort_dist_native(x, comm, capacity=cap, fused=True)  # noqa: E731
+            for _ in range(args.warmup):
+                del_ = runf()
+                del del_
+            torch.cuda.synchronize()
+            dist.barrier()
+            evf = []
+            for _ in range(max(1, min(args.steps, 5))):
+                a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                a.record(stream)
+                o = runf()
+                b.record(stream)
+                evf.append((a, b))
+                del o
+            torch.cuda.synchronize()
+            msf = maxr(sum(a.elapsed_time(b) for a, b in evf) / len(evf))
+            results[name + "_fused"] = dict(res, ms=msf, a2a_ms=None, pass_ms=None,
+                                            note="BSORT_DIST_FUSED: partition straight into the owners' "
+                                                 "receive buffers (CUDA IPC), device-side barriers")
         if name == head[0] and not (args.quick and not args.e2e):
             e2e = _e2e_dist(B, x, comm, cap, args, dev, stream, maxr)
         del x

@@ -255,6 +255,15 @@ bsort_status_t bsort_sort_dist(bsort_dtype_t dtype, const void* dev_in, uint64_t
  * one key read + an all-reduce of m x 65536 u64 per refinement level (bsort_dist_exact_boundaries)
  * and a class histogram + all-gather; it blocks the host once more per level. */
 #define BSORT_DIST_EXACT 1u
+/* BSORT_DIST_FUSED: no bucketed copy and no NCCL keys exchange -- the partition
+ * kernel stores every key directly into its owner's receive buffer, which the communicator owns
+ * (cudaMalloc, mapped into every rank by CUDA IPC: all ranks must be processes of one node with
+ * peer access), between two device-side barriers on signal pads in the same mapped memory
+ * (a peer that never arrives fails the call after BSORT_NCCL_TIMEOUT_S).  The owner sorts its
+ * buffer and copies the shard to dev_out.  The receive buffer grows collectively (all ranks
+ * decide from the same all-gathered counts) and lives until bsort_comm_destroy.  Not combinable
+ * with BSORT_DIST_EXACT (BSORT_ERROR_INVALID_ARGUMENT). */
+#define BSORT_DIST_FUSED 2u
 bsort_status_t bsort_sort_dist_ex(bsort_dtype_t dtype, const void* dev_in, uint64_t n_local, void* dev_out,
                                   uint64_t out_capacity, uint64_t* n_out, bsort_direction_t direction,
                                   unsigned flags, bsort_comm_t comm, void* stream);

@@ -387,12 +387,14 @@ class Comm:
 
 
 def sort_dist_native(t: torch.Tensor, comm: Comm, descending: bool = False,
-                     capacity: int = None, exact: bool = False) -> torch.Tensor:
+                     capacity: int = None, exact: bool = False, fused: bool = False) -> torch.Tensor:
     """§8 b ``bsort_sort_dist``: the whole MSD path in one libbsort call over ``comm`` (NCCL).
     Returns this rank's shard (sorted); ``t`` is left intact.  Collective over comm's ranks.
     If some rank's shard exceeds ``capacity`` (default 2 x n_local + 65,536) every rank gets
     BSORT_ERROR_CAPACITY and the call is retried once, collectively, with the exact sizes.
-    ``exact``: exact splitting (§8 N2) inside libbsort (bsort_sort_dist_ex, BSORT_DIST_EXACT)."""
+    ``exact``: exact splitting (§8 N2) inside libbsort (bsort_sort_dist_ex, BSORT_DIST_EXACT).
+    ``fused``: the partition stores keys straight into the owners' receive buffers over CUDA IPC
+    peer mappings (§8 N1, BSORT_DIST_FUSED; ranks on one node); not with ``exact``."""
     _check_tensor(t)
     n = t.numel()
     cap = capacity if capacity is not None else 2 * n + (1 << 16)
@@ -402,7 +404,8 @@ def sort_dist_native(t: torch.Tensor, comm: Comm, descending: bool = False,
         with _on(t.device):  # launches and allocations on the tensor's GPU
             st = lib.bsort_sort_dist_ex(dtype_code(t.dtype), ctypes.c_void_p(t.data_ptr()), n,
                                         ctypes.c_void_p(out.data_ptr()), cap, ctypes.byref(n_out),
-                                        int(bool(descending)), _lib.DIST_EXACT if exact else 0, comm._h,
+                                        int(bool(descending)),
+                                        (_lib.DIST_EXACT if exact else 0) | (_lib.DIST_FUSED if fused else 0), comm._h,
                                         _stream_ptr(t.device))
         if st == _lib.ERROR_CAPACITY and attempt == 0:
             cap = int(n_out.value)

@@ -45,6 +45,7 @@ EXPORTS = [
 REFINE_FN = ctypes.CFUNCTYPE(ctypes.c_int, ctypes.c_void_p, ctypes.POINTER(ctypes.c_uint64), ctypes.c_int,
                              ctypes.c_int, ctypes.POINTER(ctypes.c_uint64))
 DIST_EXACT = 1
+DIST_FUSED = 2
 
 
 class BsortError(RuntimeError):

@@ -351,8 +351,9 @@ bool increasing(const uint64_t* v, int m) {
 }
 }  // namespace
 
-// Host planning of exact splitting (pure host; the same logic as dist.exact_boundaries /
-// exact_send_counts in the Python orchestration, which tests pin against brute force).
+// Host planning of exact splitting (pure host; the Python orchestration calls these through
+// ctypes; tests pin them against brute force and against an independent numpy restatement in
+// tests/_exact_ref.py).
 bsort_status_t bsort_dist_exact_boundaries(const uint64_t* hg, int nranks, int key_bits, bsort_refine_fn refine,
                                            void* ctx, uint64_t* values, int* m_out, int* idx, uint64_t* quota,
                                            int* levels_out) {

@@ -12,9 +12,12 @@
 //
 // NCCL is bound at run time (dlopen "libnccl.so.2"): libbsort.so has no link-time NCCL
 // dependency, and inside a PyTorch process the already-loaded libnccl (same soname) is reused.
-// Two host syncs: after the histogram all-reduce (splitters are host math) and after the counts
+// Host syncs: after the histogram all-reduce (splitters are host math), after the counts
 // all-gather (receive sizes and the capacity check, which every rank evaluates for every rank so
-// that a too-small dev_out makes ALL ranks return BSORT_ERROR_CAPACITY before any key moves).
+// that a too-small dev_out makes ALL ranks return BSORT_ERROR_CAPACITY before any key moves) and
+// after the exchange (failure detection).  BSORT_DIST_FUSED (§8 N1) replaces a9 + a10 by the
+// partition kernel writing every key straight into its owner's receive buffer over CUDA IPC peer
+// mappings, between two device-side barriers (k_peer_barrier).
 #include <dlfcn.h>
 #include <nccl.h>
 
@@ -27,7 +30,6 @@
 #include <vector>
 
 #include "bsort.h"
-#include "common.cuh"
 #include "common.cuh"
 
 namespace {
@@ -133,6 +135,16 @@ struct bsort_comm {
   void* ws = nullptr;
   size_t ws_bytes = 0;
   cudaEvent_t ws_done = nullptr;
+  // Fused exchange (BSORT_DIST_FUSED): this rank's receive buffer and signal pad
+  // (cudaMalloc, exported by CUDA IPC handle), every peer's mapped into this process, and the
+  // barrier epoch (the same on every rank: each fused call runs the same two barriers).
+  void* rbuf = nullptr;
+  size_t rbytes = 0;
+  unsigned* pad = nullptr;  // [BSORT_DIST_MAX_RANKS] arrival epochs of each peer, then [1] error
+  void* peer_rbuf[BSORT_DIST_MAX_RANKS] = {};
+  unsigned* peer_pad[BSORT_DIST_MAX_RANKS] = {};
+  unsigned char* hbuf = nullptr;  // device staging of the all-gathered IPC handles
+  unsigned epoch = 0;
 };
 
 namespace {
@@ -237,8 +249,123 @@ int refine_cb(void* p, const uint64_t* prefixes, int m, int prefix_bits, uint64_
   return wait_watching(r->s, r->c) == BSORT_SUCCESS ? 0 : 4;
 }
 
+// ---------------------------------------------------------------- fused exchange (§8 N1)
+
+struct PeerPads {
+  unsigned* p[BSORT_DIST_MAX_RANKS];
+};
+
+__device__ __forceinline__ unsigned long long globaltimer_ns() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
+// Device-side barrier over the ranks' signal pads (no host round trip): thread q tells rank q
+// that this rank reached barrier `epoch` (a system-scope release store into q's pad, over
+// NVLink for a peer) and waits until rank q has told this rank the same.  The release orders
+// every earlier write of this stream -- the partition kernel's remote stores -- before the
+// signal.  A peer that never arrives (dead process) would hang the stream: after timeout_ns
+// the thread gives up and sets the error word, which the host checks.
+__global__ void k_peer_barrier(PeerPads pads, unsigned* mine, int me, int P, unsigned epoch,
+                               unsigned long long timeout_ns) {
+  const int q = threadIdx.x;
+  if (q >= P) return;
+  __threadfence_system();
+  asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(pads.p[q] + me), "r"(epoch) : "memory");
+  const unsigned long long t0 = globaltimer_ns();
+  for (;;) {
+    unsigned v;
+    asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(mine + q) : "memory");
+    if ((int)(v - epoch) >= 0) break;
+    if (timeout_ns && globaltimer_ns() - t0 > timeout_ns) {
+      atomicExch(mine + BSORT_DIST_MAX_RANKS, 1u);
+      break;
+    }
+    __nanosleep(256);
+  }
+}
+
+bsort_status_t peer_barrier(bsort_comm* c, cudaStream_t s) {
+  PeerPads pp{};
+  for (int q = 0; q < c->nranks; ++q) pp.p[q] = c->peer_pad[q];
+  const double lim = nccl_timeout_s();
+  const unsigned long long tns = lim > 0 ? (unsigned long long)(lim * 1e9) : 0ull;
+  BSORT_LAUNCH(bsort::PROF_DIST_PART, s,
+               k_peer_barrier<<<1, 64, 0, s>>>(pp, c->pad, c->rank, c->nranks, ++c->epoch, tns));
+  return BSORT_SUCCESS;
+}
+
+// All-gather of one 64-byte CUDA IPC handle per rank (through NCCL) and the mapping of every
+// peer's allocation into this process; out[me] = mine.
+bsort_status_t exchange_handles(bsort_comm* c, void* mine, void** out, cudaStream_t s) {
+  NcclApi& N = nccl();
+  const int P = c->nranks, me = c->rank;
+  out[me] = mine;
+  if (P == 1) return BSORT_SUCCESS;
+  cudaIpcMemHandle_t h;
+  CUDA_TRY(cudaIpcGetMemHandle(&h, mine));
+  static_assert(sizeof(cudaIpcMemHandle_t) == 64, "IPC handle size");
+  CUDA_TRY(cudaMemcpyAsync(c->hbuf + (size_t)me * 64, &h, 64, cudaMemcpyHostToDevice, s));
+  NCCL_TRY(N.AllGather(c->hbuf + (size_t)me * 64, c->hbuf, 64, ncclUint8, c->comm, s));
+  std::vector<cudaIpcMemHandle_t> all(P);
+  CUDA_TRY(cudaMemcpyAsync(all.data(), c->hbuf, (size_t)P * 64, cudaMemcpyDeviceToHost, s));
+  BS_TRY(wait_watching(s, c));
+  for (int q = 0; q < P; ++q) {
+    if (q == me) continue;
+    void* p = nullptr;
+    CUDA_TRY(cudaIpcOpenMemHandle(&p, all[q], cudaIpcMemLazyEnablePeerAccess));
+    out[q] = p;
+  }
+  return BSORT_SUCCESS;
+}
+
+void close_peers(bsort_comm* c, void** arr) {
+  for (int q = 0; q < c->nranks; ++q) {
+    if (q != c->rank && arr[q]) cudaIpcCloseMemHandle(arr[q]);
+    arr[q] = nullptr;
+  }
+}
+
+// First fused call: signal pads (zeroed; epochs only grow) and the handle staging buffer.
+bsort_status_t ensure_pads(bsort_comm* c, cudaStream_t s) {
+  if (c->pad) return BSORT_SUCCESS;
+  CUDA_TRY(cudaMalloc(&c->hbuf, (size_t)BSORT_DIST_MAX_RANKS * 64));
+  CUDA_TRY(cudaMalloc(reinterpret_cast<void**>(&c->pad), (BSORT_DIST_MAX_RANKS + 32) * sizeof(unsigned)));
+  CUDA_TRY(cudaMemsetAsync(c->pad, 0, (BSORT_DIST_MAX_RANKS + 32) * sizeof(unsigned), s));
+  CUDA_TRY(cudaStreamSynchronize(s));  // zeroed before any peer can signal into it
+  void* tmp[BSORT_DIST_MAX_RANKS] = {};
+  BS_TRY(exchange_handles(c, c->pad, tmp, s));
+  for (int q = 0; q < c->nranks; ++q) c->peer_pad[q] = static_cast<unsigned*>(tmp[q]);
+  return BSORT_SUCCESS;
+}
+
+// Receive buffers of at least `bytes` on EVERY rank (collective: all ranks evaluate the same
+// condition from the all-gathered counts, so they grow together).  Old mappings are closed and
+// the old buffer freed only after every rank has mapped the new one (NCCL all-reduce as the
+// barrier).
+bsort_status_t ensure_rbuf(bsort_comm* c, size_t bytes, cudaStream_t s) {
+  if (bytes <= c->rbytes && c->rbuf) return BSORT_SUCCESS;
+  NcclApi& N = nccl();
+  const size_t nb = round_up(std::max(bytes, c->rbytes + c->rbytes / 2), 1 << 21);
+  void* fresh = nullptr;
+  CUDA_TRY(cudaMalloc(&fresh, nb));
+  void* old = c->rbuf;
+  close_peers(c, c->peer_rbuf);
+  c->rbuf = fresh;
+  c->rbytes = nb;
+  BS_TRY(exchange_handles(c, fresh, c->peer_rbuf, s));
+  if (old) {
+    NCCL_TRY(N.AllReduce(c->hbuf, c->hbuf, 1, ncclUint8, ncclMax, c->comm, s));
+    BS_TRY(wait_watching(s, c));
+    cudaFree(old);
+  }
+  return BSORT_SUCCESS;
+}
+
 bsort_status_t sort_dist_impl(bsort_dtype_t dtype, const void* dev_in, uint64_t n, void* dev_out, uint64_t cap,
-                              uint64_t* n_out, bsort_direction_t dir, bool exact, bsort_comm* c, cudaStream_t s) {
+                              uint64_t* n_out, bsort_direction_t dir, bool exact, bool fused, bsort_comm* c,
+                              cudaStream_t s) {
   NcclApi& N = nccl();
   if (c->aborted) return nccl_status(ncclInvalidUsage);
   const int P = c->nranks, me = c->rank;
@@ -253,7 +380,7 @@ bsort_status_t sort_dist_impl(bsort_dtype_t dtype, const void* dev_in, uint64_t 
   const int CW = exact ? 2 * (P - 1) + 2 : P + 1;  // u64 words per rank in the gathered counts
   const size_t cnt_b = round_up((size_t)P * CW * 8, 256);
   const size_t ref_b = exact ? (size_t)(P - 1) * BSORT_DIST_BINS * 8 : 0;
-  const size_t bucket_b = round_up((size_t)n * es, 256);
+  const size_t bucket_b = fused ? 0 : round_up((size_t)n * es, 256);  // fused: no bucketed copy
   const size_t part_ws = exact ? bsort_dist_class_partition_workspace_bytes()
                                : bsort_dist_partition_workspace_bytes(dtype, n, P);
   const size_t head = 2 * hist_b + cnt_b + ref_b;
@@ -338,6 +465,44 @@ bsort_status_t sort_dist_impl(bsort_dtype_t dtype, const void* dev_in, uint64_t 
   }
   if (n_out) *n_out = recv_total;
   if (overflow) return BSORT_ERROR_CAPACITY;
+
+  if (fused) {
+    // §8 N1: the partition's write-out IS the exchange -- keys for rank q are stored straight
+    // into q's receive buffer (peer-mapped over NVLink) at the slots after the keys of the ranks
+    // before this one; two device-side barriers replace the host syncs of the NCCL exchange.
+    BS_TRY(ensure_pads(c, s));
+    uint64_t need = 1;
+    for (int q = 0; q < P; ++q) {
+      uint64_t tot = 0;
+      for (int r = 0; r < P; ++r) tot += sent(r, q);
+      need = std::max(need, tot);
+    }
+    BS_TRY(ensure_rbuf(c, (size_t)need * es, s));
+    std::vector<uint64_t> dst(P);
+    for (int q = 0; q < P; ++q) {
+      uint64_t off = 0;
+      for (int r = 0; r < me; ++r) off += sent(r, q);
+      dst[q] = reinterpret_cast<uint64_t>(c->peer_rbuf[q]) + off * es;
+    }
+    BS_TRY(peer_barrier(c, s));  // every owner is done with its buffer's previous contents
+    if (n > 0)
+      BS_TRY(bsort_dist_partition_remote(dtype, dev_in, n, dir, cuts.data(), &sendm[(size_t)me * P], P, dst.data(),
+                                         ws, part_ws, s));
+    BS_TRY(peer_barrier(c, s));  // every rank's keys for this rank have landed
+    unsigned err = 0;
+    CUDA_TRY(cudaMemcpyAsync(&err, c->pad + BSORT_DIST_MAX_RANKS, sizeof(err), cudaMemcpyDeviceToHost, s));
+    BS_TRY(wait_watching(s, c));
+    if (err) return abort_comm(c, ncclRemoteError);  // a peer never reached the barrier
+    if (recv_total > 1) {
+      const size_t wsb = bsort_workspace_bytes(dtype, recv_total);
+      void* sws = comm_ws(c, wsb, s);
+      if (!sws) return BSORT_ERROR_OUT_OF_MEMORY;
+      BS_TRY(bsort_sort_ws(dtype, c->rbuf, recv_total, dir, sws, wsb, s));
+    }
+    if (recv_total)
+      CUDA_TRY(cudaMemcpyAsync(dev_out, c->rbuf, (size_t)recv_total * es, cudaMemcpyDeviceToDevice, s));
+    return BSORT_SUCCESS;
+  }
 
   // a9: bucketed copy (bucket q = keys for rank q, contiguous)
   if (n > 0) {
@@ -427,6 +592,11 @@ bsort_status_t bsort_comm_destroy(bsort_comm_t c) {
     cudaEventDestroy(c->ws_done);
   }
   if (c->ws) cudaFree(c->ws);
+  close_peers(c, c->peer_rbuf);
+  close_peers(c, reinterpret_cast<void**>(c->peer_pad));
+  if (c->rbuf) cudaFree(c->rbuf);
+  if (c->pad) cudaFree(c->pad);
+  if (c->hbuf) cudaFree(c->hbuf);
   delete c;
   return nccl_status(r);
 }
@@ -444,14 +614,15 @@ bsort_status_t bsort_sort_dist(bsort_dtype_t dtype, const void* dev_in, uint64_t
   if (n_local > 0 && (!dev_in || (uintptr_t)dev_in % es)) return BSORT_ERROR_INVALID_ARGUMENT;
   if (out_capacity > 0 && (!dev_out || (uintptr_t)dev_out % es)) return BSORT_ERROR_INVALID_ARGUMENT;
   if (dev_out && dev_in && dev_out == dev_in && n_local > 0) return BSORT_ERROR_INVALID_ARGUMENT;
-  return sort_dist_impl(dtype, dev_in, n_local, dev_out, out_capacity, n_out, direction, false, comm,
+  return sort_dist_impl(dtype, dev_in, n_local, dev_out, out_capacity, n_out, direction, false, false, comm,
                         (cudaStream_t)stream);
 }
 
 bsort_status_t bsort_sort_dist_ex(bsort_dtype_t dtype, const void* dev_in, uint64_t n_local, void* dev_out,
                                   uint64_t out_capacity, uint64_t* n_out, bsort_direction_t direction,
                                   unsigned flags, bsort_comm_t comm, void* stream) {
-  if ((flags & ~BSORT_DIST_EXACT) != 0) return BSORT_ERROR_INVALID_ARGUMENT;
+  if ((flags & ~(BSORT_DIST_EXACT | BSORT_DIST_FUSED)) != 0) return BSORT_ERROR_INVALID_ARGUMENT;
+  if ((flags & BSORT_DIST_EXACT) && (flags & BSORT_DIST_FUSED)) return BSORT_ERROR_INVALID_ARGUMENT;
   if (!comm || !comm->comm) return BSORT_ERROR_INVALID_ARGUMENT;
   if (direction != BSORT_ASCENDING && direction != BSORT_DESCENDING) return BSORT_ERROR_INVALID_ARGUMENT;
   const int es = key_bytes(dtype);
@@ -460,7 +631,7 @@ bsort_status_t bsort_sort_dist_ex(bsort_dtype_t dtype, const void* dev_in, uint6
   if (out_capacity > 0 && (!dev_out || (uintptr_t)dev_out % es)) return BSORT_ERROR_INVALID_ARGUMENT;
   if (dev_out && dev_in && dev_out == dev_in && n_local > 0) return BSORT_ERROR_INVALID_ARGUMENT;
   return sort_dist_impl(dtype, dev_in, n_local, dev_out, out_capacity, n_out, direction,
-                        (flags & BSORT_DIST_EXACT) != 0, comm, (cudaStream_t)stream);
+                        (flags & BSORT_DIST_EXACT) != 0, (flags & BSORT_DIST_FUSED) != 0, comm, (cudaStream_t)stream);
 }
 
 int bsort_last_nccl_error(void) { return t_last_nccl; }

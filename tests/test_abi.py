@@ -66,6 +66,8 @@ def test_enum_values_match_binding(B):
     assert e["BSORT_ASCENDING"] == _lib.ASCENDING and e["BSORT_DESCENDING"] == _lib.DESCENDING
     src = open(HEADER).read()
     assert int(re.search(r"BSORT_DIST_BINS (\d+)", src).group(1)) == _lib.DIST_BINS
+    assert int(re.search(r"BSORT_DIST_EXACT (\d+)u", src).group(1)) == _lib.DIST_EXACT
+    assert int(re.search(r"BSORT_DIST_FUSED (\d+)u", src).group(1)) == _lib.DIST_FUSED
     assert int(re.search(r"BSORT_PROF_KINDS (\d+)", src).group(1)) == _lib.PROF_KINDS
 
 

@@ -391,7 +391,29 @@ def test_sort_dist_native_capacity(B):
         assert B.lib.bsort_sort_dist(3, ctypes.c_void_p(x.data_ptr()), 10, ctypes.c_void_p(out.data_ptr()),
                                      100, None, 0, comm._h, None) == 2  # i16: unsupported here
         assert B.lib.bsort_sort_dist_ex(8, ctypes.c_void_p(x.data_ptr()), 10, ctypes.c_void_p(out.data_ptr()),
-                                        100, None, 0, 2, comm._h, None) == 1  # unknown flag
+                                        100, None, 0, 4, comm._h, None) == 1  # unknown flag
+        assert B.lib.bsort_sort_dist_ex(8, ctypes.c_void_p(x.data_ptr()), 10, ctypes.c_void_p(out.data_ptr()),
+                                        100, None, 0, 3, comm._h, None) == 1  # EXACT | FUSED
+    finally:
+        comm.close()
+
+
+@pytest.mark.parametrize("dtype,desc", [(torch.float64, False), (torch.int32, True), (torch.uint32, False),
+                                        (torch.int64, True)])
+def test_sort_dist_native_fused_local_comm(B, dtype, desc):
+    """bsort_sort_dist_ex(BSORT_DIST_FUSED) over a one-rank communicator: the partition writes
+    into the communicator's receive buffer (the rank's own entry of the peer table), two
+    device-side barriers on the signal pads, local sort, copy to dev_out.  Sizes grow across
+    calls (the receive buffer is re-allocated) and shrink again (reused)."""
+    comm = B.Comm.local()
+    try:
+        for n in (0, 1, 5000, 300_007, (1 << 20) + 3, 70_001):
+            x = gen(dtype, n, 900 + n)
+            before = x.clone()
+            out = B.sort_dist_native(x, comm, desc, fused=True)
+            torch.cuda.synchronize()
+            assert host(out).tobytes() == oracle.sort_native(host(before), descending=desc).tobytes(), n
+            assert host(x).tobytes() == host(before).tobytes()
     finally:
         comm.close()
 
