@@ -13,6 +13,8 @@ static std::atomic<uint64_t> g_launches{0};
 static thread_local int t_last_err = 0;
 
 void count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
+uint64_t launch_count_now() { return g_launches.load(std::memory_order_relaxed); }
+void add_launches(int64_t k) { g_launches.fetch_add((uint64_t)k, std::memory_order_relaxed); }
 void set_last_cuda_error(cudaError_t e) { t_last_err = (int)e; }
 
 int current_device() {
@@ -59,6 +61,7 @@ struct ProfRec {
 };
 std::mutex g_prof_mu;
 bool g_prof_on = false;
+std::atomic<bool> g_prof_any{false};  // lock-free fast path for prof_begin/prof_end when off
 std::vector<ProfRec> g_prof_recs;
 std::vector<cudaEvent_t> g_event_pool;
 thread_local cudaEvent_t t_open_event = nullptr;
@@ -75,7 +78,10 @@ cudaEvent_t take_event() {
 }
 }  // namespace
 
+bool profiling_on() { return g_prof_any.load(std::memory_order_relaxed); }
+
 void prof_begin(int, cudaStream_t s) {
+  if (!g_prof_any.load(std::memory_order_relaxed)) return;
   std::lock_guard<std::mutex> g(g_prof_mu);
   if (!g_prof_on) return;
   t_open_event = take_event();
@@ -83,6 +89,7 @@ void prof_begin(int, cudaStream_t s) {
 }
 
 void prof_end(int kind, cudaStream_t s) {
+  if (!g_prof_any.load(std::memory_order_relaxed)) return;
   std::lock_guard<std::mutex> g(g_prof_mu);
   if (!g_prof_on || !t_open_event) return;
   cudaEvent_t b = take_event();
@@ -121,6 +128,23 @@ bsort_status_t sort_ws_impl(const DtypeInfo& di, void* keys, uint64_t n, bsort_d
                        : lsd_sort(di, keys, nullptr, n, desc, ws, wsb, s);
 }
 
+// Sorts of up to GRAPH_MAX_N keys replay a cached CUDA graph of their launch sequence (graphs.cu).
+constexpr uint64_t GRAPH_MAX_N = 1ull << 24;
+
+bsort_status_t sort_ws_graphed(bsort_dtype_t dtype, const DtypeInfo& di, void* keys, uint64_t n,
+                               bsort_direction_t dir, void* ws, size_t wsb, cudaStream_t s) {
+  if (n > GRAPH_MAX_N) return sort_ws_impl(di, keys, n, dir, ws, wsb, s);
+  GraphKey k{};
+  k.dtype = (uint64_t)dtype;
+  k.desc = dir == BSORT_DESCENDING;
+  k.device = (uint64_t)current_device();
+  k.n = n;
+  k.keys = (uint64_t)(uintptr_t)keys;
+  k.ws = (uint64_t)(uintptr_t)ws;
+  k.wsb = wsb;
+  return run_graphed(k, s, [&](cudaStream_t st) { return sort_ws_impl(di, keys, n, dir, ws, wsb, st); });
+}
+
 }  // namespace
 
 extern "C" {
@@ -138,7 +162,7 @@ bsort_status_t bsort_sort_ws(bsort_dtype_t dtype, void* dev_keys, uint64_t n, bs
   if (st != BSORT_SUCCESS) return st;
   if (n <= 1) return BSORT_SUCCESS;
   if (workspace_bytes_ < workspace_bytes(di, n)) return BSORT_ERROR_WORKSPACE_TOO_SMALL;
-  return sort_ws_impl(di, dev_keys, n, direction, workspace, workspace_bytes_, (cudaStream_t)stream);
+  return sort_ws_graphed(dtype, di, dev_keys, n, direction, workspace, workspace_bytes_, (cudaStream_t)stream);
 }
 
 size_t bsort_inplace_workspace_bytes(bsort_dtype_t dtype, uint64_t n, uint64_t chunk_keys) {
@@ -173,7 +197,7 @@ bsort_status_t bsort_sort(bsort_dtype_t dtype, void* dev_keys, uint64_t n, bsort
     cudaGetLastError();
     return BSORT_ERROR_OUT_OF_MEMORY;
   }
-  st = sort_ws_impl(di, dev_keys, n, direction, ws, wsb, s);
+  st = sort_ws_graphed(dtype, di, dev_keys, n, direction, ws, wsb, s);
   e = cudaFreeAsync(ws, s);
   if (st == BSORT_SUCCESS && e != cudaSuccess) {
     set_last_cuda_error(e);
@@ -195,7 +219,7 @@ bsort_status_t bsort_sort_host(bsort_dtype_t dtype, void* host_keys, uint64_t n,
   prof_begin(PROF_H2D, s);
   BSORT_CUDA(cudaMemcpyAsync(dev_keys, host_keys, bytes, cudaMemcpyHostToDevice, s));
   prof_end(PROF_H2D, s);
-  st = sort_ws_impl(di, dev_keys, n, direction, workspace, workspace_bytes_, s);
+  st = sort_ws_graphed(dtype, di, dev_keys, n, direction, workspace, workspace_bytes_, s);
   if (st != BSORT_SUCCESS) return st;
   prof_begin(PROF_D2H, s);
   BSORT_CUDA(cudaMemcpyAsync(host_keys, dev_keys, bytes, cudaMemcpyDeviceToHost, s));
@@ -521,6 +545,7 @@ void bsort_profile_enable(int on) {
   }
   g_prof_recs.clear();
   g_prof_on = on != 0;
+  g_prof_any.store(on != 0, std::memory_order_relaxed);
 }
 
 int bsort_profile_read(double* ms, uint64_t* launches) {

@@ -2,6 +2,7 @@
 //
 // Nothing here is shared with oracle/ (the CPU checker); this is the product side only.
 #pragma once
+#include <functional>
 
 #include <cuda_runtime.h>
 #include <stdint.h>
@@ -109,6 +110,17 @@ struct DeviceInt {
 void prof_end(int kind, cudaStream_t s);
 void count_launch();
 int num_sms();
+// graphs.cu: replay of a sort's launch sequence as a cached CUDA graph.  The key holds every
+// argument the launch sequence depends on (all 64-bit: no padding, compared with memcmp).
+struct GraphKey {
+  uint64_t dtype, desc, device, n;
+  uint64_t keys, vals, ws, wsb;
+};
+bsort_status_t run_graphed(const GraphKey& key, cudaStream_t s,
+                           const std::function<bsort_status_t(cudaStream_t)>& run);
+bool profiling_on();
+uint64_t launch_count_now();
+void add_launches(int64_t k);
 // selftest.cu: shared atomicAdd hands out old values in lane order on this device (checked
 // once per device on first use; false while `s` is being captured before the check has run)
 bool atomics_lane_ordered(cudaStream_t s);

@@ -20,7 +20,7 @@ pytestmark = pytest.mark.gpu
 
 REPO = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 NP = {torch.uint32: np.uint32, torch.int32: np.int32, torch.float32: np.float32,
-      torch.uint64: np.uint64, torch.int64: np.int64, torch.float64: np.float64}
+      torch.uint64: np.uint64, torch.int64: np.int64, torch.float64: np.float64, torch.uint8: np.uint8}
 SIGNED = {torch.uint32: torch.int32, torch.uint64: torch.int64}
 
 
@@ -146,3 +146,46 @@ def test_selftest_lane_order(B):
     did not, the library would route around those kernels and this documents that it does not
     need to on this part)."""
     assert B.selftest() == 0
+
+
+@pytest.mark.parametrize("dtype,n", [(torch.int32, 1 << 20), (torch.float64, 300_007), (torch.uint8, 100_000),
+                                     (torch.float32, (1 << 22) + 3)])
+def test_graph_replay_same_buffers(B, dtype, n):
+    """Repeated sorts of the same buffers (same Sorter workspace): call 1 runs plain launches,
+    call 2 captures the launch sequence into a CUDA graph, later calls replay it (graphs.cu).
+    New data every call, both directions: the replayed graph re-reads keys and re-plans."""
+    s = B.Sorter(dtype, n, "cuda")
+    w = torch.empty(n, dtype=dtype, device="cuda")
+    for i in range(6):
+        desc = bool(i % 2)
+        src = gen(dtype, n, 4000 + i) if dtype != torch.uint8 else W.uniform_int(dtype, n, 4000 + i, "cuda")
+        if i == 4:
+            src = torch.sort(src)[0]  # presorted input through the replayed graph (plan skips passes)
+        w.copy_(src)
+        ref = oracle.sort_native(host(w) if dtype in NP else w.cpu().numpy(), descending=desc)
+        c0 = B.launch_count()
+        s(w, desc)
+        torch.cuda.synchronize()
+        assert B.launch_count() > c0
+        got = host(w) if dtype in NP else w.cpu().numpy()
+        assert got.tobytes() == ref.tobytes(), (i, desc)
+
+
+def test_graph_replay_disabled_matches():
+    """BSORT_GRAPH=0 (plain launches every call) gives the same bytes as the replayed graphs."""
+    code = r"""
+import sys; sys.path.insert(0, %r)
+import torch, oracle, workloads as W, paper_2603_08929_b200 as B
+n = 1 << 20
+s = B.Sorter(torch.int32, n, "cuda")
+w = torch.empty(n, dtype=torch.int32, device="cuda")
+for i in range(4):
+    w.copy_(W.uniform_int(torch.int32, n, 77 + i, "cuda"))
+    ref = oracle.sort_native(w.cpu().numpy())
+    s(w); torch.cuda.synchronize()
+    assert w.cpu().numpy().tobytes() == ref.tobytes(), i
+print("ok")
+""" % REPO
+    r = subprocess.run([sys.executable, "-c", code], env=dict(os.environ, BSORT_GRAPH="0"), capture_output=True,
+                       text=True, timeout=600, cwd=REPO)
+    assert r.returncode == 0 and "ok" in r.stdout, r.stderr[-2000:]
