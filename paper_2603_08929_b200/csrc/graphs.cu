@@ -1,8 +1,8 @@
 // graphs.cu — CUDA-graph replay of small sorts (DESIGN.md §6 "Small n").
 //
-// Below 2^24 keys a sort is a handful of dependent launches whose host enqueue (~2.5-3.8 us per
-// kernel launch on B200 with this driver, tools/exp/launch_cost.cu) exceeds their device time:
-// 2^20 i32 keys are 6 launches + 1 memset = ~19 us of host time for ~21 us of GPU work.  The
+// Below 2^24 keys a sort is a handful of dependent launches whose host enqueue costs ~2.5-3.8 us
+// per kernel launch on B200 with this driver (tools/exp/launch_cost.cu): 6 launches + 1 memset
+// are ~19 us of host time before the last kernel is even queued.  The
 // launch sequence of a sort depends only on (dtype, n, direction, buffers, workspace, device) --
 // every data-dependent decision (trivial digits, presorted input, pass variants) is taken on the
 // device from the plan in the workspace -- so the library captures it once into a CUDA graph

@@ -14,6 +14,7 @@
 #include "onesweep_ws.cuh"
 #include "pass2.cuh"
 #include "small.cuh"
+#include "small_grid.cuh"
 #include "paths.cuh"
 
 namespace bsort {
@@ -59,6 +60,7 @@ template <typename U> constexpr int hist_lanes() { return sizeof(U) == 4 ? 32 : 
 struct LsdLayout {
   size_t scratch, vscratch, ghist, bases, gcount, joint, seg, plan, counters, lookback, total;
   size_t lb_bytes;    // one look-back region
+  size_t grid;        // k_grid_sort (small_grid.cuh): per-pass count matrix + barrier word
   uint64_t lb_tiles;  // look-back descriptor rows: tiles of the smallest look-back tile in use
 };
 
@@ -100,6 +102,7 @@ LsdLayout lsd_layout(uint64_t n, bool kv = false) {
   // next pass's region: no memset launches, lsd_run)
   l.lb_bytes = align_up(tiles * 256 * desc, 256);
   l.lookback = off; off += (n < WS_MIN_N ? 2 : 1) * l.lb_bytes;
+  l.grid = off;     off = align_up(off + grid_detail::workspace_bytes(), 256);  // k_grid_sort counts
   l.lb_tiles = tiles;
   l.total = off;
   return l;
@@ -265,9 +268,12 @@ bsort_status_t lsd_run(U* keys, uint32_t* vals, uint64_t n, unsigned char* ws, c
   auto* lookback = reinterpret_cast<DescT*>(ws + l.lookback);
 
   // small n: the whole sort in one single-CTA launch (small.cuh)
-  if constexpr (!KV)
-    if (n <= small_max_n<U>())
-      return launch_small<KIND, DESC, U>(keys, n, s);
+  if constexpr (!KV) {
+    if (n <= small_max_n<U>()) return launch_small<KIND, DESC, U>(keys, n, s);
+    // mid-size: one cooperative launch, one CTA per SM (small_grid.cuh)
+    if (n <= grid_max_n<U>() && n >= grid_min_n<U>())
+      return launch_grid<KIND, DESC, U>(keys, scratch, n, reinterpret_cast<uint16_t*>(ws + l.grid), s);
+  }
 
   static const bool joint_off = getenv("BSORT_NO_JOINT") != nullptr;  // A/B and debugging
   const bool use_joint = n >= JOINT_MIN_N && !joint_off;

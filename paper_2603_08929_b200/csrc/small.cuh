@@ -1,7 +1,7 @@
 // Small-n LSD sort: ONE CTA, ONE launch, the whole sort in shared memory (SURVEY §8 row
 // "small-n latency").
 //
-// Below ~12K keys the multi-launch path (memset, histogram, plan, P scatter passes, copy-back:
+// Up to 20K keys the multi-launch path (memset, histogram, plan, P scatter passes, copy-back:
 // 8-11 dependent launches, ~20 us of device time and ~30 us of host enqueue) is all fixed cost.
 // Here one CTA of 512 threads loads the keys into shared memory once and runs every LSD pass
 // (the paper's Algorithm 2 counting step per digit, P:174-184, 8 bits at a time) between two
@@ -19,10 +19,8 @@
 // A pass whose digit is constant over all keys is skipped (the counts show it).  Keys are
 // transformed (a1) only to extract digits; the buffers hold the raw keys.
 //
-// A multi-CTA variant (one CTA per SM, grid-wide barriers between a pass's count and scatter
-// phases, tried for n up to 2^22) was slower than the multi-launch path from 2^18 keys up: each
-// pass paid two grid barriers (1.2 us each, tools/exp/gridbar.cu) plus a cross-CTA count scan,
-// 10-13 us per pass against 4-5 us for a look-back pass kernel.
+// Above its capacity (20480 32-bit / 10240 64-bit keys) the one-CTA-per-SM variant
+// (small_grid.cuh) takes over.
 #pragma once
 
 #include "common.cuh"
@@ -164,7 +162,7 @@ __global__ void __launch_bounds__(small_detail::THREADS, 1)
 }
 
 // Keys-only sorts of at most small_max_n<U>() keys take this path (BSORT_SMALL=0 disables it;
-// BSORT_SMALL_MAX sets the bound, up to what fits: 20480 / 10240 keys).
+// BSORT_SMALL_MAX lowers the bound from what fits: 20480 / 10240 keys).
 template <typename U>
 inline uint64_t small_max_n() {
   static const uint64_t v = [] {
@@ -172,10 +170,7 @@ inline uint64_t small_max_n() {
     if (e && e[0] == '0') return (uint64_t)0;
     const char* mx = getenv("BSORT_SMALL_MAX");
     const uint64_t cap = small_detail::max_n<U>();
-    // one SM sorts ~1.6 Gkeys/s per pass: beyond ~12K 32-bit keys the multi-launch path's 148
-    // SMs win despite its ~8 launches (tools/time_small.py)
-    const uint64_t dflt = sizeof(U) == 4 ? 12288 : 6144;
-    return mx ? min64(strtoull(mx, nullptr, 10), cap) : dflt;
+    return mx ? min64(strtoull(mx, nullptr, 10), cap) : cap;
   }();
   return v;
 }

@@ -173,7 +173,8 @@ def test_workspace_bytes_monotone_in_n(B):
     from paper_2603_08929_b200 import _lib
     L = _lib.lib
     probes = sorted({m for e in range(1, 33) for m in ((1 << e) - 1, 1 << e, (1 << e) + 1)} |
-                    {12287, 12288, 12289, 6143, 6144, 6145, (1 << 22) - 8193, (1 << 22) - 1})
+                    {20479, 20480, 20481, 10239, 10240, 10241, 148 * 20480 - 1, 148 * 20480, 148 * 20480 + 1,
+                     148 * 10240, 148 * 10240 + 1, (1 << 22) - 8193, (1 << 22) - 1})
     for code in (_lib.U8, _lib.I16, _lib.U32, _lib.F32, _lib.I64, _lib.F64):
         prev = 0
         for m in probes:

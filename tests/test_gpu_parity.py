@@ -173,7 +173,7 @@ def test_errors_raise(B):
 
 
 def test_launch_counter_moves(B):
-    x = gen(torch.int32, 100_000, 1)
+    x = gen(torch.int32, (1 << 22) + 1, 1)
     c0 = B.launch_count()
     B.sort_(x)
     torch.cuda.synchronize()

@@ -1,10 +1,11 @@
-"""GPU parity of the small-n path (csrc/small.cuh: the whole LSD sort in shared memory by one
-CTA in one launch, keys-only sorts of n <= 12288 32-bit / 6144 64-bit keys) against the CPU
-oracle, bit for bit: sizes around warp segments and both sides of the size bound, passes
-skipped for constant digits (odd and even numbers of moving passes), both directions, the
-multi-launch path above the bound (its look-back zeroing folded into the pass kernels below
-2^22 keys) and at the same sizes (BSORT_SMALL=0, in a subprocess: the switch is read once per
-process)."""
+"""GPU parity of the small-n paths against the CPU oracle, bit for bit: csrc/small.cuh (the
+whole LSD sort in shared memory by one CTA in one launch, keys-only n <= 20480 32-bit / 10240
+64-bit keys) and csrc/small_grid.cuh (one cooperative launch, one CTA per SM with grid barriers,
+up to SMs x 20480 / 10240 keys): sizes around warp segments, chunk and grid boundaries and both
+sides of each bound, passes skipped for constant digits (odd and even numbers of moving
+passes), both directions, the multi-launch path above the bounds (its look-back zeroing folded
+into the pass kernels below 2^22 keys) and at the same sizes (BSORT_SMALL=0 / BSORT_GRID=0 /
+BSORT_SMALL_MAX, in subprocesses: the switches are read once per process)."""
 import os
 import subprocess
 import sys
@@ -54,7 +55,7 @@ def check(B, t, desc, what):
 
 
 def bound(dtype):
-    return 12288 if torch.empty(0, dtype=dtype).element_size() == 4 else 6144
+    return 20480 if torch.empty(0, dtype=dtype).element_size() == 4 else 10240
 
 
 @pytest.mark.parametrize("dtype", [torch.int32, torch.float32, torch.uint64, torch.float64],
@@ -62,8 +63,10 @@ def bound(dtype):
 @pytest.mark.parametrize("desc", [False, True], ids=["asc", "desc"])
 def test_small_sizes(B, dtype, desc):
     big = bound(dtype)
+    gmax = torch.cuda.get_device_properties(0).multi_processor_count * big  # k_grid_sort capacity
     for n in [2, 3, 15, 16, 17, 31, 32, 33, 511, 512, 513, 4097, big // 2 + 3, big - 1, big, big + 1,
-              3 * big + 7, 300_007, (1 << 22) - 1, (1 << 22) + 1]:
+              2 * 8192 + 5, 3 * big + 7, 300_007, (1 << 20) + 3, gmax - 1, gmax, gmax + 1,
+              (1 << 22) - 1, (1 << 22) + 1]:
         check(B, gen(dtype, n, 1000 + n), desc, f"n={n}")
 
 
@@ -89,7 +92,7 @@ def test_small_all_equal_and_two_values(B):
 
 
 def test_multilaunch_path_at_small_sizes():
-    """BSORT_SMALL=0: the multi-launch one-sweep path the small kernel replaces, same sizes."""
+    """BSORT_SMALL=0 BSORT_GRID=0: the multi-launch one-sweep path the small kernels replace, same sizes."""
     code = r"""
 import sys; sys.path.insert(0, %r)
 import numpy as np, torch, oracle, workloads as W, paper_2603_08929_b200 as B
@@ -102,32 +105,49 @@ for dt, n in ((torch.int32, 1000), (torch.int32, 1 << 20), (torch.float64, 70001
         assert y.cpu().numpy().tobytes() == ref.tobytes(), (dt, n, desc)
 print("ok")
 """ % REPO
-    r = subprocess.run([sys.executable, "-c", code], env=dict(os.environ, BSORT_SMALL="0"), capture_output=True,
+    r = subprocess.run([sys.executable, "-c", code], env=dict(os.environ, BSORT_SMALL="0", BSORT_GRID="0"), capture_output=True,
                        text=True, timeout=600, cwd=REPO)
     assert r.returncode == 0 and "ok" in r.stdout, r.stderr[-2000:]
 
 
-def test_small_bound_override():
-    """BSORT_SMALL_MAX=20480 (the shared-memory limit for 32-bit keys) in a subprocess: the
-    single-CTA kernel up to its capacity."""
+def _subprocess_sorts(env, cases, expect_launches=None):
     code = r"""
 import sys; sys.path.insert(0, %r)
 import numpy as np, torch, oracle, workloads as W, paper_2603_08929_b200 as B
-for dt, n in ((torch.int32, 20480), (torch.float32, 20479), (torch.uint32, 16385), (torch.float64, 10240),
-              (torch.int64, 9999)):
+U = {torch.uint32: (torch.int32, np.uint32), torch.uint64: (torch.int64, np.uint64)}
+for dt, n in %r:
     x = W.special_mix(dt, n, 9, "cuda") if dt.is_floating_point else W.uniform_int(dt, n, 9, "cuda")
-    sd = {torch.uint32: torch.int32}.get(dt, dt)
-    h = x.view(sd).cpu().numpy().view({torch.uint32: np.uint32}.get(dt, x.view(sd).cpu().numpy().dtype))
+    sd, nd = U.get(dt, (dt, None))
+    h = x.view(sd).cpu().numpy()
+    h = h.view(nd) if nd else h
     for desc in (False, True):
         ref = oracle.sort_native(h, descending=desc)
         y = x.clone(); c0 = B.launch_count(); B.sort_(y, descending=desc); torch.cuda.synchronize()
-        assert B.launch_count() - c0 == 1, "single-CTA path expected"
+        if %r is not None:
+            assert B.launch_count() - c0 == %r, (dt, n, B.launch_count() - c0)
         assert y.view(sd).cpu().numpy().tobytes() == ref.tobytes(), (dt, n, desc)
 print("ok")
-""" % REPO
-    r = subprocess.run([sys.executable, "-c", code], env=dict(os.environ, BSORT_SMALL_MAX="20480"),
-                       capture_output=True, text=True, timeout=600, cwd=REPO)
+""" % (REPO, cases, expect_launches, expect_launches)
+    code = code.replace("torch.torch.", "torch.")
+    r = subprocess.run([sys.executable, "-c", code], env=dict(os.environ, **env), capture_output=True, text=True,
+                       timeout=600, cwd=REPO)
     assert r.returncode == 0 and "ok" in r.stdout, r.stderr[-2000:]
+
+
+CASES_SMALL = "[(torch.int32, 20480), (torch.float32, 20479), (torch.uint32, 16385), (torch.int32, 1001), " \
+              "(torch.float32, 4097), (torch.float64, 1 << 18), (torch.int64, (1 << 18) + 7)]"
+
+
+def test_grid_kernel_at_small_sizes():
+    """BSORT_SMALL_MAX=1000: sizes the single-CTA kernel would take run k_grid_sort with 1-5 CTAs
+    (chunks of >= 4096 keys), one launch each; 64-bit keys from k_grid_sort's 2^18 lower bound."""
+    _subprocess_sorts({"BSORT_SMALL_MAX": "1000"}, eval(CASES_SMALL), expect_launches=1)
+
+
+def test_multilaunch_at_grid_sizes():
+    """BSORT_GRID=0: the multi-launch path at the sizes k_grid_sort takes by default."""
+    _subprocess_sorts({"BSORT_GRID": "0"}, [(torch.int32, 300_007), (torch.float64, 70_001),
+                                             (torch.uint32, (1 << 20) + 3), (torch.int64, 1 << 20)])
 
 
 def test_small_launch_count(B):
