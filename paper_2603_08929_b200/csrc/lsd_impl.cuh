@@ -169,7 +169,7 @@ inline bool ws_enabled() {
 template <typename U, typename DescT, bool KV = false, int MODE = RANK_RUN2, typename DigitF>
 bsort_status_t launch_pass_ws(const U* a, U* b, uint64_t n, DigitF digit, const unsigned long long* bases,
                               DescT* lookback, uint32_t* counter, const PassPlan* plan, int pass, cudaStream_t s,
-                              KvPtrs kvp = {}, unsigned long long* gcount = nullptr) {
+                              KvPtrs kvp = {}, unsigned long long* gcount = nullptr, uint32_t only_fewruns = 0) {
   constexpr int WS_RT = WsCfg<U, KV>::RT;
   using L = PassSmemWS<WS_RT, WsCfg<U, KV>::ITEMS, U, KV>;
   static_assert(L::bytes <= 227 * 1024, "fits one CTA per SM");
@@ -186,7 +186,8 @@ bsort_status_t launch_pass_ws(const U* a, U* b, uint64_t n, DigitF digit, const 
   const uint64_t grid = min64(tiles, (uint64_t)num_sms() * occ);  // all resident (look-back progress)
   BSORT_LAUNCH(PROF_PASS, s,
                kern<<<(unsigned)grid, WS_RT + 256, L::bytes, s>>>(a, b, n, digit, bases, lookback, counter,
-                                                                  (uint32_t)tiles, plan, pass, kvp, gcount));
+                                                                  (uint32_t)tiles, plan, pass, kvp, gcount,
+                                                                  only_fewruns));
   return BSORT_SUCCESS;
 }
 
@@ -277,6 +278,10 @@ bsort_status_t lsd_run(U* keys, uint32_t* vals, uint64_t n, unsigned char* ws, c
 
   static const bool joint_off = getenv("BSORT_NO_JOINT") != nullptr;  // A/B and debugging
   const bool use_joint = n >= JOINT_MIN_N && !joint_off;
+  // passes 2-3 of 32-bit keys: k_pass2, or the run-ranking warp-specialised kernel when the plan
+  // finds few distinct lower-bit values (k_plan_joint's fewruns; both launched, one works)
+  const bool few_alt = sizeof(U) == 4 && !KV && use_joint && n >= WS_MIN_N && n <= P2_MAX_N && p2_enabled() &&
+                       ws_enabled() && (uintptr_t)keys % 16 == 0;
   // digit histograms and, right after them, the presorted-input flags (k_onesweep_hist*)
   auto* order = reinterpret_cast<uint32_t*>(ghist + P * 256);
   BSORT_LAUNCH(PROF_MEMSET, s, cudaMemsetAsync(ghist, 0, P * 256 * 8 + 16, s));
@@ -290,7 +295,10 @@ bsort_status_t lsd_run(U* keys, uint32_t* vals, uint64_t n, unsigned char* ws, c
       hattr.mark();
     }
     BSORT_LAUNCH(PROF_MEMSET, s, cudaMemsetAsync(joint, 0, 65536 * 8, s));
-    BSORT_LAUNCH(PROF_HIST, s, hk<<<num_sms(), HIST_THREADS, hsmem, s>>>(keys, n, ghist, joint, order));
+    // presorted check first (stops early on unsorted input); the histogram sweep then checks no
+    // pairs, and does nothing for a presorted / reversed input
+    BSORT_LAUNCH(PROF_HIST, s, k_order_check<KIND, DESC, U><<<num_sms(), HIST_THREADS, 0, s>>>(keys, n, order));
+    BSORT_LAUNCH(PROF_HIST, s, hk<<<num_sms(), HIST_THREADS, hsmem, s>>>(keys, n, ghist, joint, order, true));
   } else {
     // the histogram kernel's last CTA also plans (no k_plan launch)
     auto hk = k_onesweep_hist<KIND, DESC, U, LANES, true>;
@@ -311,7 +319,9 @@ bsort_status_t lsd_run(U* keys, uint32_t* vals, uint64_t n, unsigned char* ws, c
                  k_plan_joint<<<1, 256, 0, s>>>(joint, ghist, bases + 256, J01_TILE, plan, seg,
                                                 (sizeof(U) == 4 && !KV && n <= P2_MAX_N && p2_enabled() && p2_run2_enabled())
                                                     ? p2_tile<R2_RUN2>()
-                                                    : 0));
+                                                    : 0,
+                                                few_alt ? (uint64_t)WsCfg<U, false>::RT * WsCfg<U, false>::ITEMS : 0,
+                                                n));
   bsort_status_t st = BSORT_SUCCESS;
   const bool fold = n < WS_MIN_N;  // look-back zeroing folded into the pass kernels
   auto one_pass = [&](auto shift_c) {
@@ -355,8 +365,14 @@ bsort_status_t lsd_run(U* keys, uint32_t* vals, uint64_t n, unsigned char* ws, c
             atomics_lane_ordered(s)) {
           // (half-warp counter rows for skewed top digits, k_pass2<..., HALVES = 2> with
           // P2_SKEWVAR, measured no faster on cfg3's sign+exponent digit: 3.98 vs 3.92 ms)
+          const bool alt = few_alt && p >= 2;
           st = launch_pass2<KIND, DESC, SH>(keys, scratch, n, bases + p * 256,
-                                            reinterpret_cast<uint32_t*>(lookback), counters + p, plan, p, s);
+                                            reinterpret_cast<uint32_t*>(lookback), counters + p, plan, p, s,
+                                            alt ? P2_FEWALT : 0u);
+          if (st == BSORT_SUCCESS && alt)
+            st = launch_pass_ws<U, DescT, false, RANK_RUN2>(keys, scratch, n, RadixDigit<KIND, DESC, U, SH>{},
+                                                            bases + p * 256, lookback, counters + p, plan, p, s,
+                                                            KvPtrs{}, nullptr, 1u);
           // pass 2 ranked by runs when the plan allows it (each launch checks plan->run2)
           if constexpr (p == 2)
             if (st == BSORT_SUCCESS && use_joint)

@@ -112,7 +112,9 @@ struct PassPlan {
   uint32_t last;        // last executed pass (8: none) -- k_pass2 decodes keys as it writes them
   uint32_t run2;        // pass 2 runs as R2_RUN2 (every nonzero (digit 1, digit 0) bin >= one tile)
   uint32_t skew;        // bit p: one bin of digit p holds > n/8 keys (pass2.cuh half-warp counters)
-  uint32_t pad[8];
+  uint32_t fewruns;     // bit p: pass p's input has few distinct lower-bit values (long runs): the
+                        // run-ranking look-back kernel replaces k_pass2 (k_plan_joint)
+  uint32_t pad[7];
 };
 
 // Presorted-input check (§8 a3 "sortedness test"), folded into the histogram sweep: for every
@@ -317,12 +319,120 @@ __global__ void __launch_bounds__(HIST_THREADS, 1)
 // so that nearly sorted keys spread over banks; a warp whose 32 keys share one joint bin (runs
 // of equal keys) adds once.  The marginals of digits 0 and 1 are derived from J by k_plan.  One
 // read of the keys.
+// Presorted check as a sweep of its own (joint-histogram sizes): order[0] |= some adjacent pair
+// out of the requested order, order[1] |= some pair out of the opposite order (OrderFlags).  Warps
+// publish a flag as soon as they see it and stop once both flags are set anywhere, so an unsorted
+// input costs each warp about one vector (microseconds), while a presorted, reversed or
+// all-equal input -- the cases where the result is decided here -- is read once, and the
+// histogram sweep then returns at once (k_onesweep_hist_joint, prechecked).
+template <int KIND, bool DESC, typename U>
+__global__ void __launch_bounds__(HIST_THREADS) k_order_check(const U* __restrict__ keys, uint64_t n,
+                                                              uint32_t* __restrict__ order) {
+  constexpr int PER_VEC = 16 / sizeof(U);
+  OrderFlags of;
+  const uint64_t T = (uint64_t)gridDim.x * HIST_THREADS;
+  const uint64_t gt = (uint64_t)blockIdx.x * HIST_THREADS + threadIdx.x;
+  const uint32_t lane = threadIdx.x & 31;
+  const uint64_t head = min64(n, ((16 - ((uintptr_t)keys & 15)) & 15) / sizeof(U));
+  for (uint64_t j = gt; j < head; j += T)
+    if (j + 1 < n) of.pair(key_encode<KIND, DESC>(keys[j]), key_encode<KIND, DESC>(keys[j + 1]));
+  const uint4* v = reinterpret_cast<const uint4*>(keys + head);
+  const uint64_t nv = (n - head) / PER_VEC;
+  auto check_vec = [&](uint4 q, uint64_t i) {
+    if constexpr (sizeof(U) == 4) {
+      const U kv[4] = {U(q.x), U(q.y), U(q.z), U(q.w)};
+      of.vector<KIND, DESC>(kv, head + i * PER_VEC, keys, n);
+    } else {
+      const U kv[2] = {U(q.x) | (U(q.y) << 32), U(q.z) | (U(q.w) << 32)};
+      of.vector<KIND, DESC>(kv, head + i * PER_VEC, keys, n);
+    }
+  };
+  // round 0, the whole CTA: one vector per thread, one flag publication per CTA.  An unsorted
+  // input ends here (every CTA meets both violations in its first vectors).
+  if (gt < nv) check_vec(__ldcs(v + gt), gt);
+  {
+    const int u = __syncthreads_or(of.up), d = __syncthreads_or(of.down);
+    if (threadIdx.x == 0) {
+      if (u) atomicOr(&order[0], 1u);
+      if (d) atomicOr(&order[1], 1u);
+    }
+    if (u && d) return;
+    of.up = u;  // a flag the CTA has published needs no further checking
+    of.down = d;
+  }
+  const volatile uint32_t* vo = order;
+  uint32_t told = (of.up ? 1u : 0u) | (of.down ? 2u : 0u);  // flags already published
+  uint32_t polled = 0;  // lane 0: global flags read at the previous poll (not waited on)
+  auto publish = [&]() -> bool {  // whole warp; true once both flags are set globally
+    const uint32_t f = __reduce_or_sync(0xffffffffu, (of.up ? 1u : 0u) | (of.down ? 2u : 0u));
+    uint32_t both = 0;
+    if (lane == 0) {
+      if ((f & 1u) && !(told & 1u)) atomicOr(&order[0], 1u);
+      if ((f & 2u) && !(told & 2u)) atomicOr(&order[1], 1u);
+      both = polled;
+      polled = vo[0] & vo[1];
+    }
+    told |= f;
+    return __shfl_sync(0xffffffffu, both, 0) != 0u;
+  };
+  // later rounds: four vectors per thread in flight; warp-uniform bounds (collectives inside).
+  // Whole warps hold 32 consecutive vectors: the key after a lane's vector is the next lane's
+  // first key (shuffle), and lane 31's is loaded with the vectors (no dependent load later).
+  const uint64_t wbase = gt - lane;
+  auto check_full = [&](uint4 q, U nxt) {
+    U e[PER_VEC];
+    if constexpr (sizeof(U) == 4) {
+      e[0] = U(q.x); e[1] = U(q.y); e[2] = U(q.z); e[3] = U(q.w);
+    } else {
+      e[0] = U(q.x) | (U(q.y) << 32); e[1] = U(q.z) | (U(q.w) << 32);
+    }
+    const U nb = OrderFlags::shfl_down_u(0xffffffffu, e[0]);
+#pragma unroll
+    for (int j = 0; j < PER_VEC; ++j) e[j] = key_encode<KIND, DESC>(e[j]);
+#pragma unroll
+    for (int j = 0; j + 1 < PER_VEC; ++j) of.pair(e[j], e[j + 1]);
+    of.pair(e[PER_VEC - 1], key_encode<KIND, DESC>(lane < 31 ? nb : nxt));
+  };
+  uint64_t r = T;
+  for (uint32_t round = 0; wbase + r + 3 * T + 32 < nv; r += 4 * T, ++round) {
+    const uint64_t i = gt + r;
+    const uint4 q0 = __ldcs(v + i), q1 = __ldcs(v + i + T), q2 = __ldcs(v + i + 2 * T), q3 = __ldcs(v + i + 3 * T);
+    U x0 = 0, x1 = 0, x2 = 0, x3 = 0;  // lane 31: the key after its vector (inside the array)
+    if (lane == 31) {
+      const U* kb = keys + head + (i + 1) * PER_VEC;
+      x0 = kb[0];
+      x1 = kb[T * PER_VEC];
+      x2 = kb[2 * T * PER_VEC];
+      x3 = kb[3 * T * PER_VEC];
+    }
+    check_full(q0, x0);
+    check_full(q1, x1);
+    check_full(q2, x2);
+    check_full(q3, x3);
+    if ((round & 3u) == 3u && publish()) return;
+  }
+  for (; wbase + r < nv; r += T) {
+    const uint64_t i = gt + r;
+    if (i < nv) check_vec(__ldcs(v + i), i);
+  }
+  for (uint64_t j = head + nv * PER_VEC + gt; j < n; j += T)
+    if (j + 1 < n) of.pair(key_encode<KIND, DESC>(keys[j]), key_encode<KIND, DESC>(keys[j + 1]));
+  publish();
+}
+
 template <int KIND, bool DESC, typename U, int LANES>
 __global__ void __launch_bounds__(HIST_THREADS, 1)
     k_onesweep_hist_joint(const U* __restrict__ keys, uint64_t n, unsigned long long* __restrict__ ghist,
-                          unsigned long long* __restrict__ gjoint, uint32_t* __restrict__ order = nullptr) {
+                          unsigned long long* __restrict__ gjoint, uint32_t* __restrict__ order = nullptr,
+                          bool prechecked = false) {
   constexpr int P = sizeof(U);
   OrderFlags of;
+  if (prechecked) {
+    // k_order_check ran first: a presorted (or reversed) input needs no histogram -- no pass
+    // runs -- and otherwise both violations are known, so this sweep checks no pairs
+    if (__ldcg(&order[0]) == 0 || __ldcg(&order[1]) == 0) return;
+    of.up = of.down = 1;
+  }
   auto check1 = [&](uint64_t j, U kj) {
     if (j + 1 < n) of.pair(kj, key_encode<KIND, DESC>(ldg_nc(keys + j + 1)));
   };
@@ -451,7 +561,8 @@ __global__ void __launch_bounds__(HIST_THREADS, 1)
 static __global__ void __launch_bounds__(256)
     k_plan_joint(const unsigned long long* __restrict__ gjoint, const unsigned long long* __restrict__ ghist,
                  const unsigned long long* __restrict__ bases1, uint64_t tile, PassPlan* __restrict__ plan,
-                 unsigned long long* __restrict__ seg, uint64_t run2_tile = 0) {
+                 unsigned long long* __restrict__ seg, uint64_t run2_tile = 0, uint64_t fewruns_tile = 0,
+                 uint64_t fewruns_n = 0) {
   const uint32_t t = threadIdx.x;
   // RUN2 for pass 2 (pass2.cuh): its input is sorted by the low 16 bits, whose runs are the joint
   // bins; a tile meets at most two of them when every nonzero bin is at least a tile long
@@ -462,6 +573,19 @@ static __global__ void __launch_bounds__(256)
   }
   const int run2 = __syncthreads_and(ok2);
   if (t == 0) plan->run2 = (uint32_t)run2 && !plan->skip[2];
+  // Few distinct lower-bit values (fewruns_tile > 0, 32-bit keys): pass 2's input is sorted by
+  // the low 16 bits, whose distinct values are the nonzero joint bins (nz16); pass 3's by the
+  // low 24 bits, at most nz16 x (nonzero digit-2 bins) distinct values.  When the average run is
+  // at least 4 tiles, almost every tile meets at most two runs, and the run-ranking kernel (one
+  // unstable atomic per key, per-tile fallback to the stable ranking) beats the lane-ordered
+  // stable pass, whose same-word atomics serialize on few distinct digits (cfg4 16-distinct).
+  if (fewruns_tile > 0) {  // nz16 was counted by k_plan (plan->pad[0])
+    const uint32_t nz2 = (uint32_t)__syncthreads_count(ghist[512 + t] != 0);
+    if (t == 0) {
+      const unsigned long long r2 = plan->pad[0], r3 = r2 * nz2, lim = fewruns_n / (4 * fewruns_tile);
+      plan->fewruns = (r2 <= lim ? 4u : 0u) | (r3 <= lim ? 8u : 0u);
+    }
+  }
   const unsigned long long c0 = ghist[t];  // digit-0 marginal
   const int eligible = __syncthreads_and(c0 == 0 || c0 >= tile);
   if (t == 0) plan->j01 = (uint32_t)eligible && !plan->skip[1];
@@ -523,6 +647,7 @@ __device__ __forceinline__ void plan_body(const unsigned long long* ghist, uint6
     plan->executed = executed;
     plan->j01 = 0;  // k_plan_joint (if launched) may enable the look-back-free pass 1
     plan->run2 = 0;  // ... and pass 2 ranked by runs (pass2.cuh R2_RUN2)
+    plan->fewruns = 0;  // ... and passes 2-3 of 32-bit keys ranked by runs (k_onesweep_pass_ws)
     plan->reverse = 0;
     const bool in_order = order != nullptr && __ldcg(&order[0]) == 0;
     const bool reversed = order != nullptr && !in_order && __ldcg(&order[1]) == 0;
@@ -555,11 +680,21 @@ static __global__ void __launch_bounds__(256)
       const ulonglong2 q = row[a];
       r += q.x + q.y;
     }
+    uint32_t nz = 0;  // nonzero joint bins = distinct low-16-bit values (k_plan_joint's fewruns)
 #pragma unroll 8
-    for (int b = 0; b < 256; ++b) c += gjoint[b * 256 + threadIdx.x];
+    for (int b = 0; b < 256; ++b) {
+      const unsigned long long v = gjoint[b * 256 + threadIdx.x];
+      c += v;
+      nz += v != 0;
+    }
     ghist[threadIdx.x] = c;
     ghist[256 + threadIdx.x] = r;
+    __shared__ uint32_t nz_s;
+    if (threadIdx.x == 0) nz_s = 0;
     __syncthreads();
+    atomicAdd(&nz_s, nz);
+    __syncthreads();
+    if (threadIdx.x == 0) plan->pad[0] = nz_s;
   }
   plan_body<256>(ghist, n, P, bases, plan, tile_counters, gcount, order);
 }

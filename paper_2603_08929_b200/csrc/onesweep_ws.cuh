@@ -79,7 +79,8 @@ __global__ void __launch_bounds__(RT + 256, MINB)
     k_onesweep_pass_ws(const U* a_ptr, U* b_ptr, uint64_t n, DigitF digit,
                        const unsigned long long* __restrict__ bases, DescT* __restrict__ lookback,
                        uint32_t* __restrict__ tile_counter, uint32_t num_tiles, const PassPlan* __restrict__ plan,
-                       int pass, KvPtrs kvp = {}, unsigned long long* __restrict__ gcount = nullptr) {
+                       int pass, KvPtrs kvp = {}, unsigned long long* __restrict__ gcount = nullptr,
+                       uint32_t only_fewruns = 0) {
   static_assert(MODE == RANK_RUN2 || MODE == RANK_STABLE || MODE == RANK_UNSTABLE, "no J01");
   constexpr bool LOOKBACK = MODE != RANK_UNSTABLE;
   static_assert(RT >= 256 && RT % 32 == 0, "at least one ranker per digit");
@@ -113,6 +114,8 @@ __global__ void __launch_bounds__(RT + 256, MINB)
     if constexpr (MODE == RANK_RUN2) {
       if (pass == 1 && plan->j01) return;  // the J01 launch of this pass runs instead
     }
+    // launched as the few-runs alternative of a k_pass2 launch: works only when the plan says so
+    if (only_fewruns && !((plan->fewruns >> pass) & 1u)) return;
     if (plan->src_alt[pass]) {
       src = b_ptr;
       dst = const_cast<U*>(a_ptr);

@@ -227,6 +227,9 @@ constexpr uint32_t P2_RAW = 4;
 // P2_SKEWVAR: one of a pair of STABLE launches for the same pass; the HALVES = 2 kernel works when
 // the plan marks the pass's digit skewed, the HALVES = 1 kernel otherwise
 constexpr uint32_t P2_SKEWVAR = 8;
+// P2_FEWALT: a run-ranking launch (k_onesweep_pass_ws, only_fewruns) follows for the same pass; this
+// launch does no work when the plan marks the pass's input as having few distinct lower bits
+constexpr uint32_t P2_FEWALT = 16;
 
 // MODE R2_STABLE: look-back pass; with CHUNKED the chains of `cm`, else one chain over tiles of
 //   TILE keys (gcount unused).
@@ -289,6 +292,7 @@ __global__ void __launch_bounds__(RT + WT, 1)
       if (pass == 2 && plan->run2) return;
       if (flags & P2_SKEWVAR)
         if ((((plan->skew >> pass) & 1u) != 0) != (HALVES == 2)) return;
+      if ((flags & P2_FEWALT) && ((plan->fewruns >> pass) & 1u)) return;
     }
     if (plan->src_alt[pass]) {
       src = b_ptr;

@@ -418,3 +418,28 @@ def test_presorted_one_swap_interior(B, dtype, n, desc):
             b.sort_(x, descending=desc)
             torch.cuda.synchronize()
             assert bool((x == want).all()), f"{name} at {p} (n={n}, desc={desc})"
+
+
+@pytest.mark.parametrize("dtype", [torch.int32, torch.float32, torch.uint32], ids=lambda d: str(d).split(".")[-1])
+def test_few_runs_passes(B, dtype):
+    """Few distinct keys at joint-histogram sizes: the plan routes LSD passes 2-3 of 32-bit keys to
+    the run-ranking look-back kernel (PassPlan::fewruns) instead of the lane-ordered k_pass2.
+    Cases: 16 distinct values (every tile meets <= 2 runs), 300 distinct values of which 10 are
+    rare (tiles around a rare value meet > 2 runs: per-tile fallback to the stable ranking), and
+    a misaligned pointer (no TMA: k_pass2 alone)."""
+    n = (1 << 24) + 4099
+    idx = W.bits(n, 41, "cuda")
+    table = sview(gen(dtype, 300, 42))
+    y = table[((idx >> 60) & 15)].view(dtype)
+    check_equal(B, y.clone(), False, "16 distinct asc")
+    check_equal(B, y.clone(), True, "16 distinct desc")
+    k = ((idx >> 33) & 0x7FFFFFFF) % 290
+    pos = torch.arange(n, device="cuda")
+    rare = pos % 100003 == 5
+    k = torch.where(rare, 290 + (pos // 100003) % 10, k)
+    z = table[k].view(dtype)
+    check_equal(B, z.clone(), False, "290 common + 10 rare")
+    check_equal(B, z.clone(), True, "290 common + 10 rare desc")
+    buf = torch.empty(n + 1, dtype=dtype, device="cuda")
+    buf[1:] = y
+    check_equal(B, buf[1:], False, "16 distinct misaligned")

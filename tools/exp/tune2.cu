@@ -277,12 +277,27 @@ int main(int argc, char** argv) {
   k_fill_cfg3<<<1184, 256>>>(B.in, B.n, 42);
   CK(cudaDeviceSynchronize());
   const bool exact = logn <= 24;
+  // realistic inputs of passes 2 and 3: encoded keys sorted by the low 16 / 24 bits
+  uint32_t* m2;
+  uint32_t* m3;
+  CK(cudaMalloc(&m2, B.n * 4));
+  CK(cudaMalloc(&m3, B.n * 4));
   run<0, 512, 256, 20, R2_UNSTABLE, false, 2>("unstable_d0_enc", B, exact, B.in, P2_ENC);
   CK(cudaMemcpy(B.mid, B.out, B.n * 4, cudaMemcpyDeviceToDevice));
   run<8, 512, 256, 18, R2_J01, false, 2>("j01_512_18", B, exact, B.mid, 0);
-  run<8, 640, 256, 14, R2_J01, false, 2>("j01_640_14", B, exact, B.mid, 0);
-  run<8, 384, 256, 24, R2_J01, false, 2>("j01_384_24", B, exact, B.mid, 0);
-  run<0, 384, 256, 24, R2_UNSTABLE, false, 2>("u_384_256_24", B, exact, B.in, 0);
-  run<8, 640, 256, 16, R2_STABLE, true, 2>("s_640_256_16", B, exact, B.mid, 0);
+  CK(cudaMemcpy(m2, B.out, B.n * 4, cudaMemcpyDeviceToDevice));
+  run<16, 640, 256, 16, R2_STABLE, false, 2>("p2_stable_640_16", B, exact, m2, 0);
+  CK(cudaMemcpy(m3, B.out, B.n * 4, cudaMemcpyDeviceToDevice));
+  run<16, 512, 384, 20, R2_STABLE, false, 2>("p2_512_384_20", B, exact, m2, 0);
+  run<16, 512, 384, 20, R2_STABLE, false, 1>("p2_512_384_20_lbv1", B, exact, m2, 0);
+  run<16, 512, 512, 20, R2_STABLE, false, 1>("p2_512_512_20_lbv1", B, exact, m2, 0);
+  run<16, 640, 384, 16, R2_STABLE, false, 1>("p2_640_384_16_lbv1", B, exact, m2, 0);
+  run<16, 640, 256, 16, R2_STABLE, false, 1>("p2_640_256_16_lbv1", B, exact, m2, 0);
+  run<16, 768, 256, 12, R2_STABLE, false, 1>("p2_768_256_12_lbv1", B, exact, m2, 0);
+  run<16, 512, 256, 20, R2_STABLE, false, 1>("p2_512_256_20_lbv1", B, exact, m2, 0);
+  run<24, 640, 256, 16, R2_STABLE, false, 2>("p3_stable_640_16", B, exact, m3, P2_DEC);
+  run<24, 640, 256, 16, R2_STABLE, false, 1>("p3_640_256_16_lbv1", B, exact, m3, P2_DEC);
+  run<24, 512, 384, 20, R2_STABLE, false, 1>("p3_512_384_20_lbv1", B, exact, m3, P2_DEC);
+  run<24, 640, 384, 16, R2_STABLE, false, 1>("p3_640_384_16_lbv1", B, exact, m3, P2_DEC);
   return 0;
 }
