@@ -94,7 +94,11 @@ LsdLayout lsd_layout(uint64_t n, bool kv = false) {
   l.bases = off;    off = align_up(off + P * 256 * 8, 256);
   l.gcount = off;   off = align_up(off + P * 256 * 8, 256);
   const size_t jbytes = n >= JOINT_MIN_N ? 65536 * 8 : 0;  // joint histogram + segment starts
-  l.joint = off;    off = align_up(off + jbytes, 256);
+  // + the coarse joints of passes 2-3 and their chunk maps (32-bit keys; LB_NC)
+  const size_t cbytes = n >= JOINT_MIN_N ? 2 * LB_NC * 256 * 8 + 2 * (LB_NC + 1) * 8 + 2 * (LB_NC + 1) * 4 +
+                                               2 * LB_NC * 256 * 4 + 64
+                                         : 0;
+  l.joint = off;    off = align_up(off + jbytes + cbytes, 256);
   l.seg = off;      off = align_up(off + jbytes, 256);
   l.plan = off;     off = align_up(off + sizeof(PassPlan), 256);
   l.counters = off; off = align_up(off + 16 * 4, 256);
@@ -225,23 +229,25 @@ inline bool p2_enabled() {
   }();
   return on;
 }
-template <int KIND, bool DESC, int SHIFT, int MODE = R2_STABLE, int HALVES = 1, typename U>
+template <int KIND, bool DESC, int SHIFT, int MODE = R2_STABLE, int HALVES = 1, bool CHUNKED = false, typename U>
 bsort_status_t launch_pass2(const U* a, U* b, uint64_t n, const unsigned long long* bases, uint32_t* lookback,
-                            uint32_t* counter, const PassPlan* plan, int pass, cudaStream_t s, uint32_t xflags = 0) {
+                            uint32_t* counter, const PassPlan* plan, int pass, cudaStream_t s, uint32_t xflags = 0,
+                            ChunkMap cm = {}) {
   using C = std::conditional_t<HALVES == 2, P2SkewCfg, P2Cfg<MODE>>;
   using L = Pass2Smem<C::RT, C::WT, C::ITEMS, U, MODE, HALVES>;
-  auto kern = k_pass2<U, KIND, DESC, SHIFT, C::RT, C::WT, C::ITEMS, MODE, false, 2, HALVES>;
+  auto kern = k_pass2<U, KIND, DESC, SHIFT, C::RT, C::WT, C::ITEMS, MODE, CHUNKED, 2, HALVES>;
   static DeviceOnce attr;  // per instantiation and device
   if (attr.pending()) {
     BSORT_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L::bytes));
     attr.mark();
   }
-  const uint64_t tiles = (n + L::TILE - 1) / L::TILE;
+  // chunked: at most one partial tile per chunk more (the kernel stops at the map's tile count)
+  const uint64_t tiles = (n + L::TILE - 1) / L::TILE + (CHUNKED ? cm.nc : 0);
   const uint64_t grid = min64(tiles, (uint64_t)num_sms());  // one CTA per SM, all resident
   BSORT_LAUNCH(PROF_PASS, s,
                kern<<<(unsigned)grid, C::RT + C::WT, L::bytes, s>>>(
                    a, b, n, bases, lookback, nullptr, counter, (uint32_t)tiles, plan, pass,
-                   P2_RAW | P2_ENC | P2_DEC | xflags, ChunkMap{}));
+                   P2_RAW | P2_ENC | P2_DEC | xflags, cm));
   return BSORT_SUCCESS;
 }
 
@@ -263,6 +269,11 @@ bsort_status_t lsd_run(U* keys, uint32_t* vals, uint64_t n, unsigned char* ws, c
   auto* bases = reinterpret_cast<unsigned long long*>(ws + l.bases);
   auto* gcount = reinterpret_cast<unsigned long long*>(ws + l.gcount);
   auto* joint = reinterpret_cast<unsigned long long*>(ws + l.joint);
+  // coarse joints of passes 2-3 and their chunk maps, after the joint histogram (lsd_layout)
+  auto* gcoarse = joint + 65536;
+  auto* cstart = gcoarse + 2 * LB_NC * 256;
+  auto* ctile = reinterpret_cast<uint32_t*>(cstart + 2 * (LB_NC + 1));
+  auto* cjp = ctile + 2 * (LB_NC + 1);
   auto* seg = reinterpret_cast<unsigned long long*>(ws + l.seg);
   auto* plan = reinterpret_cast<PassPlan*>(ws + l.plan);
   auto* counters = reinterpret_cast<uint32_t*>(ws + l.counters);
@@ -282,23 +293,31 @@ bsort_status_t lsd_run(U* keys, uint32_t* vals, uint64_t n, unsigned char* ws, c
   // finds few distinct lower-bit values (k_plan_joint's fewruns; both launched, one works)
   const bool few_alt = sizeof(U) == 4 && !KV && use_joint && n >= WS_MIN_N && n <= P2_MAX_N && p2_enabled() &&
                        ws_enabled() && (uintptr_t)keys % 16 == 0;
+  // passes 2-3 of 32-bit keys with LB_NC look-back chains (the histogram sweep counted the coarse
+  // joints); BSORT_P2_CHUNKED=0 turns it off (A/B)
+  static const bool chunk_on = [] {
+    const char* e = getenv("BSORT_P2_CHUNKED");
+    return !(e && e[0] == '0');
+  }();
+  const bool chunked = sizeof(U) == 4 && !KV && use_joint && n <= P2_MAX_N && chunk_on;
   // digit histograms and, right after them, the presorted-input flags (k_onesweep_hist*)
   auto* order = reinterpret_cast<uint32_t*>(ghist + P * 256);
   BSORT_LAUNCH(PROF_MEMSET, s, cudaMemsetAsync(ghist, 0, P * 256 * 8 + 16, s));
   if (use_joint) {
     constexpr int JL = sizeof(U) == 4 ? 32 : 16;  // lanes of the digit >= 2 counters (224 KB for u64)
     auto hk = k_onesweep_hist_joint<KIND, DESC, U, JL>;
-    constexpr int hsmem = (32768 + (P - 2) * 256 * JL) * 4;
+    constexpr int hsmem = hist_joint_words<P, JL>() * 4;
     static DeviceOnce hattr;
     if (hattr.pending()) {
       BSORT_CUDA(cudaFuncSetAttribute(hk, cudaFuncAttributeMaxDynamicSharedMemorySize, hsmem));
       hattr.mark();
     }
-    BSORT_LAUNCH(PROF_MEMSET, s, cudaMemsetAsync(joint, 0, 65536 * 8, s));
+    BSORT_LAUNCH(PROF_MEMSET, s, cudaMemsetAsync(joint, 0, (65536 + 2 * LB_NC * 256) * 8, s));
     // presorted check first (stops early on unsorted input); the histogram sweep then checks no
     // pairs, and does nothing for a presorted / reversed input
     BSORT_LAUNCH(PROF_HIST, s, k_order_check<KIND, DESC, U><<<num_sms(), HIST_THREADS, 0, s>>>(keys, n, order));
-    BSORT_LAUNCH(PROF_HIST, s, hk<<<num_sms(), HIST_THREADS, hsmem, s>>>(keys, n, ghist, joint, order, true));
+    BSORT_LAUNCH(PROF_HIST, s,
+                 hk<<<num_sms(), HIST_THREADS, hsmem, s>>>(keys, n, ghist, joint, order, true, gcoarse));
   } else {
     // the histogram kernel's last CTA also plans (no k_plan launch)
     auto hk = k_onesweep_hist<KIND, DESC, U, LANES, true>;
@@ -321,7 +340,10 @@ bsort_status_t lsd_run(U* keys, uint32_t* vals, uint64_t n, unsigned char* ws, c
                                                     ? p2_tile<R2_RUN2>()
                                                     : 0,
                                                 few_alt ? (uint64_t)WsCfg<U, false>::RT * WsCfg<U, false>::ITEMS : 0,
-                                                n));
+                                                n,
+                                                chunked ? ChunkPlanArgs{bases, gcoarse, cstart, ctile, cjp,
+                                                                        p2_tile<R2_STABLE>(), n}
+                                                        : ChunkPlanArgs{}));
   bsort_status_t st = BSORT_SUCCESS;
   const bool fold = n < WS_MIN_N;  // look-back zeroing folded into the pass kernels
   auto one_pass = [&](auto shift_c) {
@@ -366,9 +388,18 @@ bsort_status_t lsd_run(U* keys, uint32_t* vals, uint64_t n, unsigned char* ws, c
           // (half-warp counter rows for skewed top digits, k_pass2<..., HALVES = 2> with
           // P2_SKEWVAR, measured no faster on cfg3's sign+exponent digit: 3.98 vs 3.92 ms)
           const bool alt = few_alt && p >= 2;
-          st = launch_pass2<KIND, DESC, SH>(keys, scratch, n, bases + p * 256,
-                                            reinterpret_cast<uint32_t*>(lookback), counters + p, plan, p, s,
-                                            alt ? P2_FEWALT : 0u);
+          if (chunked && p == 2) {
+            const int q = p - 2;
+            const ChunkMap cm{nullptr, cstart + q * (LB_NC + 1), ctile + q * (LB_NC + 1), cjp + q * LB_NC * 256,
+                              (uint32_t)LB_NC};
+            st = launch_pass2<KIND, DESC, SH, R2_STABLE, 1, true>(keys, scratch, n, bases + p * 256,
+                                                                  reinterpret_cast<uint32_t*>(lookback), counters + p,
+                                                                  plan, p, s, alt ? P2_FEWALT : 0u, cm);
+          } else {
+            st = launch_pass2<KIND, DESC, SH>(keys, scratch, n, bases + p * 256,
+                                              reinterpret_cast<uint32_t*>(lookback), counters + p, plan, p, s,
+                                              alt ? P2_FEWALT : 0u);
+          }
           if (st == BSORT_SUCCESS && alt)
             st = launch_pass_ws<U, DescT, false, RANK_RUN2>(keys, scratch, n, RadixDigit<KIND, DESC, U, SH>{},
                                                             bases + p * 256, lookback, counters + p, plan, p, s,

@@ -54,10 +54,59 @@ constexpr int P2_NC = 32;  // look-back chains (chunks) of a chunked stable pass
 // Chunk map of a stable pass (device arrays written by the plan kernel).
 struct ChunkMap {
   const uint32_t* disp;              // dispatch order: disp[t] = chunk << 24 | tile within chunk
-  const unsigned long long* cstart;  // [P2_NC + 1] chunk starts (keys)
-  const uint32_t* ctile;             // [P2_NC + 1] linear id of each chunk's first tile
-  const uint32_t* jp;                // [P2_NC][256] global start of (chunk, digit)
+                                     // (nullptr: round-robin over the nc chunks, computed on the fly)
+  const unsigned long long* cstart;  // [nc + 1] chunk starts (keys)
+  const uint32_t* ctile;             // [nc + 1] linear id of each chunk's first tile
+  const uint32_t* jp;                // [nc][256] global start of (chunk, digit)
+  uint32_t nc;                       // chunks (<= P2_NC; disp == nullptr needs nc <= 8)
 };
+
+// Round-robin dispatch without a table: tiles are handed out k-major (tile k of every chunk that
+// has one, in chunk order, then tile k + 1 ...).  Between consecutive distinct chunk tile counts
+// the set of chunks still dispatching is fixed, so dispatch ids split into at most nc segments of
+// slope m (the number of such chunks): ChunkRR holds them, built once per CTA by one thread.
+struct ChunkRR {
+  unsigned long long cstart[9];  // the map's chunk starts and first tiles (shared-memory copies)
+  uint32_t ctile[9];
+  uint32_t kstart[8], idstart[9], m[8], nseg;
+  uint8_t act[8][8];             // chunks still dispatching in segment j, in chunk order
+};
+__device__ __forceinline__ void chunk_rr_build(const ChunkMap& cm, ChunkRR* r) {
+  uint32_t nt[8];
+  for (uint32_t c = 0; c <= cm.nc && c < 9; ++c) {
+    r->cstart[c] = cm.cstart[c];
+    r->ctile[c] = cm.ctile[c];
+  }
+  for (uint32_t c = 0; c < 8; ++c) nt[c] = c < cm.nc ? r->ctile[c + 1] - r->ctile[c] : 0u;
+  uint32_t k0 = 0, id0 = 0, j = 0;
+  for (; j < 8; ++j) {
+    uint32_t m = 0, next = 0xFFFFFFFFu;
+    for (uint32_t c = 0; c < 8; ++c)
+      if (nt[c] > k0) {
+        r->act[j][m++] = (uint8_t)c;
+        next = min(next, nt[c]);
+      }
+    if (m == 0) break;
+    r->kstart[j] = k0;
+    r->idstart[j] = id0;
+    r->m[j] = m;
+    id0 += (next - k0) * m;
+    k0 = next;
+  }
+  r->idstart[j] = id0;
+  r->nseg = j;
+}
+// false past the last tile
+__device__ __forceinline__ bool chunk_rr(const ChunkRR* r, uint32_t id, uint32_t& chunk, uint32_t& k) {
+  const uint32_t ns = r->nseg;
+  uint32_t j = 0;
+  while (j < ns && id >= r->idstart[j + 1]) ++j;
+  if (j >= ns) return false;
+  const uint32_t off = id - r->idstart[j], m = r->m[j];
+  k = r->kstart[j] + off / m;
+  chunk = r->act[j][off % m];
+  return true;
+}
 
 // Vectorised look-back descriptors (u32 = {2-bit flag | 30-bit count}, LookbackBits<uint32_t>):
 // (linear tile q, digit d) lives at lb[((q >> 2) * 256 + d) * 4 + (q & 3)].
@@ -213,7 +262,8 @@ struct Pass2Smem {
   static constexpr size_t mbar_off = align_up(wt_off + 4 * (RW + 1), 16);     // u64[2]
   static constexpr size_t islot_off = mbar_off + 16;                          // SlotInfo[2] input
   static constexpr size_t sslot_off = islot_off + 64;                         // SlotInfo[2] staged
-  static constexpr size_t bytes = align_up(sslot_off + 64, 128);
+  static constexpr size_t rr_off = sslot_off + 64;  // ChunkRR (round-robin chunk dispatch)
+  static constexpr size_t bytes = align_up(rr_off + sizeof(ChunkRR), 128);
 };
 
 // named barriers: 0 = __syncthreads; R = rankers; W = writers; per staging slot s:
@@ -276,6 +326,7 @@ __global__ void __launch_bounds__(RT + WT, 1)
   uint64_t* mbar = reinterpret_cast<uint64_t*>(smem + L::mbar_off);
   volatile SlotInfo* islot = reinterpret_cast<volatile SlotInfo*>(smem + L::islot_off);
   volatile SlotInfo* sslot = reinterpret_cast<volatile SlotInfo*>(smem + L::sslot_off);
+  ChunkRR* rr = reinterpret_cast<ChunkRR*>(smem + L::rr_off);  // thread 0 only
   const uint32_t smem_base = smem_u32(smem);
 
   const U* src = a_ptr;
@@ -315,13 +366,27 @@ __global__ void __launch_bounds__(RT + WT, 1)
     uint32_t lin, len, chunk = 0, first;
     unsigned long long start;
     if constexpr (CHUNKED) {
-      const uint32_t v = cm.disp[id];
-      chunk = v >> 24;
-      const uint32_t k = v & 0xFFFFFFu;
-      const unsigned long long cs = cm.cstart[chunk], ce = cm.cstart[chunk + 1];
+      uint32_t k = 0;
+      unsigned long long cs, ce;
+      if (cm.disp != nullptr) {
+        const uint32_t v = cm.disp[id];
+        chunk = v >> 24;
+        k = v & 0xFFFFFFu;
+        cs = cm.cstart[chunk];
+        ce = cm.cstart[chunk + 1];
+        lin = cm.ctile[chunk] + k;
+      } else {
+        if (!chunk_rr(rr, id, chunk, k)) {
+          islot[b].lin = P2_END;
+          mbar_arrive(&mbar[b]);
+          return;
+        }
+        cs = rr->cstart[chunk];
+        ce = rr->cstart[chunk + 1];
+        lin = rr->ctile[chunk] + k;
+      }
       start = cs + (unsigned long long)k * TILE;
       len = (uint32_t)min64((uint64_t)TILE, ce - start);
-      lin = cm.ctile[chunk] + k;
       first = k == 0;
     } else {
       lin = id;
@@ -346,6 +411,9 @@ __global__ void __launch_bounds__(RT + WT, 1)
               &mbar[b]);
   };
   if (t == 0) {
+    if constexpr (CHUNKED) {
+      if (cm.disp == nullptr) chunk_rr_build(cm, rr);
+    }
     for (int b = 0; b < 2; ++b) mbar_init(&mbar[b], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     for (int b = 0; b < 2; ++b) refill(b);

@@ -443,3 +443,31 @@ def test_few_runs_passes(B, dtype):
     buf = torch.empty(n + 1, dtype=dtype, device="cuda")
     buf[1:] = y
     check_equal(B, buf[1:], False, "16 distinct misaligned")
+
+
+@pytest.mark.parametrize("dtype", [torch.uint32, torch.int32, torch.float32], ids=lambda d: str(d).split(".")[-1])
+def test_chunked_lookback_passes(B, dtype):
+    """LSD pass 2 of 32-bit keys at joint-histogram sizes runs as LB_NC = 4 look-back chains
+    (chunks = top two bits of digit 1; chunk map from the histogram sweep's coarse joint,
+    round-robin dispatch by segment table).  Edge cases: every key in one chunk (others empty),
+    a trivial digit 1 (pass 1 skipped: pass 2's chunks follow digit 1 anyway), chunks of very
+    different sizes (tile counts 1 vs ~1,600: segments of slope 4 then 1), both directions,
+    ragged n."""
+    n = (1 << 24) + 12345
+    r = W.bits(n, 51, "cuda")
+    lo = r & 0xFFFFFFFF
+
+    def as_dtype(v):
+        v = v & 0xFFFFFFFF
+        v = torch.where(v >= (1 << 31), v - (1 << 32), v).to(torch.int32)
+        return v.view(dtype)
+
+    if dtype == torch.float32:
+        lo = lo & ~(0xFF << 23) | (0x7E << 23)  # finite, both signs (exponent fixed, sign random)
+    one = (lo & ~(3 << 14)) | (3 << 22)         # pass 2: all in chunk 0
+    triv = (lo & ~(0xFF << 8)) | (0x5A << 8)    # digit 1 trivial
+    skew = torch.where((r >> 40) % 100 == 0, lo, lo & ~(3 << 14))  # chunk 0 ~99%, others ~0.3%
+    for v, what in ((lo, "random"), (one, "single chunks"), (triv, "trivial digit 1"), (skew, "skewed chunks")):
+        x = as_dtype(v)
+        check_equal(B, x.clone(), False, what)
+        check_equal(B, x.clone(), True, what + " desc")

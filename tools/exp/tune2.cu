@@ -104,7 +104,12 @@ struct HostPlan {
   std::vector<uint32_t> ctile, jp, disp;
   uint32_t tiles;
 };
-HostPlan make_plan(const std::vector<unsigned long long>& jc, uint64_t tile) {
+int g_merge = 1;  // chunks = 32 / g_merge (coarser chains)
+bool g_rr = false;  // dispatch by chunk_rr (no table)
+HostPlan make_plan(const std::vector<unsigned long long>& jc_in, uint64_t tile) {
+  std::vector<unsigned long long> jc(32 * 256, 0);
+  for (int g = 0; g < 32; ++g)
+    for (int d = 0; d < 256; ++d) jc[(g / g_merge) * 256 + d] += jc_in[g * 256 + d];
   HostPlan P;
   P.bases.assign(256, 0);
   std::vector<unsigned long long> marg(256, 0), grp(32, 0);
@@ -165,7 +170,7 @@ void run(const char* tag, Bufs& B, bool exact_check, const uint32_t* in, uint32_
   CK(cudaMemcpy(B.ctile, P.ctile.data(), 33 * 4, cudaMemcpyHostToDevice));
   CK(cudaMemcpy(B.jp, P.jp.data(), 32 * 256 * 4, cudaMemcpyHostToDevice));
   CK(cudaMemcpy(B.disp, P.disp.data(), P.disp.size() * 4, cudaMemcpyHostToDevice));
-  ChunkMap cm{B.disp, B.cstart, B.ctile, B.jp};
+  ChunkMap cm{g_rr ? nullptr : B.disp, B.cstart, B.ctile, B.jp, (uint32_t)(32 / g_merge)};
   const uint32_t tiles = CHUNKED ? P.tiles : (uint32_t)((n + LTILE - 1) / LTILE);
   const unsigned grid = (unsigned)std::min<uint64_t>(tiles, 148 * (V3 ? V3 : 1));
   CK(cudaMemset(B.res, 0, 16));
@@ -288,16 +293,12 @@ int main(int argc, char** argv) {
   CK(cudaMemcpy(m2, B.out, B.n * 4, cudaMemcpyDeviceToDevice));
   run<16, 640, 256, 16, R2_STABLE, false, 2>("p2_stable_640_16", B, exact, m2, 0);
   CK(cudaMemcpy(m3, B.out, B.n * 4, cudaMemcpyDeviceToDevice));
-  run<16, 512, 384, 20, R2_STABLE, false, 2>("p2_512_384_20", B, exact, m2, 0);
-  run<16, 512, 384, 20, R2_STABLE, false, 1>("p2_512_384_20_lbv1", B, exact, m2, 0);
-  run<16, 512, 512, 20, R2_STABLE, false, 1>("p2_512_512_20_lbv1", B, exact, m2, 0);
-  run<16, 640, 384, 16, R2_STABLE, false, 1>("p2_640_384_16_lbv1", B, exact, m2, 0);
-  run<16, 640, 256, 16, R2_STABLE, false, 1>("p2_640_256_16_lbv1", B, exact, m2, 0);
-  run<16, 768, 256, 12, R2_STABLE, false, 1>("p2_768_256_12_lbv1", B, exact, m2, 0);
-  run<16, 512, 256, 20, R2_STABLE, false, 1>("p2_512_256_20_lbv1", B, exact, m2, 0);
-  run<24, 640, 256, 16, R2_STABLE, false, 2>("p3_stable_640_16", B, exact, m3, P2_DEC);
-  run<24, 640, 256, 16, R2_STABLE, false, 1>("p3_640_256_16_lbv1", B, exact, m3, P2_DEC);
-  run<24, 512, 384, 20, R2_STABLE, false, 1>("p3_512_384_20_lbv1", B, exact, m3, P2_DEC);
-  run<24, 640, 384, 16, R2_STABLE, false, 1>("p3_640_384_16_lbv1", B, exact, m3, P2_DEC);
+  g_merge = 8;
+  run<16, 640, 256, 16, R2_STABLE, true, 2>("p2_chunked4_disp", B, exact, m2, 0);
+  g_rr = true;
+  run<16, 640, 256, 16, R2_STABLE, true, 2>("p2_chunked4_rr", B, exact, m2, 0);
+  run<24, 640, 256, 16, R2_STABLE, true, 2>("p3_chunked4_rr", B, exact, m3, P2_DEC);
+  g_rr = false;
+  run<24, 640, 256, 16, R2_STABLE, true, 2>("p3_chunked4_disp", B, exact, m3, P2_DEC);
   return 0;
 }
