@@ -388,7 +388,7 @@ bsort_status_t lsd_run(U* keys, uint32_t* vals, uint64_t n, unsigned char* ws, c
           // (half-warp counter rows for skewed top digits, k_pass2<..., HALVES = 2> with
           // P2_SKEWVAR, measured no faster on cfg3's sign+exponent digit: 3.98 vs 3.92 ms)
           const bool alt = few_alt && p >= 2;
-          if (chunked && p == 2) {
+          if (chunked && p >= 2) {
             const int q = p - 2;
             const ChunkMap cm{nullptr, cstart + q * (LB_NC + 1), ctile + q * (LB_NC + 1), cjp + q * LB_NC * 256,
                               (uint32_t)LB_NC};

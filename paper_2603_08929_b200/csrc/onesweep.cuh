@@ -430,12 +430,15 @@ constexpr int LB_NC = 4;
 // coarse-joint shared counters [256 digits][LB_NC chunks][CJ_LANES lane banks]: lanes l and l + 16
 // share a bank only when their chunks have equal parity
 constexpr int CJ_LANES = 16;
+// pass 3's coarse joint (digit 3, digit 2 >> 6): 8 lane banks (the 16-bank pass-2 table and the
+// 65,536-bin joint fill the rest of the 227 KB)
+constexpr int CJ3_LANES = 8;
 
 // shared words of k_onesweep_hist_joint: 65,536 u16 joint bins + digit counters (32-bit keys:
 // digit 3 lane-banked + the pass-2 coarse joint; 64-bit keys: digits 2-7 with LANES banks)
 template <int P, int LANES>
 __host__ __device__ constexpr int hist_joint_words() {
-  return 32768 + (P == 4 ? 256 * 32 + 256 * LB_NC * CJ_LANES : (P - 2) * 256 * LANES);
+  return 32768 + (P == 4 ? 256 * LB_NC * (CJ3_LANES + CJ_LANES) : (P - 2) * 256 * LANES);
 }
 
 template <int KIND, bool DESC, typename U, int LANES>
@@ -444,8 +447,8 @@ __global__ void __launch_bounds__(HIST_THREADS, 1)
                           unsigned long long* __restrict__ gjoint, uint32_t* __restrict__ order = nullptr,
                           bool prechecked = false, unsigned long long* __restrict__ gcoarse = nullptr) {
   constexpr int P = sizeof(U);
-  // 32-bit keys: digit 2 counted as the coarse joint of pass 2 (LB_NC): 256 x 4 x 16 words after
-  // the lane-banked digit-3 counters (the launch sizes shared memory by hist_joint_smem)
+  // 32-bit keys: digits 2 and 3 counted as the coarse joints of passes 2 and 3 (LB_NC; the launch
+  // sizes shared memory by hist_joint_words)
   constexpr bool COARSE = P == 4;
   static_assert(!COARSE || LANES == 32, "digit-3 counters lane-banked");
   OrderFlags of;
@@ -476,10 +479,10 @@ __global__ void __launch_bounds__(HIST_THREADS, 1)
   auto add_high = [&](U k) {
     if constexpr (COARSE) {
       const uint32_t x = uint32_t(k);
-      // digit 3 lane-banked (conflict-free); (digit 2, digit 1 >> 6) = bits 14-23 of the key, as
-      // index digit * LB_NC + chunk
-      atomicAdd(&hd[(x >> 24) * 32 + lane], 1u);
-      atomicAdd(&hd[256 * 32 + ((x >> 14) & 0x3FFu) * CJ_LANES + (lane & (CJ_LANES - 1))], 1u);
+      // (digit 3, digit 2 >> 6) = bits 22-31 and (digit 2, digit 1 >> 6) = bits 14-23 of the key,
+      // as index digit * LB_NC + chunk
+      atomicAdd(&hd[(x >> 22) * CJ3_LANES + (lane & (CJ3_LANES - 1))], 1u);
+      atomicAdd(&hd[256 * LB_NC * CJ3_LANES + ((x >> 14) & 0x3FFu) * CJ_LANES + (lane & (CJ_LANES - 1))], 1u);
     } else {
 #pragma unroll
       for (int p = 2; p < P; ++p) {
@@ -577,14 +580,18 @@ __global__ void __launch_bounds__(HIST_THREADS, 1)
   }
   if constexpr (COARSE) {
     static_assert(LB_NC == 4, "shared index digit * 4 + chunk");
-    for (int b = threadIdx.x; b < 256; b += HIST_THREADS) {  // digit 3
+    // coarse joints to gcoarse[pass - 2][chunk][digit]; their marginals are digits 2 and 3
+    for (int b = threadIdx.x; b < LB_NC * 256; b += HIST_THREADS) {  // pass 3
       uint32_t s = 0;
-#pragma unroll 8
-      for (int l = 0; l < 32; ++l) s += hd[b * 32 + ((l + b) & 31)];
-      if (s) atomicAdd(&ghist[768 + b], (unsigned long long)s);
+#pragma unroll
+      for (int l = 0; l < CJ3_LANES; ++l) s += hd[b * CJ3_LANES + ((l + b) & (CJ3_LANES - 1))];
+      if (s) {
+        const int d = b >> 2, c = b & 3;
+        atomicAdd(&gcoarse[(LB_NC + c) * 256 + d], (unsigned long long)s);
+        atomicAdd(&ghist[768 + d], (unsigned long long)s);
+      }
     }
-    // coarse joint to gcoarse[chunk][digit]; its marginal is digit 2
-    const uint32_t* hc = hd + 256 * 32;
+    const uint32_t* hc = hd + 256 * LB_NC * CJ3_LANES;  // pass 2
     for (int b = threadIdx.x; b < LB_NC * 256; b += HIST_THREADS) {
       uint32_t s = 0;
 #pragma unroll
@@ -630,7 +637,7 @@ static __global__ void __launch_bounds__(256)
                  uint64_t fewruns_n = 0, ChunkPlanArgs cp = {}) {
   const uint32_t t = threadIdx.x;
   if (cp.jp != nullptr) {
-    for (int q = 0; q < 1; ++q) {  // pass 2 (index q = pass - 2)
+    for (int q = 0; q < 2; ++q) {  // passes 2 and 3 (index q = pass - 2)
       unsigned long long run = cp.bases[(2 + q) * 256 + t];
       for (int c = 0; c < LB_NC; ++c) {
         cp.jp[(q * LB_NC + c) * 256 + t] = (uint32_t)run;
