@@ -201,7 +201,7 @@ bsort_status_t launch_pass_ws(const U* a, U* b, uint64_t n, DigitF digit, const 
 // (tools/exp/tune2.cu: 3.45 ms per 2^30-key pass on cfg3 vs 3.65 / 4.16 ms for round 1's RUN2 /
 // stable passes).  Needs n <= 2^30 (30-bit look-back counts).
 template <int MODE> struct P2Cfg {
-  static constexpr int RT = 640, WT = 256, ITEMS = 16;
+  static constexpr int RT = 512, WT = 256, ITEMS = 20;  // chunked passes 2 / 3: 2.97 -> 2.91 / 3.44 -> 3.37 ms vs 640 x 16
 };
 // RUN2 holds two lane-banked tables (counts, offsets): 8192-key tiles
 template <> struct P2Cfg<R2_RUN2> {
@@ -342,7 +342,8 @@ bsort_status_t lsd_run(U* keys, uint32_t* vals, uint64_t n, unsigned char* ws, c
                                                 few_alt ? (uint64_t)WsCfg<U, false>::RT * WsCfg<U, false>::ITEMS : 0,
                                                 n,
                                                 chunked ? ChunkPlanArgs{bases, gcoarse, cstart, ctile, cjp,
-                                                                        p2_tile<R2_STABLE>(), n}
+                                                                        p2_tile<R2_STABLE>(), n,
+                                                                        (uint64_t)P2SkewCfg::RT * P2SkewCfg::ITEMS}
                                                         : ChunkPlanArgs{}));
   bsort_status_t st = BSORT_SUCCESS;
   const bool fold = n < WS_MIN_N;  // look-back zeroing folded into the pass kernels
@@ -392,9 +393,17 @@ bsort_status_t lsd_run(U* keys, uint32_t* vals, uint64_t n, unsigned char* ws, c
             const int q = p - 2;
             const ChunkMap cm{nullptr, cstart + q * (LB_NC + 1), ctile + q * (LB_NC + 1), cjp + q * LB_NC * 256,
                               (uint32_t)LB_NC};
+            // skewed digit (plan->skew: one bin > n/8, e.g. cfg3's sign + exponent byte): half-warp
+            // counter rows halve same-word atomic serialization (chunked pass 3: 3.44 -> 3.30 ms);
+            // both launched, the plan's skew bit lets one work (its tile size is in the chunk map)
+            const uint32_t xf = (alt ? P2_FEWALT : 0u) | P2_SKEWVAR;
             st = launch_pass2<KIND, DESC, SH, R2_STABLE, 1, true>(keys, scratch, n, bases + p * 256,
                                                                   reinterpret_cast<uint32_t*>(lookback), counters + p,
-                                                                  plan, p, s, alt ? P2_FEWALT : 0u, cm);
+                                                                  plan, p, s, xf, cm);
+            if (st == BSORT_SUCCESS)
+              st = launch_pass2<KIND, DESC, SH, R2_STABLE, 2, true>(keys, scratch, n, bases + p * 256,
+                                                                    reinterpret_cast<uint32_t*>(lookback),
+                                                                    counters + p, plan, p, s, xf, cm);
           } else {
             st = launch_pass2<KIND, DESC, SH>(keys, scratch, n, bases + p * 256,
                                               reinterpret_cast<uint32_t*>(lookback), counters + p, plan, p, s,

@@ -628,6 +628,7 @@ struct ChunkPlanArgs {
   uint32_t* ctile;                    // [2][LB_NC + 1]
   uint32_t* jp;                       // [2][LB_NC][256]
   uint64_t tile, n;                   // nullptr jp: no chunked passes
+  uint64_t tile_skew;                 // tile of the half-warp-row kernel (passes whose digit is skewed)
 };
 
 static __global__ void __launch_bounds__(256)
@@ -649,7 +650,9 @@ static __global__ void __launch_bounds__(256)
         for (int c = 0; c < LB_NC; ++c) cs[c] = cp.bases[(1 + q) * 256 + 64 * c];
         cs[LB_NC] = cp.n;
         ct[0] = 0;
-        for (int c = 0; c < LB_NC; ++c) ct[c + 1] = ct[c] + (uint32_t)((cs[c + 1] - cs[c] + cp.tile - 1) / cp.tile);
+        // the pass runs k_pass2's half-warp-row variant when its digit is skewed (k_plan's skew bit)
+        const uint64_t tl = ((plan->skew >> (2 + q)) & 1u) ? cp.tile_skew : cp.tile;
+        for (int c = 0; c < LB_NC; ++c) ct[c + 1] = ct[c] + (uint32_t)((cs[c + 1] - cs[c] + tl - 1) / tl);
       }
     }
   }

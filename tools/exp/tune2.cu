@@ -138,10 +138,10 @@ HostPlan make_plan(const std::vector<unsigned long long>& jc_in, uint64_t tile) 
   return P;
 }
 
-template <int SHIFT, int RT, int WT, int ITEMS, int MODE, bool CHUNKED, int LBV, int V3 = 0>
+template <int SHIFT, int RT, int WT, int ITEMS, int MODE, bool CHUNKED, int LBV, int V3 = 0, int HALVES = 1>
 void run(const char* tag, Bufs& B, bool exact_check, const uint32_t* in, uint32_t flags) {
   // V3 > 0: k_pass3 with RT threads, V3 CTAs per SM (WT unused)
-  using L2 = Pass2Smem<RT, (WT > 0 ? WT : 256), ITEMS, uint32_t, MODE>;
+  using L2 = Pass2Smem<RT, (WT > 0 ? WT : 256), ITEMS, uint32_t, MODE, HALVES>;
   using L3 = Pass3Smem<RT, ITEMS, uint32_t, MODE>;
   constexpr int LTILE = V3 ? L3::TILE : L2::TILE;
   constexpr size_t LBYTES = V3 ? L3::bytes : L2::bytes;
@@ -151,7 +151,7 @@ void run(const char* tag, Bufs& B, bool exact_check, const uint32_t* in, uint32_
   if constexpr (V3 > 0)
     kern = k_pass3<uint32_t, KIND_F, false, SHIFT, RT, ITEMS, MODE, CHUNKED, LBV, (V3 > 0 ? V3 : 1)>;
   else
-    kern = k_pass2<uint32_t, KIND_F, false, SHIFT, RT, WT, ITEMS, MODE, CHUNKED, LBV>;
+    kern = k_pass2<uint32_t, KIND_F, false, SHIFT, RT, WT, ITEMS, MODE, CHUNKED, LBV, HALVES>;
   const int nthreads = V3 ? RT : RT + WT;
   CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)LBYTES));
   cudaFuncAttributes fa;
@@ -294,11 +294,18 @@ int main(int argc, char** argv) {
   run<16, 640, 256, 16, R2_STABLE, false, 2>("p2_stable_640_16", B, exact, m2, 0);
   CK(cudaMemcpy(m3, B.out, B.n * 4, cudaMemcpyDeviceToDevice));
   g_merge = 8;
-  run<16, 640, 256, 16, R2_STABLE, true, 2>("p2_chunked4_disp", B, exact, m2, 0);
   g_rr = true;
   run<16, 640, 256, 16, R2_STABLE, true, 2>("p2_chunked4_rr", B, exact, m2, 0);
   run<24, 640, 256, 16, R2_STABLE, true, 2>("p3_chunked4_rr", B, exact, m3, P2_DEC);
+  run<24, 640, 256, 15, R2_STABLE, true, 2, 0, 2>("p3_chunked4_rr_halves", B, exact, m3, P2_DEC);
+  run<24, 640, 256, 15, R2_STABLE, true, 2, 0, 1>("p3_chunked4_rr_15", B, exact, m3, P2_DEC);
+  run<24, 512, 256, 20, R2_STABLE, true, 2, 0, 1>("p3_chunked4_rr_512x20", B, exact, m3, P2_DEC);
+  run<16, 512, 256, 20, R2_STABLE, true, 2, 0, 1>("p2_chunked4_rr_512x20", B, exact, m2, 0);
+  run<16, 640, 256, 16, R2_STABLE, true, 1, 0, 1>("p2_chunked4_rr_lbv1", B, exact, m2, 0);
+  run<24, 640, 256, 16, R2_STABLE, true, 1, 0, 1>("p3_chunked4_rr_lbv1", B, exact, m3, P2_DEC);
+  g_merge = 4;
+  run<24, 640, 256, 16, R2_STABLE, true, 2>("p3_chunked8_rr", B, exact, m3, P2_DEC);
+  g_merge = 1;
   g_rr = false;
-  run<24, 640, 256, 16, R2_STABLE, true, 2>("p3_chunked4_disp", B, exact, m3, P2_DEC);
   return 0;
 }
