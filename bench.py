@@ -254,7 +254,7 @@ def bench_single(args, B):
                          "steps outside the timed events", "parallelism": "single GPU"},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
                      "frac": achieved / hbm_peak, "traffic": load_traffic("onesweep_pass"),
-                     "kernel": "LSD scatter pass (k_onesweep_pass; k_onesweep_pass_ws for look-back passes)",
+                     "kernel": "LSD scatter pass (k_onesweep_pass for passes 0-1; k_pass2 chunked look-back for passes 2-3)",
                      "algorithmic_bytes_per_launch": pass_bytes,
                      "avg_launch_ms": pass_ms, "working_launches_per_step": 4,
                      "launches_per_step": pk["launches"] / len(ptimes), "peak_source": peak_src,
