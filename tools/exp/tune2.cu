@@ -295,16 +295,9 @@ int main(int argc, char** argv) {
   CK(cudaMemcpy(m3, B.out, B.n * 4, cudaMemcpyDeviceToDevice));
   g_merge = 8;
   g_rr = true;
-  run<16, 640, 256, 16, R2_STABLE, true, 2>("p2_chunked4_rr", B, exact, m2, 0);
-  run<24, 640, 256, 16, R2_STABLE, true, 2>("p3_chunked4_rr", B, exact, m3, P2_DEC);
-  run<24, 640, 256, 15, R2_STABLE, true, 2, 0, 2>("p3_chunked4_rr_halves", B, exact, m3, P2_DEC);
-  run<24, 640, 256, 15, R2_STABLE, true, 2, 0, 1>("p3_chunked4_rr_15", B, exact, m3, P2_DEC);
-  run<24, 512, 256, 20, R2_STABLE, true, 2, 0, 1>("p3_chunked4_rr_512x20", B, exact, m3, P2_DEC);
-  run<16, 512, 256, 20, R2_STABLE, true, 2, 0, 1>("p2_chunked4_rr_512x20", B, exact, m2, 0);
-  run<16, 640, 256, 16, R2_STABLE, true, 1, 0, 1>("p2_chunked4_rr_lbv1", B, exact, m2, 0);
-  run<24, 640, 256, 16, R2_STABLE, true, 1, 0, 1>("p3_chunked4_rr_lbv1", B, exact, m3, P2_DEC);
-  g_merge = 4;
-  run<24, 640, 256, 16, R2_STABLE, true, 2>("p3_chunked8_rr", B, exact, m3, P2_DEC);
+  run<16, 512, 256, 20, R2_STABLE, true, 2>("p2_chunked4_512x20", B, exact, m2, 0);
+  run<24, 640, 256, 15, R2_STABLE, true, 2, 0, 2>("p3_chunked4_halves", B, exact, m3, P2_DEC);
+  run<16, 640, 256, 16, R2_STABLE, true, 2>("p2_chunked4_640x16", B, exact, m2, 0);
   g_merge = 1;
   g_rr = false;
   return 0;
