@@ -209,3 +209,54 @@ print("ok")
     r = subprocess.run([sys.executable, "-c", code], env=dict(os.environ, BSORT_GRAPH="0"), capture_output=True,
                        text=True, timeout=600, cwd=REPO)
     assert r.returncode == 0 and "ok" in r.stdout, r.stderr[-2000:]
+
+
+@pytest.mark.parametrize("dtype", [torch.int32, torch.float32, torch.uint32], ids=lambda d: str(d).split(".")[-1])
+@pytest.mark.parametrize("desc", [False, True], ids=["asc", "desc"])
+def test_grid_msd_fast_path_and_fallback(B, dtype, desc):
+    """k_grid_sort's MSD-first path (32-bit keys): one grid pass on the top digit, then every
+    bucket sorted in one CTA's shared memory.  Cases: uniform keys (256 buckets of ~4K keys), a
+    top byte confined to 48 values (buckets of ~21K, some above one CTA's capacity: the LSD
+    fallback), 40 values over 700K keys (buckets of ~17K, below capacity: uneven bucket loads),
+    a constant top byte (the MSD pass moves nothing; one bucket of all keys: fallback), and a
+    5% heavy top byte (one bucket of ~52K keys: fallback)."""
+    n = (1 << 20) + 3
+    r = W.bits(n, 61, "cuda")
+    lo = r & 0xFFFFFF
+
+    def mk(top, m=n):
+        v = ((top[:m] << 24) | lo[:m]) & 0xFFFFFFFF
+        v = torch.where(v >= (1 << 31), v - (1 << 32), v).to(torch.int32)
+        return v.view(dtype)
+
+    tb = (r >> 40) & 255
+    cases = [(mk(tb), "uniform"), (mk(0x30 + (r >> 40) % 48), "48 top values"),
+             (mk(0x41 + (r >> 40) % 40, 700_001), "40 top values, 700K keys"),
+             (mk(torch.full_like(tb, 0x3C)), "constant top byte"),
+             (mk(torch.where((r >> 50) % 20 == 0, torch.full_like(tb, 0x3D), tb)), "5% heavy top byte")]
+    for x, what in cases:
+        check(B, x.clone(), desc, what)
+
+
+def test_grid_lsd_only_at_grid_sizes():
+    """BSORT_GRID_MSD=0: k_grid_sort's plain LSD passes (the MSD path's fallback) at grid sizes."""
+    _subprocess_sorts({"BSORT_GRID_MSD": "0"}, [(torch.int32, 300_007), (torch.float32, (1 << 20) + 3),
+                                                 (torch.uint32, 50_001)], expect_launches=1)
+
+
+def test_grid_msd_single_bucket_in_place():
+    """BSORT_SMALL_MAX=1000: a 20,000-key grid sort whose top digit is constant -- the MSD pass
+    moves nothing and its one bucket (all keys, still in the caller's buffer) fits one CTA."""
+    code = r"""
+import sys; sys.path.insert(0, %r)
+import numpy as np, torch, oracle, workloads as W, paper_2603_08929_b200 as B
+x = (W.uniform_int(torch.int32, 20000, 3, "cuda") & 0x00FFFFFF) | 0x15000000
+for desc in (False, True):
+    ref = oracle.sort_native(x.cpu().numpy(), descending=desc)
+    y = x.clone(); B.sort_(y, descending=desc); torch.cuda.synchronize()
+    assert y.cpu().numpy().tobytes() == ref.tobytes(), desc
+print("ok")
+""" % REPO
+    r = subprocess.run([sys.executable, "-c", code], env=dict(os.environ, BSORT_SMALL_MAX="1000"),
+                       capture_output=True, text=True, timeout=600, cwd=REPO)
+    assert r.returncode == 0 and "ok" in r.stdout, r.stderr[-2000:]
