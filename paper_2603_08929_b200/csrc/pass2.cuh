@@ -50,6 +50,9 @@ enum Rank2 : int { R2_STABLE = 0, R2_UNSTABLE = 1, R2_J01 = 2, R2_RUN2 = 3 };
 // ranking by (digit, run of the lower bits) in lane-banked tables: J01 and RUN2
 constexpr bool p2_runs(int mode) { return mode == R2_J01 || mode == R2_RUN2; }
 constexpr int P2_NC = 32;  // look-back chains (chunks) of a chunked stable pass
+#ifndef P2_SCAN1
+#define P2_SCAN1 1  // stable passes: one-barrier digit scan (scan256_1bar)
+#endif
 
 // Chunk map of a stable pass (device arrays written by the plan kernel).
 struct ChunkMap {
@@ -184,6 +187,22 @@ __device__ __forceinline__ uint32_t p2_digit(U k) {
     return uint32_t(uint64_t(k) >> SHIFT) & 0xFFu;
   else
     return (uint32_t(k) >> SHIFT) & 0xFFu;
+}
+
+// Exclusive scan over the first 256 threads of a named-barrier group of NT threads (the others
+// pass 0): ONE barrier -- every warp adds the totals of the warps before it itself (at most 7
+// broadcast loads) instead of waiting for warp 0 to scan them behind a second barrier.  The
+// totals array is rewritten only after the group's next barriers.
+template <int NT, uint32_t BAR>
+__device__ __forceinline__ uint32_t scan256_1bar(uint32_t v, uint32_t* warp_tot) {
+  const uint32_t lane = lane_id(), warp = threadIdx.x >> 5;
+  const uint32_t inc = warp_inclusive_scan(v);
+  if (lane == 31 && warp < 8) warp_tot[warp] = inc;
+  named_bar_sync(BAR, NT);
+  uint32_t base = 0;
+  if (warp < 8)
+    for (uint32_t w = 0; w < warp; ++w) base += warp_tot[w];
+  return base + inc - v;
 }
 
 // Exclusive prefix of linear tile T for digit d: fold predecessors T-1, T-2, ... (aggregates)
@@ -544,7 +563,8 @@ __global__ void __launch_bounds__(RT + WT, 1)
             meta[s * 256 + t].y = tot;
           }
           named_bar_arrive(P2_BAR_COUNTED + s, RT + WT);  // writers may start the look-back
-          const uint32_t excl = group_exclusive_scan<RT, P2_BAR_R>(t < 256 ? tot : 0u, wt);
+          const uint32_t excl = P2_SCAN1 ? scan256_1bar<RT, P2_BAR_R>(t < 256 ? tot : 0u, wt)
+                                         : group_exclusive_scan<RT, P2_BAR_R>(t < 256 ? tot : 0u, wt);
           if (t < 256) {
             uint32_t run = sbuf_a + (excl << KS);
 #pragma unroll
