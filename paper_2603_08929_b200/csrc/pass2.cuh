@@ -316,8 +316,8 @@ constexpr uint32_t P2_FEWALT = 16;
 // Keys: digit SHIFT/8 of the encoded key; n < 2^32 (32-bit offsets), n <= 2^30 for R2_STABLE
 // (30-bit look-back counts).
 template <typename U, int KIND, bool DESC, int SHIFT, int RT, int WT, int ITEMS, int MODE, bool CHUNKED = false,
-          int LBV = 2, int HALVES = 1>
-__global__ void __launch_bounds__(RT + WT, 1)
+          int LBV = 2, int HALVES = 1, int MINB = 1>
+__global__ void __launch_bounds__(RT + WT, MINB)
     k_pass2(const U* a_ptr, U* b_ptr, uint64_t n, const unsigned long long* __restrict__ bases,
             uint32_t* __restrict__ lookback, unsigned long long* __restrict__ gcount,
             uint32_t* __restrict__ tile_counter, uint32_t num_tiles, const PassPlan* __restrict__ plan, int pass,

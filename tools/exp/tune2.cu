@@ -138,7 +138,7 @@ HostPlan make_plan(const std::vector<unsigned long long>& jc_in, uint64_t tile) 
   return P;
 }
 
-template <int SHIFT, int RT, int WT, int ITEMS, int MODE, bool CHUNKED, int LBV, int V3 = 0, int HALVES = 1>
+template <int SHIFT, int RT, int WT, int ITEMS, int MODE, bool CHUNKED, int LBV, int V3 = 0, int HALVES = 1, int P2MB = 1>
 void run(const char* tag, Bufs& B, bool exact_check, const uint32_t* in, uint32_t flags) {
   // V3 > 0: k_pass3 with RT threads, V3 CTAs per SM (WT unused)
   using L2 = Pass2Smem<RT, (WT > 0 ? WT : 256), ITEMS, uint32_t, MODE, HALVES>;
@@ -151,7 +151,7 @@ void run(const char* tag, Bufs& B, bool exact_check, const uint32_t* in, uint32_
   if constexpr (V3 > 0)
     kern = k_pass3<uint32_t, KIND_F, false, SHIFT, RT, ITEMS, MODE, CHUNKED, LBV, (V3 > 0 ? V3 : 1)>;
   else
-    kern = k_pass2<uint32_t, KIND_F, false, SHIFT, RT, WT, ITEMS, MODE, CHUNKED, LBV, HALVES>;
+    kern = k_pass2<uint32_t, KIND_F, false, SHIFT, RT, WT, ITEMS, MODE, CHUNKED, LBV, HALVES, P2MB>;
   const int nthreads = V3 ? RT : RT + WT;
   CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)LBYTES));
   cudaFuncAttributes fa;
@@ -172,7 +172,7 @@ void run(const char* tag, Bufs& B, bool exact_check, const uint32_t* in, uint32_
   CK(cudaMemcpy(B.disp, P.disp.data(), P.disp.size() * 4, cudaMemcpyHostToDevice));
   ChunkMap cm{g_rr ? nullptr : B.disp, B.cstart, B.ctile, B.jp, (uint32_t)(32 / g_merge)};
   const uint32_t tiles = CHUNKED ? P.tiles : (uint32_t)((n + LTILE - 1) / LTILE);
-  const unsigned grid = (unsigned)std::min<uint64_t>(tiles, 148 * (V3 ? V3 : 1));
+  const unsigned grid = (unsigned)std::min<uint64_t>(tiles, 148 * (V3 ? V3 : P2MB));
   CK(cudaMemset(B.res, 0, 16));
   k_check<<<296, 512>>>(in, n, SHIFT, enc_in, B.res);
   unsigned long long ref[2];
@@ -296,8 +296,11 @@ int main(int argc, char** argv) {
   g_merge = 8;
   g_rr = true;
   run<16, 512, 256, 20, R2_STABLE, true, 2>("p2_chunked4_512x20", B, exact, m2, 0);
+  run<16, 256, 256, 20, R2_STABLE, true, 2, 0, 1, 2>("p2_ch4_256x20_2cta", B, exact, m2, 0);
+  run<16, 256, 256, 16, R2_STABLE, true, 2, 0, 1, 2>("p2_ch4_256x16_2cta", B, exact, m2, 0);
+  run<16, 384, 256, 12, R2_STABLE, true, 2, 0, 1, 2>("p2_ch4_384x12_2cta", B, exact, m2, 0);
   run<24, 640, 256, 15, R2_STABLE, true, 2, 0, 2>("p3_chunked4_halves", B, exact, m3, P2_DEC);
-  run<16, 640, 256, 16, R2_STABLE, true, 2>("p2_chunked4_640x16", B, exact, m2, 0);
+  run<24, 256, 256, 21, R2_STABLE, true, 2, 0, 2, 2>("p3_ch4_256x21_h2_2cta", B, exact, m3, P2_DEC);
   g_merge = 1;
   g_rr = false;
   return 0;
