@@ -331,8 +331,11 @@ bsort_status_t lsd_run(U* keys, uint32_t* vals, uint64_t n, unsigned char* ws, c
                  hk<<<num_sms(), HIST_THREADS, hsmem, s>>>(keys, n, ghist, order,
                                                            PlanArgs{bases, plan, counters, gcount}));
   }
-  if (use_joint)
-    BSORT_LAUNCH(PROF_SCAN, s, k_plan<<<1, 256, 0, s>>>(ghist, n, P, bases, plan, counters, gcount, joint, order));
+  if (use_joint) {
+    // marginals, nonzero-bin count (order[2]) and J01's relative segment starts: 256 CTAs
+    BSORT_LAUNCH(PROF_SCAN, s, k_joint_marg<<<256, 256, 0, s>>>(joint, ghist, seg, order + 2));
+    BSORT_LAUNCH(PROF_SCAN, s, k_plan<<<1, 256, 0, s>>>(ghist, n, P, bases, plan, counters, gcount, nullptr, order));
+  }
   if (use_joint)
     BSORT_LAUNCH(PROF_SCAN, s,
                  k_plan_joint<<<1, 256, 0, s>>>(joint, ghist, bases + 256, J01_TILE, plan, seg,

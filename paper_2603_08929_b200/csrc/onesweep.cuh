@@ -612,6 +612,29 @@ __global__ void __launch_bounds__(HIST_THREADS, 1)
   }
 }
 
+// Marginals and row prefixes of the joint (digit 1, digit 0) histogram, one CTA per digit-1 value
+// a (256 CTAs x 256 threads; thread b = digit-0 value), instead of one CTA reading all 65,536
+// bins twice: the digit-1 marginal ghist[256 + a], the digit-0 marginal ghist[b] (atomics; the
+// histogram region is zeroed before the sweep), the number of nonzero bins (*nz, zeroed with it)
+// and J01's segment starts relative to digit a's base, seg[b * 256 + a] = sum_{b' < b} J[a][b']
+// (the J01 pass adds the base).
+static __global__ void __launch_bounds__(256)
+    k_joint_marg(const unsigned long long* __restrict__ gjoint, unsigned long long* __restrict__ ghist,
+                 unsigned long long* __restrict__ seg, uint32_t* __restrict__ nz) {
+  __shared__ unsigned long long wt[256 / 32 + 1];
+  const uint32_t a = blockIdx.x, b = threadIdx.x;
+  const unsigned long long v = gjoint[a * 256 + b];
+  unsigned long long total = 0;
+  const unsigned long long ex = block_exclusive_scan<256>(v, wt, &total);
+  seg[b * 256 + a] = ex;
+  if (v) atomicAdd(&ghist[b], v);
+  const int c = __syncthreads_count(v != 0);
+  if (b == 0) {
+    ghist[256 + a] = total;
+    if (c) atomicAdd(nz, (uint32_t)c);
+  }
+}
+
 // Joint plan for RANK_J01 (one CTA of 256 threads, after k_plan): pass 1 may skip the look-back
 // when every nonzero digit-0 bucket holds at least `tile` keys -- then any tile-sized window of
 // the pass-0 output meets at most two digit-0 runs.  Segment (d1 = a, d0 = b) of the pass-1
@@ -681,16 +704,9 @@ static __global__ void __launch_bounds__(256)
   const unsigned long long c0 = ghist[t];  // digit-0 marginal
   const int eligible = __syncthreads_and(c0 == 0 || c0 >= tile);
   if (t == 0) plan->j01 = (uint32_t)eligible && !plan->skip[1];
-  if (!eligible) return;
-  unsigned long long run = bases1[t];
-  const ulonglong2* row = reinterpret_cast<const ulonglong2*>(gjoint + t * 256);  // row a = t
-  for (int b = 0; b < 128; ++b) {
-    const ulonglong2 q = row[b];
-    seg[(2 * b) * 256 + t] = run;
-    run += q.x;
-    seg[(2 * b + 1) * 256 + t] = run;
-    run += q.y;
-  }
+  (void)eligible;  // the segment starts (relative to digit 1's bases) are k_joint_marg's
+  (void)seg;
+  (void)bases1;
 }
 
 // Plan: exclusive scan of every digit histogram into global digit bases, trivial-digit
@@ -789,6 +805,8 @@ static __global__ void __launch_bounds__(256)
     if (threadIdx.x == 0) plan->pad[0] = nz_s;
   }
   plan_body<256>(ghist, n, P, bases, plan, tile_counters, gcount, order);
+  // k_joint_marg counted the nonzero joint bins into order[2] (k_plan_joint's fewruns)
+  if (gjoint == nullptr && order != nullptr && threadIdx.x == 0) plan->pad[0] = __ldcg(&order[2]);
 }
 
 // ---------------------------------------------------------------------------------------
@@ -1245,8 +1263,8 @@ __global__ void __launch_bounds__(THREADS, MINB)
         }
         gofs[t] = bases[t] + (unsigned long long)excl - tile_excl;
       } else if constexpr (MODE == RANK_J01) {
-        gofs[t] = jg0 - tile_excl;
-        gofs[256 + t] = jg1 - (tile_excl + c0);
+        gofs[t] = bases[t] + jg0 - tile_excl;  // seg holds starts relative to digit t's base
+        gofs[256 + t] = bases[t] + jg1 - (tile_excl + c0);
       } else {
         if constexpr (DigitF::REMOTE)  // byte address of element 0 of this tile's run for t
           gofs[t] = t < 256u && total ? digit.dst_base[t < (uint32_t)BSORT_DIST_MAX_RANKS ? t : 0] +
