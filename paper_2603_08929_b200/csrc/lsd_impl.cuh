@@ -60,6 +60,8 @@ template <typename U> constexpr int hist_lanes() { return sizeof(U) == 4 ? 32 : 
 struct LsdLayout {
   size_t scratch, vscratch, ghist, bases, gcount, joint, seg, plan, counters, lookback, total;
   size_t lb_bytes;    // one look-back region
+  int lb_regions;     // 2 below WS_MIN_N (alternating), 3 for 32-bit keys-only joint sorts (passes
+                      // 1-3 each their own, zeroed by the histogram sweep), else 1 (memset per pass)
   size_t grid;        // k_grid_sort (small_grid.cuh): per-pass count matrix + barrier word
   uint64_t lb_tiles;  // look-back descriptor rows: tiles of the smallest look-back tile in use
 };
@@ -105,7 +107,8 @@ LsdLayout lsd_layout(uint64_t n, bool kv = false) {
   // below WS_MIN_N two look-back regions alternate by pass parity (each pass kernel zeroes the
   // next pass's region: no memset launches, lsd_run)
   l.lb_bytes = align_up(tiles * 256 * desc, 256);
-  l.lookback = off; off += (n < WS_MIN_N ? 2 : 1) * l.lb_bytes;
+  l.lb_regions = n < WS_MIN_N ? 2 : ((sizeof(U) == 4 && !kv && n >= JOINT_MIN_N) ? 3 : 1);
+  l.lookback = off; off += l.lb_regions * l.lb_bytes;
   l.grid = off;     off = align_up(off + grid_detail::workspace_bytes(), 256);  // k_grid_sort counts
   l.lb_tiles = tiles;
   l.total = off;
@@ -289,6 +292,9 @@ bsort_status_t lsd_run(U* keys, uint32_t* vals, uint64_t n, unsigned char* ws, c
 
   static const bool joint_off = getenv("BSORT_NO_JOINT") != nullptr;  // A/B and debugging
   const bool use_joint = n >= JOINT_MIN_N && !joint_off;
+  // passes 1-3 of 32-bit keys-only joint sorts use three look-back regions that the histogram
+  // sweep zeroes (no memset launch per pass)
+  const bool tri = use_joint && l.lb_regions == 3;
   // passes 2-3 of 32-bit keys: k_pass2, or the run-ranking warp-specialised kernel when the plan
   // finds few distinct lower-bit values (k_plan_joint's fewruns; both launched, one works)
   const bool few_alt = sizeof(U) == 4 && !KV && use_joint && n >= WS_MIN_N && n <= P2_MAX_N && p2_enabled() &&
@@ -317,7 +323,9 @@ bsort_status_t lsd_run(U* keys, uint32_t* vals, uint64_t n, unsigned char* ws, c
     // pairs, and does nothing for a presorted / reversed input
     BSORT_LAUNCH(PROF_HIST, s, k_order_check<KIND, DESC, U><<<num_sms(), HIST_THREADS, 0, s>>>(keys, n, order));
     BSORT_LAUNCH(PROF_HIST, s,
-                 hk<<<num_sms(), HIST_THREADS, hsmem, s>>>(keys, n, ghist, joint, order, true, gcoarse));
+                 hk<<<num_sms(), HIST_THREADS, hsmem, s>>>(
+                     keys, n, ghist, joint, order, true, gcoarse,
+                     tri ? ZeroSpan{reinterpret_cast<uint4*>(lookback), (uint32_t)(3 * l.lb_bytes / 16)} : ZeroSpan{}));
   } else {
     // the histogram kernel's last CTA also plans (no k_plan launch)
     auto hk = k_onesweep_hist<KIND, DESC, U, LANES, true>;
@@ -364,8 +372,12 @@ bsort_status_t lsd_run(U* keys, uint32_t* vals, uint64_t n, unsigned char* ws, c
         zs = ZeroSpan{reinterpret_cast<uint4*>(reinterpret_cast<unsigned char*>(lookback) + ((p + 1) & 1) * l.lb_bytes),
                       (uint32_t)(l.lb_bytes / 16)};
     } else if constexpr (p > 0) {
-      st = memset_async(lookback, l.lb_tiles * 256 * sizeof(DescT), s);
-      if (st != BSORT_SUCCESS) return;
+      if (tri && p <= 3) {
+        lb = reinterpret_cast<DescT*>(reinterpret_cast<unsigned char*>(lookback) + (p - 1) * l.lb_bytes);
+      } else {
+        st = memset_async(lookback, l.lb_tiles * 256 * sizeof(DescT), s);
+        if (st != BSORT_SUCCESS) return;
+      }
     }
     // The first LSD pass may order equal digits arbitrarily (the input order carries no
     // information); every later pass must be stable.
@@ -376,7 +388,7 @@ bsort_status_t lsd_run(U* keys, uint32_t* vals, uint64_t n, unsigned char* ws, c
       if constexpr (sizeof(U) == 8 && !KV) {
         if (n >= WS_MIN_N && ws_enabled() && (uintptr_t)keys % 16 == 0) {
           st = launch_pass_ws<U, DescT, false, RANK_UNSTABLE>(keys, scratch, n, RadixDigit<KIND, DESC, U, SH>{},
-                                                              bases, lookback, counters, plan, p, s, KvPtrs{},
+                                                              bases, lb, counters, plan, p, s, KvPtrs{},
                                                               gcount);
           done = true;
         }
@@ -389,8 +401,8 @@ bsort_status_t lsd_run(U* keys, uint32_t* vals, uint64_t n, unsigned char* ws, c
       if constexpr (sizeof(U) == 4 && !KV) {
         if (n >= WS_MIN_N && n <= P2_MAX_N && p2_enabled() && (uintptr_t)keys % sizeof(U) == 0 &&
             atomics_lane_ordered(s)) {
-          // (half-warp counter rows for skewed top digits, k_pass2<..., HALVES = 2> with
-          // P2_SKEWVAR, measured no faster on cfg3's sign+exponent digit: 3.98 vs 3.92 ms)
+          // (below 2^24 keys, unchunked: half-warp counter rows for skewed digits measured no
+          // faster, 3.98 vs 3.92 ms; with chunked chains they are, below)
           const bool alt = few_alt && p >= 2;
           if (chunked && p >= 2) {
             const int q = p - 2;
@@ -401,26 +413,26 @@ bsort_status_t lsd_run(U* keys, uint32_t* vals, uint64_t n, unsigned char* ws, c
             // both launched, the plan's skew bit lets one work (its tile size is in the chunk map)
             const uint32_t xf = (alt ? P2_FEWALT : 0u) | P2_SKEWVAR;
             st = launch_pass2<KIND, DESC, SH, R2_STABLE, 1, true>(keys, scratch, n, bases + p * 256,
-                                                                  reinterpret_cast<uint32_t*>(lookback), counters + p,
+                                                                  reinterpret_cast<uint32_t*>(lb), counters + p,
                                                                   plan, p, s, xf, cm);
             if (st == BSORT_SUCCESS)
               st = launch_pass2<KIND, DESC, SH, R2_STABLE, 2, true>(keys, scratch, n, bases + p * 256,
-                                                                    reinterpret_cast<uint32_t*>(lookback),
+                                                                    reinterpret_cast<uint32_t*>(lb),
                                                                     counters + p, plan, p, s, xf, cm);
           } else {
             st = launch_pass2<KIND, DESC, SH>(keys, scratch, n, bases + p * 256,
-                                              reinterpret_cast<uint32_t*>(lookback), counters + p, plan, p, s,
+                                              reinterpret_cast<uint32_t*>(lb), counters + p, plan, p, s,
                                               alt ? P2_FEWALT : 0u);
           }
           if (st == BSORT_SUCCESS && alt)
             st = launch_pass_ws<U, DescT, false, RANK_RUN2>(keys, scratch, n, RadixDigit<KIND, DESC, U, SH>{},
-                                                            bases + p * 256, lookback, counters + p, plan, p, s,
+                                                            bases + p * 256, lb, counters + p, plan, p, s,
                                                             KvPtrs{}, nullptr, 1u);
           // pass 2 ranked by runs when the plan allows it (each launch checks plan->run2)
           if constexpr (p == 2)
             if (st == BSORT_SUCCESS && use_joint)
               st = launch_pass2<KIND, DESC, SH, R2_RUN2>(keys, scratch, n, bases + p * 256,
-                                                         reinterpret_cast<uint32_t*>(lookback), counters + 12, plan, p,
+                                                         reinterpret_cast<uint32_t*>(lb), counters + 12, plan, p,
                                                          s);
           done = true;
         }
@@ -428,7 +440,7 @@ bsort_status_t lsd_run(U* keys, uint32_t* vals, uint64_t n, unsigned char* ws, c
       // TMA on both buffers (the scratch buffers are aligned)
       if (!done && n >= WS_MIN_N && ws_enabled() && (uintptr_t)keys % 16 == 0 && (!KV || (uintptr_t)vals % 16 == 0)) {
         st = launch_pass_ws<U, DescT, KV>(keys, scratch, n, RadixDigit<KIND, DESC, U, SH>{}, bases + p * 256,
-                                          lookback, counters + p, plan, p, s, kvp);
+                                          lb, counters + p, plan, p, s, kvp);
         done = true;
       }
       if (!done)
@@ -441,7 +453,7 @@ bsort_status_t lsd_run(U* keys, uint32_t* vals, uint64_t n, unsigned char* ws, c
     if constexpr (p == 1)
       if (st == BSORT_SUCCESS && use_joint)
         st = launch_pass<U, RANK_J01, DescT, KV>(keys, scratch, n, RadixDigit<KIND, DESC, U, SH>{}, bases + 256,
-                                                 lookback, seg, counters + 8, plan, p, s, kvp);
+                                                 lb, seg, counters + 8, plan, p, s, kvp);
   };
   one_pass(std::integral_constant<int, 0>{});
   one_pass(std::integral_constant<int, 8>{});

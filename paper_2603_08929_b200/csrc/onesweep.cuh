@@ -215,6 +215,14 @@ struct RankDigit {
   }
 };
 
+// A region a kernel zeroes (grid-stride, 16-byte stores): look-back descriptors of later passes,
+// so no memset launch per pass (lsd_impl.cuh: the pass kernels below 2^22 keys, the joint
+// histogram sweep above 2^24).
+struct ZeroSpan {
+  uint4* p;
+  uint32_t n16;
+};
+
 // ---------------------------------------------------------------------------------------
 // a3: one read of all keys, P = sizeof(U) digit histograms of 256 bins.  Counters are
 // lane-banked (address = bin*LANES + lane%LANES, bank = lane) so the shared-memory atomics of a
@@ -445,7 +453,8 @@ template <int KIND, bool DESC, typename U, int LANES>
 __global__ void __launch_bounds__(HIST_THREADS, 1)
     k_onesweep_hist_joint(const U* __restrict__ keys, uint64_t n, unsigned long long* __restrict__ ghist,
                           unsigned long long* __restrict__ gjoint, uint32_t* __restrict__ order = nullptr,
-                          bool prechecked = false, unsigned long long* __restrict__ gcoarse = nullptr) {
+                          bool prechecked = false, unsigned long long* __restrict__ gcoarse = nullptr,
+                          ZeroSpan zs = {}) {
   constexpr int P = sizeof(U);
   // 32-bit keys: digits 2 and 3 counted as the coarse joints of passes 2 and 3 (LB_NC; the launch
   // sizes shared memory by hist_joint_words)
@@ -571,6 +580,9 @@ __global__ void __launch_bounds__(HIST_THREADS, 1)
     add(keys[j]);
     check1(j, key_encode<KIND, DESC>(keys[j]));
   }
+  // the look-back regions of the LSD passes (lsd_run): zeroed here, where HBM has room (this
+  // sweep is bound by shared atomics), instead of one memset launch per look-back pass
+  for (uint64_t i = gt; i < zs.n16; i += T) __stcs(&zs.p[i], make_uint4(0u, 0u, 0u, 0u));
   of.flush(order);
   __syncthreads();
   for (int w = threadIdx.x; w < 32768; w += HIST_THREADS) {
@@ -879,12 +891,6 @@ struct KvPtrs {
   uint32_t* vb;
 };
 
-// A region the pass kernel zeroes (grid-stride, 16-byte stores) before anything else: the next
-// pass's look-back descriptors, so small sorts need no memset launch per pass (lsd_impl.cuh).
-struct ZeroSpan {
-  uint4* p;
-  uint32_t n16;
-};
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return (uint32_t)__cvta_generic_to_shared(p);
