@@ -435,6 +435,9 @@ __global__ void __launch_bounds__(HIST_THREADS) k_order_check(const U* __restric
 // which the histogram sweep counts instead of a plain digit-2 histogram (its marginal).  (Pass 3
 // chunked the same way measured slower in the sort: 3.94 -> 4.12 ms.)
 constexpr int LB_NC = 4;
+#ifndef HIST_PLAIN_VEC
+#define HIST_PLAIN_VEC 1
+#endif
 // coarse-joint shared counters [256 digits][LB_NC chunks][CJ_LANES lane banks]: lanes l and l + 16
 // share a bank only when their chunks have equal parity
 constexpr int CJ_LANES = 16;
@@ -510,6 +513,36 @@ __global__ void __launch_bounds__(HIST_THREADS, 1)
   // a full vector of PER_VEC consecutive keys, called by whole warps: equal joint bins within
   // the thread, and within the warp, are added once (runs of equal keys do not serialize)
   auto add_vec = [&](const U (&kv)[PER_VEC]) {
+    if constexpr (COARSE && HIST_PLAIN_VEC) {
+      // 32-bit keys: single increments (the drain test is one compare), except that a warp whose
+      // 128 keys share one joint bin (long runs of equal keys that are not presorted: those
+      // never reach this sweep, k_order_check) adds once
+      U k[PER_VEC];
+      uint32_t jb[PER_VEC];
+#pragma unroll
+      for (int j = 0; j < PER_VEC; ++j) {
+        k[j] = key_encode<KIND, DESC>(kv[j]);
+        jb[j] = uint32_t(k[j]) & 0xFFFFu;
+      }
+      const uint32_t j0 = __shfl_sync(0xffffffffu, jb[0], 0);
+      const bool uniform = __all_sync(0xffffffffu, ((jb[0] ^ j0) | (jb[1] ^ j0) | (jb[2] ^ j0) | (jb[3] ^ j0)) == 0u);
+      if (uniform) {
+        if ((threadIdx.x & 31) == 0) add_joint(jb[0], 32u * PER_VEC);
+      } else {
+#pragma unroll
+        for (int j = 0; j < PER_VEC; ++j) {
+          const uint32_t sh = (jb[j] & 1u) << 4;
+          const uint32_t old = atomicAdd(&hj[jb[j] >> 1], 1u << sh);
+          if (((old >> sh) & 0xFFFFu) == 0x7FFFu) {  // this add took the half to 0x8000: drain
+            atomicAdd(&hj[jb[j] >> 1], 0u - (0x8000u << sh));
+            atomicAdd(&gjoint[jb[j]], 0x8000ull);
+          }
+        }
+      }
+#pragma unroll
+      for (int j = 0; j < PER_VEC; ++j) add_high(k[j]);
+      return;
+    }
     U k[PER_VEC];
     uint32_t jb[PER_VEC];
     bool same = true;

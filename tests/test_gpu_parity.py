@@ -471,3 +471,17 @@ def test_chunked_lookback_passes(B, dtype):
         x = as_dtype(v)
         check_equal(B, x.clone(), False, what)
         check_equal(B, x.clone(), True, what + " desc")
+
+
+@pytest.mark.parametrize("dtype", [torch.int32, torch.float32], ids=lambda d: str(d).split(".")[-1])
+def test_blocks_of_equal_keys_joint_sizes(B, dtype):
+    """Long runs of equal keys in non-sorted order at joint-histogram sizes: warps whose 128 keys
+    share a joint bin add once (the u16 bins then cross 0x8000 by a 128-key step: drain path),
+    the rest add per key; runs of 4096 keys of three values, plus a ragged tail."""
+    n = (1 << 24) + 5
+    i = torch.arange(n, device="cuda")
+    vals = torch.tensor([0x40490FDB, -7, 0x12345], dtype=torch.int64, device="cuda")
+    v = vals[((i // 4096) * 7919) % 3]
+    x = torch.where(v >= (1 << 31), v - (1 << 32), v).to(torch.int32).view(dtype)
+    check_equal(B, x.clone(), False, "blocks of equal keys")
+    check_equal(B, x.clone(), True, "blocks of equal keys desc")
