@@ -81,6 +81,9 @@ constexpr uint64_t JOINT_MIN_N = 1ull << 24;
 
 // Smallest n for the warp-specialised / round-2 look-back passes (lsd_run).
 constexpr uint64_t WS_MIN_N = 1ull << 22;
+// Smallest look-back tile of the kernels that use the three look-back regions of 32-bit
+// keys-only joint sorts (k_pass2's half-warp-row variant: 640 x 15; checked below)
+constexpr uint64_t TRI_MIN_TILE = 9600;
 
 template <typename U>
 LsdLayout lsd_layout(uint64_t n, bool kv = false) {
@@ -106,9 +109,18 @@ LsdLayout lsd_layout(uint64_t n, bool kv = false) {
   l.counters = off; off = align_up(off + 16 * 4, 256);
   // below WS_MIN_N two look-back regions alternate by pass parity (each pass kernel zeroes the
   // next pass's region: no memset launches, lsd_run)
-  l.lb_bytes = align_up(tiles * 256 * desc, 256);
-  l.lb_regions = n < WS_MIN_N ? 2 : ((sizeof(U) == 4 && !kv && n >= JOINT_MIN_N) ? 3 : 1);
+  l.lb_regions = n < WS_MIN_N ? 2 : ((sizeof(U) == 4 && !kv && n >= JOINT_MIN_N && n <= (1ull << 30)) ? 3 : 1);
+  // three regions: only k_pass2 (tiles >= TRI_MIN_TILE keys, + one partial tile per chunk) and the
+  // few-runs kernel (10,240-key tiles) use them, so they are sized for those tiles
+  const uint64_t lbt = l.lb_regions == 3 ? n / TRI_MIN_TILE + 16 : tiles;
+  l.lb_bytes = align_up(lbt * 256 * desc, 256);
   l.lookback = off; off += l.lb_regions * l.lb_bytes;
+  // just above 2^30 keys one (64-bit) region is smaller than the three regions at 2^30: pad, so
+  // the workspace stays monotone in n (a workspace sized for n serves every smaller n)
+  if (sizeof(U) == 4 && !kv && n > (1ull << 30)) {
+    const uint64_t tri = 3 * align_up(((1ull << 30) / TRI_MIN_TILE + 16) * 256 * 4, 256);
+    if (tri > l.lb_regions * l.lb_bytes) off += tri - l.lb_regions * l.lb_bytes;
+  }
   l.grid = off;     off = align_up(off + grid_detail::workspace_bytes(), 256);  // k_grid_sort counts
   l.lb_tiles = tiles;
   l.total = off;
@@ -216,6 +228,10 @@ struct P2SkewCfg {
   static constexpr int RT = 640, WT = 256, ITEMS = 15;
 };
 constexpr uint64_t P2_MAX_N = 1ull << 30;
+static_assert((uint64_t)P2SkewCfg::RT * P2SkewCfg::ITEMS >= TRI_MIN_TILE &&
+                  (uint64_t)P2Cfg<R2_STABLE>::RT * P2Cfg<R2_STABLE>::ITEMS >= TRI_MIN_TILE &&
+                  (uint64_t)WsCfg<uint32_t, false>::RT * WsCfg<uint32_t, false>::ITEMS >= TRI_MIN_TILE,
+              "the three look-back regions are sized for TRI_MIN_TILE-key tiles");
 // RUN2 for pass 2 measured slower than the stable pass on cfg3 (4.25 vs 3.6 ms, ALU-bound):
 // off unless BSORT_P2_RUN2=1
 inline bool p2_run2_enabled() {
@@ -430,7 +446,7 @@ bsort_status_t lsd_run(U* keys, uint32_t* vals, uint64_t n, unsigned char* ws, c
                                                             KvPtrs{}, nullptr, 1u);
           // pass 2 ranked by runs when the plan allows it (each launch checks plan->run2)
           if constexpr (p == 2)
-            if (st == BSORT_SUCCESS && use_joint)
+            if (st == BSORT_SUCCESS && use_joint && !tri)  // (8192-key tiles: not in the tri regions)
               st = launch_pass2<KIND, DESC, SH, R2_RUN2>(keys, scratch, n, bases + p * 256,
                                                          reinterpret_cast<uint32_t*>(lb), counters + 12, plan, p,
                                                          s);
