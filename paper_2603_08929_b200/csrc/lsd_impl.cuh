@@ -218,9 +218,10 @@ bsort_status_t launch_pass_ws(const U* a, U* b, uint64_t n, DigitF digit, const 
 template <int MODE> struct P2Cfg {
   static constexpr int RT = 512, WT = 256, ITEMS = 20;  // chunked passes 2 / 3: 2.97 -> 2.91 / 3.44 -> 3.37 ms vs 640 x 16
 };
-// RUN2 holds two lane-banked tables (counts, offsets): 8192-key tiles
+// RUN2 holds two lane-banked tables (counts, offsets): 640 x 15 = 9600-key tiles (TRI_MIN_TILE:
+// the chunked RUN2 pass 2 uses the three look-back regions; 225 KB of shared memory)
 template <> struct P2Cfg<R2_RUN2> {
-  static constexpr int RT = 512, WT = 256, ITEMS = 16;
+  static constexpr int RT = 640, WT = 256, ITEMS = 15;
 };
 template <int MODE> constexpr uint64_t p2_tile() { return (uint64_t)P2Cfg<MODE>::RT * P2Cfg<MODE>::ITEMS; }
 // skewed digits (plan->skew): half-warp counter rows, odd ITEMS (conflict-free key loads)
@@ -230,6 +231,7 @@ struct P2SkewCfg {
 constexpr uint64_t P2_MAX_N = 1ull << 30;
 static_assert((uint64_t)P2SkewCfg::RT * P2SkewCfg::ITEMS >= TRI_MIN_TILE &&
                   (uint64_t)P2Cfg<R2_STABLE>::RT * P2Cfg<R2_STABLE>::ITEMS >= TRI_MIN_TILE &&
+                  p2_tile<R2_RUN2>() >= TRI_MIN_TILE &&
                   (uint64_t)WsCfg<uint32_t, false>::RT * WsCfg<uint32_t, false>::ITEMS >= TRI_MIN_TILE,
               "the three look-back regions are sized for TRI_MIN_TILE-key tiles");
 // RUN2 for pass 2 measured slower than the stable pass on cfg3 (4.25 vs 3.6 ms, ALU-bound):
@@ -435,6 +437,13 @@ bsort_status_t lsd_run(U* keys, uint32_t* vals, uint64_t n, unsigned char* ws, c
               st = launch_pass2<KIND, DESC, SH, R2_STABLE, 2, true>(keys, scratch, n, bases + p * 256,
                                                                     reinterpret_cast<uint32_t*>(lb),
                                                                     counters + p, plan, p, s, xf, cm);
+            // pass 2 ranked by runs (chunked, same chains) when the plan sets run2; the stable
+            // launches above then return at once
+            if constexpr (p == 2)
+              if (st == BSORT_SUCCESS && p2_run2_enabled())
+                st = launch_pass2<KIND, DESC, SH, R2_RUN2, 1, true>(keys, scratch, n, bases + p * 256,
+                                                                    reinterpret_cast<uint32_t*>(lb),
+                                                                    counters + 12, plan, p, s, 0u, cm);
           } else {
             st = launch_pass2<KIND, DESC, SH>(keys, scratch, n, bases + p * 256,
                                               reinterpret_cast<uint32_t*>(lb), counters + p, plan, p, s,
@@ -446,7 +455,7 @@ bsort_status_t lsd_run(U* keys, uint32_t* vals, uint64_t n, unsigned char* ws, c
                                                             KvPtrs{}, nullptr, 1u);
           // pass 2 ranked by runs when the plan allows it (each launch checks plan->run2)
           if constexpr (p == 2)
-            if (st == BSORT_SUCCESS && use_joint && !tri)  // (8192-key tiles: not in the tri regions)
+            if (st == BSORT_SUCCESS && use_joint && !chunked && p2_run2_enabled())
               st = launch_pass2<KIND, DESC, SH, R2_RUN2>(keys, scratch, n, bases + p * 256,
                                                          reinterpret_cast<uint32_t*>(lb), counters + 12, plan, p,
                                                          s);

@@ -705,6 +705,35 @@ static __global__ void __launch_bounds__(256)
                  unsigned long long* __restrict__ seg, uint64_t run2_tile = 0, uint64_t fewruns_tile = 0,
                  uint64_t fewruns_n = 0, ChunkPlanArgs cp = {}) {
   const uint32_t t = threadIdx.x;
+  // RUN2 for pass 2 (pass2.cuh): its input is sorted by the low 16 bits, whose runs are the joint
+  // bins; a tile meets at most two of them when every nonzero bin is at least a tile long
+  bool ok2 = run2_tile > 0;
+  for (int b = 0; b < 256 && ok2; ++b) {
+    const unsigned long long c = gjoint[t * 256 + b];
+    ok2 = c == 0 || c >= run2_tile;
+  }
+  const int run2 = __syncthreads_and(ok2);
+  // Few distinct lower-bit values (fewruns_tile > 0, 32-bit keys): pass 2's input is sorted by
+  // the low 16 bits, whose distinct values are the nonzero joint bins (nz16); pass 3's by the
+  // low 24 bits, at most nz16 x (nonzero digit-2 bins) distinct values.  When the average run is
+  // at least 4 tiles, almost every tile meets at most two runs, and the run-ranking kernel (one
+  // unstable atomic per key, per-tile fallback to the stable ranking) beats the lane-ordered
+  // stable pass, whose same-word atomics serialize on few distinct digits (cfg4 16-distinct).
+  __shared__ uint32_t few_s;
+  if (fewruns_tile > 0) {  // nz16 was counted by k_plan (plan->pad[0])
+    const uint32_t nz2 = (uint32_t)__syncthreads_count(ghist[512 + t] != 0);
+    if (t == 0) {
+      const unsigned long long r2 = plan->pad[0], r3 = r2 * nz2, lim = fewruns_n / (4 * fewruns_tile);
+      few_s = (r2 <= lim ? 4u : 0u) | (r3 <= lim ? 8u : 0u);
+      plan->fewruns = few_s;
+    }
+  } else if (t == 0) {
+    few_s = 0;
+  }
+  __syncthreads();
+  // pass 2 by runs unless the few-runs kernel takes it
+  const bool run2_on = run2 && !plan->skip[2] && !(few_s & 4u);
+  if (t == 0) plan->run2 = run2_on ? 1u : 0u;
   if (cp.jp != nullptr) {
     for (int q = 0; q < 2; ++q) {  // passes 2 and 3 (index q = pass - 2)
       unsigned long long run = cp.bases[(2 + q) * 256 + t];
@@ -718,32 +747,12 @@ static __global__ void __launch_bounds__(256)
         for (int c = 0; c < LB_NC; ++c) cs[c] = cp.bases[(1 + q) * 256 + 64 * c];
         cs[LB_NC] = cp.n;
         ct[0] = 0;
-        // the pass runs k_pass2's half-warp-row variant when its digit is skewed (k_plan's skew bit)
-        const uint64_t tl = ((plan->skew >> (2 + q)) & 1u) ? cp.tile_skew : cp.tile;
+        // the pass runs k_pass2's half-warp-row variant when its digit is skewed (k_plan's skew
+        // bit), pass 2 the chunked RUN2 launch when run2 is set
+        const uint64_t tl = (q == 0 && run2_on) ? run2_tile
+                            : ((plan->skew >> (2 + q)) & 1u) ? cp.tile_skew : cp.tile;
         for (int c = 0; c < LB_NC; ++c) ct[c + 1] = ct[c] + (uint32_t)((cs[c + 1] - cs[c] + tl - 1) / tl);
       }
-    }
-  }
-  // RUN2 for pass 2 (pass2.cuh): its input is sorted by the low 16 bits, whose runs are the joint
-  // bins; a tile meets at most two of them when every nonzero bin is at least a tile long
-  bool ok2 = run2_tile > 0;
-  for (int b = 0; b < 256 && ok2; ++b) {
-    const unsigned long long c = gjoint[t * 256 + b];
-    ok2 = c == 0 || c >= run2_tile;
-  }
-  const int run2 = __syncthreads_and(ok2);
-  if (t == 0) plan->run2 = (uint32_t)run2 && !plan->skip[2];
-  // Few distinct lower-bit values (fewruns_tile > 0, 32-bit keys): pass 2's input is sorted by
-  // the low 16 bits, whose distinct values are the nonzero joint bins (nz16); pass 3's by the
-  // low 24 bits, at most nz16 x (nonzero digit-2 bins) distinct values.  When the average run is
-  // at least 4 tiles, almost every tile meets at most two runs, and the run-ranking kernel (one
-  // unstable atomic per key, per-tile fallback to the stable ranking) beats the lane-ordered
-  // stable pass, whose same-word atomics serialize on few distinct digits (cfg4 16-distinct).
-  if (fewruns_tile > 0) {  // nz16 was counted by k_plan (plan->pad[0])
-    const uint32_t nz2 = (uint32_t)__syncthreads_count(ghist[512 + t] != 0);
-    if (t == 0) {
-      const unsigned long long r2 = plan->pad[0], r3 = r2 * nz2, lim = fewruns_n / (4 * fewruns_tile);
-      plan->fewruns = (r2 <= lim ? 4u : 0u) | (r3 <= lim ? 8u : 0u);
     }
   }
   const unsigned long long c0 = ghist[t];  // digit-0 marginal

@@ -335,7 +335,7 @@ __global__ void __launch_bounds__(RT + WT, MINB)
   static_assert(MODE == R2_STABLE || TILE * sizeof(U) < (1 << 16), "staging offsets fit u16");
   static_assert((TILE * sizeof(U)) % 16 == 0 && L::bytes < (1 << 18) && L::bytes <= 227 * 1024,
                 "16-byte tiles; addresses fit 18 bits; fits shared memory");
-  static_assert(!CHUNKED || MODE == R2_STABLE, "chunks are look-back chains");
+  static_assert(!CHUNKED || MODE == R2_STABLE || MODE == R2_RUN2, "chunks are look-back chains");
   extern __shared__ __align__(128) unsigned char smem[];
   U* ibufs = reinterpret_cast<U*>(smem + L::ibuf_off);
   uint32_t* cnt = reinterpret_cast<uint32_t*>(smem + L::cnt_off);

@@ -17,11 +17,16 @@
 //      slot order (a digit's keys are one contiguous run in the destination);        grid barrier
 //
 // A pass whose digit is constant over all keys (T[d] == n) is skipped by every CTA alike.  The
-// count matrix is double-buffered by pass parity.  The grid barrier is a counter in the workspace
-// zeroed by a 4-byte memset before the launch (one release-add per CTA, relaxed polls, one
-// acquire fence): 1.2 us per barrier on B200 (tools/exp/gridbar.cu).  The launch is cooperative
-// for its co-residency guarantee.
+// count matrix is double-buffered by pass parity.  The grid barrier is cooperative groups'
+// grid.sync() on the barrier word the runtime keeps for a cooperative launch, so the launch
+// needs no memset of a counter of ours (one launch per sort instead of memset + launch:
+// ~2 us at cfg1); with BSORT_GRID_CG=0 it is a counter in the workspace zeroed by a 4-byte
+// memset before the launch (one release-add per CTA, relaxed polls, one acquire fence).  Both
+// cost 1.2 us per barrier on B200 (tools/exp/gridbar.cu).  The launch is cooperative for its
+// co-residency guarantee.
 #pragma once
+
+#include <cooperative_groups.h>
 
 #include "common.cuh"
 
@@ -49,6 +54,10 @@ __host__ __device__ constexpr size_t barrier_offset() { return 2ull * 256 * ROW 
 __host__ __device__ constexpr size_t workspace_bytes() { return barrier_offset() + 256; }
 
 __device__ __forceinline__ void grid_barrier(unsigned* ctr, unsigned target) {
+  if (ctr == nullptr) {  // cooperative groups' barrier (no workspace word, no memset)
+    cooperative_groups::this_grid().sync();
+    return;
+  }
   __syncthreads();
   if (threadIdx.x == 0) {  // bar.sync above + a cumulative release: the CTA's writes are published
     asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(ctr) : "memory");
@@ -174,7 +183,7 @@ __device__ __forceinline__ U* small_lsd(U* a, U* b, uint32_t m, uint32_t* wc, ui
 template <int KIND, bool DESC, typename U>
 __global__ void __launch_bounds__(grid_detail::THREADS, 1)
     k_grid_sort(U* __restrict__ keys, U* __restrict__ scratch, uint64_t n, uint32_t chunk,
-                uint16_t* __restrict__ cnt, int keys_vec, int lane_atomics, int msd) {
+                uint16_t* __restrict__ cnt, int keys_vec, int lane_atomics, int msd, int cgsync) {
   using namespace grid_detail;
   extern __shared__ __align__(128) unsigned char smem[];
   U* sk = reinterpret_cast<U*>(smem);                                  // the chunk, input order
@@ -187,7 +196,7 @@ __global__ void __launch_bounds__(grid_detail::THREADS, 1)
   __shared__ int gtriv[2];  // MSD bucket groups' trivial flags
   __shared__ int trivial;
   __shared__ uint32_t bT[256], bS[256], bmax;  // MSD: bucket sizes and starts, largest bucket
-  unsigned* bar = reinterpret_cast<unsigned*>(reinterpret_cast<unsigned char*>(cnt) + barrier_offset());
+  unsigned* bar = cgsync ? nullptr : reinterpret_cast<unsigned*>(reinterpret_cast<unsigned char*>(cnt) + barrier_offset());
 
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
   const uint32_t G = gridDim.x, c = blockIdx.x;
@@ -469,8 +478,15 @@ bsort_status_t launch_grid(U* keys, U* scratch, uint64_t n, uint16_t* cnt, cudaS
   // (small grids would sort 256 / G buckets per CTA one after the other: 2^16 keys on 16 CTAs
   // took 72 us against 35 us for the LSD passes)
   int msd = (sizeof(U) == 4 && msd_on && g >= 64) ? 1 : 0;
-  void* args[] = {&keys, &scratch, &n, &chunk, &cnt, &keys_vec, &lane_atomics, &msd};
-  BSORT_LAUNCH(PROF_MEMSET, s, cudaMemsetAsync(reinterpret_cast<unsigned char*>(cnt) + barrier_offset(), 0, 4, s));
+  static const int cgsync = [] {
+    const char* e = getenv("BSORT_GRID_CG");
+    return (e && e[0] == '0') ? 0 : 1;
+  }();
+  int cg = cgsync;
+  void* args[] = {&keys, &scratch, &n, &chunk, &cnt, &keys_vec, &lane_atomics, &msd, &cg};
+  if (!cg) {
+    BSORT_LAUNCH(PROF_MEMSET, s, cudaMemsetAsync(reinterpret_cast<unsigned char*>(cnt) + barrier_offset(), 0, 4, s));
+  }
   BSORT_LAUNCH(PROF_PASS, s, cudaLaunchCooperativeKernel((const void*)kern, dim3((unsigned)g), dim3(THREADS), args,
                                                          SMEM, s));
   return BSORT_SUCCESS;

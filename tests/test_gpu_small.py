@@ -244,6 +244,13 @@ def test_grid_lsd_only_at_grid_sizes():
                                                  (torch.uint32, 50_001)], expect_launches=1)
 
 
+def test_grid_counter_barrier():
+    """BSORT_GRID_CG=0: k_grid_sort's grid barriers on the workspace counter (memset before the
+    launch) instead of cooperative groups' grid.sync(); MSD and LSD grid sizes, 64-bit keys."""
+    _subprocess_sorts({"BSORT_GRID_CG": "0"}, [(torch.int32, (1 << 20) + 5), (torch.float32, 300_007),
+                                               (torch.int64, (1 << 18) + 7)])
+
+
 def test_grid_msd_single_bucket_in_place():
     """BSORT_SMALL_MAX=1000: a 20,000-key grid sort whose top digit is constant -- the MSD pass
     moves nothing and its one bucket (all keys, still in the caller's buffer) fits one CTA."""

@@ -30,7 +30,7 @@ CMD="python bench.py --steps 2 --warmup 3 --quick --no-cpu"
 if has launches; then
   timeout 600 $CMD > "$OUT/plain.log" 2>&1 &&
   timeout 900 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum \
-      --clock-control none --csv -k regex:"k_(count|onesweep|plan|copy|dist)" \
+      --clock-control none --csv -k regex:"k_" \
       --log-file "$OUT/launches.csv" $CMD > "$OUT/ncu_launches.log" 2>&1
   echo "ncu launches exit $?" >> "$OUT/status.txt"
 fi
