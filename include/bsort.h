@@ -95,6 +95,16 @@ bsort_status_t bsort_sort_host(bsort_dtype_t dtype, void* host_keys, uint64_t n,
                                bsort_direction_t direction, void* dev_keys, void* workspace,
                                size_t workspace_bytes, void* stream);
 
+/* Out-of-place end-to-end form: H2D of `host_in` (n keys, read only) into `dev_keys`, the sort,
+ * and D2H of the result into `host_out` (n keys; may equal host_in, then this is
+ * bsort_sort_host).  Both host buffers should be pinned.  Because host_in is never written, a
+ * caller can keep several sorts in flight on different streams (each with its own dev_keys,
+ * workspace and host_out): one sort's D2H then overlaps the next one's H2D and sort, and PCIe
+ * carries both directions at once.  Errors as bsort_sort_host(). */
+bsort_status_t bsort_sort_host_to(bsort_dtype_t dtype, const void* host_in, void* host_out, uint64_t n,
+                                  bsort_direction_t direction, void* dev_keys, void* workspace,
+                                  size_t workspace_bytes, void* stream);
+
 /* ----------------------------------------------------------- key-value sort
  * Sort n keys of a 32/64-bit dtype (u32/i32/f32/u64/i64/f64; 8/16-bit keys return
  * BSORT_ERROR_UNSUPPORTED_DTYPE) and move the n uint32 values at dev_values (device,

@@ -211,6 +211,28 @@ class Sorter:
                                       _stream_ptr(dev_buf.device)), "bsort_sort_host")
         return host
 
+    def sort_host_to(self, host_in: torch.Tensor, host_out: torch.Tensor, dev_buf: torch.Tensor,
+                     descending: bool = False, stream=None):
+        """Enqueue H2D(host_in -> dev_buf), sort, D2H(dev_buf -> host_out) on `stream` (default:
+        the current stream of dev_buf's device).  host_in is only read, so sorts on different
+        streams (each with its own Sorter, dev_buf and host_out) can overlap."""
+        for h in (host_in, host_out):
+            if h.is_cuda or not h.is_contiguous() or h.dtype != self.dtype:
+                raise ValueError("sort_host_to: need contiguous host tensors of the Sorter dtype")
+        if host_out.numel() != host_in.numel():
+            raise ValueError("sort_host_to: host_in and host_out differ in size")
+        _check_tensor(dev_buf)
+        if dev_buf.numel() < host_in.numel() or host_in.numel() > self.n:
+            raise ValueError("sort_host_to: device buffer / workspace too small")
+        sp = ctypes.c_void_p(stream.cuda_stream) if stream is not None else _stream_ptr(dev_buf.device)
+        with _on(dev_buf.device):
+            check(lib.bsort_sort_host_to(self.code, ctypes.c_void_p(host_in.data_ptr()),
+                                         ctypes.c_void_p(host_out.data_ptr()), host_in.numel(),
+                                         int(bool(descending)), ctypes.c_void_p(dev_buf.data_ptr()),
+                                         ctypes.c_void_p(self.ws.data_ptr()), self.ws_bytes, sp),
+                  "bsort_sort_host_to")
+        return host_out
+
 
 def sort_host(host: torch.Tensor, descending: bool = False, device="cuda") -> torch.Tensor:
     """Sort a (preferably pinned) host tensor through the GPU; returns after completion."""

@@ -26,7 +26,7 @@ ERROR_NCCL = 6
 ERROR_CAPACITY = 7
 
 EXPORTS = [
-    "bsort_workspace_bytes", "bsort_sort", "bsort_sort_ws", "bsort_sort_host",
+    "bsort_workspace_bytes", "bsort_sort", "bsort_sort_ws", "bsort_sort_host", "bsort_sort_host_to",
     "bsort_pairs_workspace_bytes", "bsort_sort_pairs_ws", "bsort_sort_pairs",
     "bsort_inplace_workspace_bytes", "bsort_sort_inplace_ws",
     "bsort_dist_top_hist", "bsort_dist_splitters", "bsort_dist_send_counts",
@@ -75,6 +75,7 @@ def _load():
         "bsort_sort": (i32, [i32, vp, u64, i32, vp]),
         "bsort_sort_ws": (i32, [i32, vp, u64, i32, vp, sz, vp]),
         "bsort_sort_host": (i32, [i32, vp, u64, i32, vp, vp, sz, vp]),
+        "bsort_sort_host_to": (i32, [i32, vp, vp, u64, i32, vp, vp, sz, vp]),
         "bsort_pairs_workspace_bytes": (sz, [i32, u64]),
         "bsort_sort_pairs_ws": (i32, [i32, vp, vp, u64, i32, vp, sz, vp]),
         "bsort_sort_pairs": (i32, [i32, vp, vp, u64, i32, vp]),

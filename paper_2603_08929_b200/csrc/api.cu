@@ -208,21 +208,28 @@ bsort_status_t bsort_sort(bsort_dtype_t dtype, void* dev_keys, uint64_t n, bsort
 
 bsort_status_t bsort_sort_host(bsort_dtype_t dtype, void* host_keys, uint64_t n, bsort_direction_t direction,
                                void* dev_keys, void* workspace, size_t workspace_bytes_, void* stream) {
+  return bsort_sort_host_to(dtype, host_keys, host_keys, n, direction, dev_keys, workspace, workspace_bytes_,
+                            stream);
+}
+
+bsort_status_t bsort_sort_host_to(bsort_dtype_t dtype, const void* host_in, void* host_out, uint64_t n,
+                                  bsort_direction_t direction, void* dev_keys, void* workspace,
+                                  size_t workspace_bytes_, void* stream) {
   DtypeInfo di;
   bsort_status_t st = validate(dtype, dev_keys, n, direction, &di);
   if (st != BSORT_SUCCESS) return st;
-  if (n > 0 && host_keys == nullptr) return BSORT_ERROR_INVALID_ARGUMENT;
+  if (n > 0 && (host_in == nullptr || host_out == nullptr)) return BSORT_ERROR_INVALID_ARGUMENT;
   if (n == 0) return BSORT_SUCCESS;
   if (n > 1 && workspace_bytes_ < workspace_bytes(di, n)) return BSORT_ERROR_WORKSPACE_TOO_SMALL;
   cudaStream_t s = (cudaStream_t)stream;
   const size_t bytes = (size_t)n * di.bytes;
   prof_begin(PROF_H2D, s);
-  BSORT_CUDA(cudaMemcpyAsync(dev_keys, host_keys, bytes, cudaMemcpyHostToDevice, s));
+  BSORT_CUDA(cudaMemcpyAsync(dev_keys, host_in, bytes, cudaMemcpyHostToDevice, s));
   prof_end(PROF_H2D, s);
   st = sort_ws_graphed(dtype, di, dev_keys, n, direction, workspace, workspace_bytes_, s);
   if (st != BSORT_SUCCESS) return st;
   prof_begin(PROF_D2H, s);
-  BSORT_CUDA(cudaMemcpyAsync(host_keys, dev_keys, bytes, cudaMemcpyDeviceToHost, s));
+  BSORT_CUDA(cudaMemcpyAsync(host_out, dev_keys, bytes, cudaMemcpyDeviceToHost, s));
   prof_end(PROF_D2H, s);
   return BSORT_SUCCESS;
 }

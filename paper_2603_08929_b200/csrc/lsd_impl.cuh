@@ -225,8 +225,14 @@ template <> struct P2Cfg<R2_RUN2> {
 };
 template <int MODE> constexpr uint64_t p2_tile() { return (uint64_t)P2Cfg<MODE>::RT * P2Cfg<MODE>::ITEMS; }
 // skewed digits (plan->skew): half-warp counter rows, odd ITEMS (conflict-free key loads)
+#ifndef P2SKEW_RT
+#define P2SKEW_RT 640
+#endif
+#ifndef P2SKEW_ITEMS
+#define P2SKEW_ITEMS 15
+#endif
 struct P2SkewCfg {
-  static constexpr int RT = 640, WT = 256, ITEMS = 15;
+  static constexpr int RT = P2SKEW_RT, WT = 256, ITEMS = P2SKEW_ITEMS;
 };
 constexpr uint64_t P2_MAX_N = 1ull << 30;
 static_assert((uint64_t)P2SkewCfg::RT * P2SkewCfg::ITEMS >= TRI_MIN_TILE &&

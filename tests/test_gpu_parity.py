@@ -162,6 +162,26 @@ def test_sort_host_roundtrip(B):
     assert x.numpy().tobytes() == ref.tobytes()
 
 
+def test_sort_host_to_two_streams(B):
+    """bsort_sort_host_to: pinned input never written; two sorts in flight on two streams (the
+    bench's pipelined e2e), joint-histogram size (2^24 + 5) and a small one, both directions."""
+    for n, dt in (((1 << 24) + 5, torch.float32), (70001, torch.int64)):
+        x = gen(dt, n, 12).cpu().pin_memory()
+        keep = x.clone()
+        for desc in (False, True):
+            ref = oracle.sort_native(x.numpy(), descending=desc)
+            streams = [torch.cuda.Stream(), torch.cuda.Stream()]
+            sorters = [B.Sorter(dt, n, "cuda") for _ in range(2)]
+            devs = [torch.empty(n, dtype=dt, device="cuda") for _ in range(2)]
+            outs = [torch.empty(n, dtype=dt, pin_memory=True) for _ in range(2)]
+            for i in range(4):
+                sorters[i % 2].sort_host_to(x, outs[i % 2], devs[i % 2], desc, stream=streams[i % 2])
+            torch.cuda.synchronize()
+            for o in outs:
+                assert o.numpy().tobytes() == ref.tobytes(), (n, dt, desc)
+            assert x.numpy().tobytes() == keep.numpy().tobytes()  # the input was only read (NaNs: bytes)
+
+
 def test_errors_raise(B):
     t = torch.zeros(10, dtype=torch.complex64, device="cuda")
     with pytest.raises(TypeError):

@@ -14,5 +14,5 @@ M="--metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum -
 CMD="python bench.py --steps 2 --warmup 3 --quick --no-cpu"
 timeout 600 $CMD > $OUT/plain.log 2>&1 && timeout 900 ncu $M -k regex:"k_" --log-file $OUT/launches_bench.csv $CMD > $OUT/ncu_launches.log 2>&1
 echo "launches $?" >> $OUT/status.txt
-timeout 900 ncu --set full --import-source on --clock-control none -k regex:k_pass2 -s 5 -c 1 -o $OUT/pass3_chunked python tools/prof_sort.py --cfg cfg3 --reps 1 > $OUT/ncu_p3.log 2>&1
+timeout 900 ncu --set full --import-source on --clock-control none -k regex:k_pass2 -s 4 -c 1 -o $OUT/pass3_chunked python tools/prof_sort.py --cfg cfg3 --reps 1 > $OUT/ncu_p3.log 2>&1
 echo "ncu p3 $?" >> $OUT/status.txt

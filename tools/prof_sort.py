@@ -25,4 +25,4 @@ for _ in range(a.reps):
     w.copy_(x)
     s(w, a.desc)
 torch.cuda.synchronize()
-print("ok", x.dtype, x.numel(), B.launch_count())
+print("ok", x.dtype, x.numel(), B.launch_count(), "selftest", B.selftest())
