@@ -318,7 +318,19 @@ bsort_status_t lsd_run(U* keys, uint32_t* vals, uint64_t n, unsigned char* ws, c
   const bool use_joint = n >= JOINT_MIN_N && !joint_off;
   // passes 1-3 of 32-bit keys-only joint sorts use three look-back regions that the histogram
   // sweep zeroes (no memset launch per pass)
-  const bool tri = use_joint && l.lb_regions == 3;
+  // They are sized for TRI_MIN_TILE-key tiles (lsd_layout).  Where neither k_pass2 (BSORT_P2=0, or
+  // a device that fails the lane-order self-test) nor the warp-specialised kernel (BSORT_WS=0, or
+  // a caller pointer that is not 16-byte aligned) can run, the look-back passes fall back to
+  // k_onesweep_pass, whose smaller tiles need more descriptor rows than one region holds: then
+  // the three regions serve as one (3 x lb_bytes >= l.lb_tiles rows), zeroed by a memset per pass.
+  bool tri = use_joint && l.lb_regions == 3;
+  if constexpr (sizeof(U) == 4 && !KV) {
+    if (tri) {
+      const bool p2_ok = p2_enabled() && atomics_lane_ordered(s);
+      const bool ws_ok = ws_enabled() && (uintptr_t)keys % 16 == 0;
+      if (!p2_ok && !ws_ok) tri = false;
+    }
+  }
   // passes 2-3 of 32-bit keys: k_pass2, or the run-ranking warp-specialised kernel when the plan
   // finds few distinct lower-bit values (k_plan_joint's fewruns; both launched, one works)
   const bool few_alt = sizeof(U) == 4 && !KV && use_joint && n >= WS_MIN_N && n <= P2_MAX_N && p2_enabled() &&

@@ -1187,16 +1187,20 @@ __global__ void __launch_bounds__(THREADS, MINB)
     // 2. ranking.  info = bin | rank << 9 (bin = digit, + 256 for run 1 in RUN2).
     uint32_t info[ITEMS];
     if (unstable_rank) {
-      // invalid tail slots are not counted at all
+      auto rank_item = [&](int k) {
+        U lo;
+        uint32_t bin = digit.digit_low(keys[k], &lo);
+        if constexpr (RUNS) bin |= (lo != low_first) ? 256u : 0u;
+        info[k] = bin | (atomicAdd(&bcnt[bin * BREP + (lane & (BREP - 1))], 1u) << 9);
+      };
+      if (full) {  // no per-item bounds branch (a BSSY / BSYNC pair per key otherwise)
 #pragma unroll
-      for (int k = 0; k < ITEMS; ++k) {
-        if (full || seg + IS * k < valid) {
-          U lo;
-          uint32_t bin = digit.digit_low(keys[k], &lo);
-          if constexpr (RUNS) bin |= (lo != low_first) ? 256u : 0u;
-          info[k] = bin | (atomicAdd(&bcnt[bin * BREP + (lane & (BREP - 1))], 1u) << 9);
-        } else {
-          info[k] = 0xFFFFFFFFu;
+        for (int k = 0; k < ITEMS; ++k) rank_item(k);
+      } else {  // invalid tail slots are not counted at all
+#pragma unroll
+        for (int k = 0; k < ITEMS; ++k) {
+          if (seg + IS * k < valid) rank_item(k);
+          else info[k] = 0xFFFFFFFFu;
         }
       }
     } else if constexpr (MODE == RANK_STABLE || MODE == RANK_RUN2) {
@@ -1285,13 +1289,19 @@ __global__ void __launch_bounds__(THREADS, MINB)
     __syncthreads();  // (B)
 
     if (unstable_rank) {
+      auto place_item = [&](int k) {
+        const uint32_t pos = bcnt[(info[k] & 0x1FFu) * BREP + (lane & (BREP - 1))] + (info[k] >> 9);
+        buf[pos] = keys[k];
+        if constexpr (KV) vbuf[pos] = vals[k];
+      };
+      if (full) {
 #pragma unroll
-      for (int k = 0; k < ITEMS; ++k)
-        if (info[k] != 0xFFFFFFFFu) {
-          const uint32_t pos = bcnt[(info[k] & 0x1FFu) * BREP + (lane & (BREP - 1))] + (info[k] >> 9);
-          buf[pos] = keys[k];
-          if constexpr (KV) vbuf[pos] = vals[k];
-        }
+        for (int k = 0; k < ITEMS; ++k) place_item(k);
+      } else {
+#pragma unroll
+        for (int k = 0; k < ITEMS; ++k)
+          if (info[k] != 0xFFFFFFFFu) place_item(k);
+      }
     } else {
 #pragma unroll
       for (int k = 0; k < ITEMS; ++k) {
@@ -1324,27 +1334,32 @@ __global__ void __launch_bounds__(THREADS, MINB)
     }
     __syncthreads();  // (C)
 
-    // 5. write-out
-#pragma unroll
-    for (int k = 0; k < ITEMS; ++k) {
+    // 5. write-out (full tiles without the per-item bounds branch)
+    auto write_item = [&](int k) {
       const uint32_t i = t + k * THREADS;
-      if (full || i < valid) {
-        const U x = buf[i];
-        if constexpr (DigitF::REMOTE) {
-          reinterpret_cast<U*>(gofs[digit(x)])[i] = x;  // st.global to the owner's buffer
+      const U x = buf[i];
+      if constexpr (DigitF::REMOTE) {
+        reinterpret_cast<U*>(gofs[digit(x)])[i] = x;  // st.global to the owner's buffer
+      } else {
+        unsigned long long o;
+        if constexpr (MODE == RANK_J01) {
+          U lo;
+          const uint32_t d = digit.digit_low(x, &lo);
+          o = gofs[d + (lo != low_first ? 256u : 0u)] + i;
         } else {
-          unsigned long long o;
-          if constexpr (MODE == RANK_J01) {
-            U lo;
-            const uint32_t d = digit.digit_low(x, &lo);
-            o = gofs[d + (lo != low_first ? 256u : 0u)] + i;
-          } else {
-            o = gofs[digit(x)] + i;
-          }
-          dst[o] = x;
-          if constexpr (KV) vdst[o] = vbuf[i];
+          o = gofs[digit(x)] + i;
         }
+        dst[o] = x;
+        if constexpr (KV) vdst[o] = vbuf[i];
       }
+    };
+    if (full) {
+#pragma unroll
+      for (int k = 0; k < ITEMS; ++k) write_item(k);
+    } else {
+#pragma unroll
+      for (int k = 0; k < ITEMS; ++k)
+        if (t + k * THREADS < valid) write_item(k);
     }
     if constexpr (BULK) {
       __syncthreads();  // (D) buffer `cur` fully read: refill it with the tile after next

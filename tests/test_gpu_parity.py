@@ -505,3 +505,33 @@ def test_blocks_of_equal_keys_joint_sizes(B, dtype):
     x = torch.where(v >= (1 << 31), v - (1 << 32), v).to(torch.int32).view(dtype)
     check_equal(B, x.clone(), False, "blocks of equal keys")
     check_equal(B, x.clone(), True, "blocks of equal keys desc")
+
+
+@pytest.mark.parametrize("env", [{"BSORT_P2": "0"}, {"BSORT_P2": "0", "BSORT_WS": "0"}, {"BSORT_WS": "0"}])
+def test_round1_fallback_kernels_at_joint_sizes(env):
+    """The kernels that run where k_pass2 cannot (BSORT_P2=0: what a device that fails the
+    lane-order self-test gets) and where the warp-specialised kernel cannot (BSORT_WS=0, or a caller
+    pointer that is not 16-byte aligned) -- k_onesweep_pass with 8,192-key look-back tiles -- on a
+    32-bit joint-histogram sort, whose three look-back regions are sized for larger tiles
+    (lsd_impl.cuh: they then serve as one region).  The switches are read once per process."""
+    import os
+    import subprocess
+    import sys
+    repo = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    code = r"""
+import sys; sys.path.insert(0, %r)
+import numpy as np, torch, oracle, workloads as W, paper_2603_08929_b200 as B
+n = (1 << 24) + 777
+for dt, off in ((torch.float32, 1), (torch.float32, 0), (torch.int32, 3)):
+    base = W.special_mix(dt, n + 4, 77, "cuda") if dt.is_floating_point else W.uniform_int(dt, n + 4, 77, "cuda")
+    for desc in (False, True):
+        x = base.clone()[off:off + n]
+        assert (x.data_ptr() %% 16 != 0) == (off != 0)
+        ref = oracle.sort_native(x.cpu().numpy(), descending=desc)
+        B.sort_(x, descending=desc); torch.cuda.synchronize()
+        assert x.cpu().numpy().tobytes() == ref.tobytes(), (dt, off, desc)
+print("ok")
+""" % repo
+    r = subprocess.run([sys.executable, "-c", code], env=dict(os.environ, **env), capture_output=True, text=True,
+                       timeout=900, cwd=repo)
+    assert r.returncode == 0 and "ok" in r.stdout, (r.stdout[-500:], r.stderr[-2000:])
