@@ -350,19 +350,12 @@ __global__ void __launch_bounds__(RT + 256, MINB)
       gofs[w] = bases[w] + excl - m.x;
       named_bar_sync(WS_BAR_W, 256);
       const uint32_t valid = tile_valid(tile);
-      auto write_item = [&](uint32_t i) {
+#pragma unroll 4
+      for (uint32_t i = w; i < valid; i += 256) {
         const U x = buf[i];
         const unsigned long long o = gofs[digit(x)] + i;
         dst[o] = x;
         if constexpr (KV) vdst[o] = vbuf[i];
-      };
-      if (valid == (uint32_t)TILE) {  // fixed trip count: loads of several items in flight
-        static_assert(TILE % 256 == 0, "writers take whole rounds of a full tile");
-#pragma unroll 4
-        for (uint32_t k = 0; k < (uint32_t)TILE / 256u; ++k) write_item(w + 256u * k);
-      } else {
-#pragma unroll 4
-        for (uint32_t i = w; i < valid; i += 256) write_item(i);
       }
       named_bar_sync(WS_BAR_W, 256);  // buffer and gofs fully read
       if (w == 0) refill((int)slot);
